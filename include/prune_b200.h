@@ -1,0 +1,309 @@
+/*
+ * prune_b200.h — C-ABI of the B200 execution path for PRUNE data-parallel actors.
+ *
+ * Plain pointers and sizes only (no torch / no C++ types).  Every entry point
+ * returns an int status: PB_OK (0) or a negative PB_E_* code; pb_last_error()
+ * returns the text of the last failure on the calling thread.  Device memory
+ * referenced by the descriptor structs below is owned by the caller of the
+ * pb_fire_* entry points (normally the Python engine, through pb_malloc);
+ * rings own their storage.  Host buffers are always owned by the caller.
+ *
+ * Reference interfaces each group replaces (paths relative to the reference
+ * root, /root/reference):
+ *   - FIFO channel engine ........ pkg/src/tokenflow/fifos.py:49-338
+ *       (CapacityPlan/layout_plan :49-98, writer_gate/reader_gate/copy_gate
+ *        :106-139, FifoChannel :142-338, errors InvalidParams/ProtocolError/
+ *        EndOfStream/Poisoned :25-46)
+ *   - per-firing rate gating ..... pkg/src/tokenflow/runtime.py:107-116 (Eq. 1),
+ *       Eq. 1 recheck :195-220, oracle twin interp.py:126-148,
+ *       decode_control behavior.py:34-38
+ *   - actor firings .............. FirBranch.fire apps/predistortion.py:41-65,
+ *       BranchSum.fire :68-83, Route.fire behavior.py:176-184,
+ *       Passthrough :158-165, AddMod :168-173, Merge :187-199,
+ *       MatMul.fire apps/bypass.py:36-49, PathMerge.fire :52-66
+ *   - host configuration actors .. _PolicyBase/FixedPolicy/AlternatePolicy/
+ *       SeededPolicy/SubsetPolicy behavior.py:202-256 (CPython `random`)
+ *
+ * Error codes map onto the reference exception types (fifos.py:25-46,
+ * runtime.py:26-48): PB_E_INVALID -> InvalidParams/ValueError,
+ * PB_E_PROTOCOL -> ProtocolError, PB_E_EOS -> EndOfStream,
+ * PB_E_POISONED -> Poisoned, PB_E_CUDA / PB_E_ACTOR -> ActorPanic.
+ */
+#ifndef PRUNE_B200_H
+#define PRUNE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PB_ABI_VERSION 1
+
+enum {
+  PB_OK = 0,
+  PB_E_INVALID = -1,     /* InvalidParams / ValueError */
+  PB_E_PROTOCOL = -2,    /* ProtocolError (span protocol misuse, ring overflow) */
+  PB_E_EOS = -3,         /* EndOfStream */
+  PB_E_POISONED = -4,    /* Poisoned */
+  PB_E_CUDA = -5,        /* device runtime failure */
+  PB_E_NOMEM = -6,       /* allocation failure */
+  PB_E_UNSUPPORTED = -7, /* shape the kernels do not cover */
+  PB_E_ACTOR = -8        /* an actor firing reported a failure (ActorPanic) */
+};
+
+#define PB_TAPS 10          /* FIR taps, predistortion.py:24 (TAPS) */
+#define PB_MAX_BRANCHES 32  /* branches one fused filter-bank launch covers */
+#define PB_MAX_PORTS 16     /* data ports of one actor in the byte kernels */
+
+/* ------------------------------------------------------------------ runtime */
+int pb_abi_version(void);
+const char* pb_last_error(void);
+int pb_device_count(int* n);
+int pb_set_device(int device);
+int pb_device_sync(void);
+int pb_sm_count(int* n);
+int pb_malloc(void** dptr, size_t bytes);
+int pb_free(void* dptr);
+int pb_host_alloc(void** hptr, size_t bytes); /* page-locked host memory */
+int pb_host_free(void* hptr);
+int pb_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+int pb_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
+int pb_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
+int pb_memset(void* dst, int value, size_t bytes, void* stream);
+/* pitched copies: height rows of width bytes; kind 1 = H2D, 2 = D2H, 3 = D2D */
+int pb_memcpy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                 size_t height, int kind, void* stream);
+int pb_stream_create(void** stream);
+int pb_stream_destroy(void* stream);
+int pb_stream_sync(void* stream);
+int pb_event_create(void** event);
+int pb_event_destroy(void* event);
+int pb_event_record(void* event, void* stream);
+int pb_event_elapsed_ms(void* start, void* end, float* ms);
+/* Number of device kernels this library has launched (process lifetime). */
+int64_t pb_launch_count(void);
+
+/* --------------------------------------------- capacity plan (fifos.py:49-139) */
+typedef struct {
+  int32_t rate, token_bytes, delay, factor;
+  int32_t aligned; /* 1 when delay % rate == 0 */
+  int32_t pad_;
+  int64_t slots;   /* token slots */
+  int64_t nbytes;  /* slots * token_bytes */
+  int64_t copy_src, copy_dst, copy_count; /* wrap copy (unaligned), else -1 */
+} pb_plan;
+
+/* layout_plan, fifos.py:87-98 */
+int pb_layout_plan(int rate, int delay, int factor, int token_bytes, pb_plan* out);
+/* writer_gate fifos.py:106-121, reader_gate :124-127, copy_gate :130-139 */
+int64_t pb_writer_gate(int64_t w, int rate, int delay, int factor, int aligned);
+int64_t pb_reader_gate(int64_t i, int rate, int delay);
+int64_t pb_copy_gate(int64_t n, int rate, int delay, int factor);
+
+/* ------------------------------------- device rings (FifoChannel, fifos.py:142) */
+/* One ring per FIFO, replicated over n_streams independent streams.  Storage
+ * and the per-stream counters (chunk writes, chunk reads, max occupancy in
+ * tokens, wrap copies done) live in HBM; kernels address spans through pb_span_ref. */
+typedef struct pb_ring pb_ring;
+int pb_ring_create(int rate, int token_bytes, int delay, int factor, int n_streams,
+                   const void* delay_payload, pb_ring** out);
+int pb_ring_destroy(pb_ring* ring);
+int pb_ring_plan(const pb_ring* ring, pb_plan* out);
+int pb_ring_storage(const pb_ring* ring, void** data, int64_t* stream_stride,
+                    int64_t** counters /* device int64[4][n_streams] */);
+/* write n_chunks spans (rate tokens each) from host memory; PB_E_PROTOCOL if
+ * the writer gate (fifos.py:106) would block, PB_E_PROTOCOL after close. */
+int pb_ring_push_host(pb_ring* ring, int stream, const void* src, int64_t n_chunks,
+                      void* cuda_stream);
+/* read n_chunks spans into host memory; PB_E_EOS when closed and short,
+ * PB_E_PROTOCOL when open and short (the reference would block). */
+int pb_ring_pop_host(pb_ring* ring, int stream, void* dst, int64_t n_chunks,
+                     void* cuda_stream);
+int pb_ring_counters(const pb_ring* ring, int stream, int64_t* writes, int64_t* reads,
+                     int64_t* max_occupancy);
+int pb_ring_close(pb_ring* ring);
+int pb_ring_poison(pb_ring* ring, const char* reason);
+
+/* ------------------------------------------ epoch resolution (Eq. 1 on device) */
+/* A condition is one (control output port, element) pair of the control
+ * table (model.py:137-163).  Its control tokens for the epoch are resident in
+ * HBM: token of iteration n of stream s at
+ *   tokens + s*stream_stride + ((base + n) % slots) * token_stride. */
+typedef struct {
+  const uint8_t* tokens;
+  int64_t stream_stride;
+  int32_t token_stride; /* FIFO token_bytes of the control channel */
+  int32_t element;      /* 0-based: T[p] - 1 */
+  int32_t slots;        /* ring chunk positions of the control channel */
+  int32_t base;         /* chunk index of iteration 0 */
+} pb_condition;
+
+/* Device-resident resolution of one epoch: per condition c and stream s,
+ * act[c][s][n] (0/1), prefix[c][s][n] (exclusive count of active iterations
+ * before n), count[c][s] and worklist[c][s][j] (iteration of the j-th active
+ * firing).  Strides: act/prefix/worklist use cap per (c, s) row. */
+typedef struct {
+  uint8_t* act;
+  int32_t* prefix;
+  int32_t* count;
+  int32_t* worklist;
+  int32_t n_cond, n_streams, n_iter, cap;
+} pb_resolved;
+
+/* Decode control tokens into per-iteration activity (decode_control,
+ * behavior.py:34-38; Eq. 1 runtime.py:107-116) and compact the firings. */
+int pb_resolve(const pb_condition* conds /* host array [n_cond] */, pb_resolved res,
+               void* stream);
+
+/* Eq. 1 recheck (runtime.py:195-220): for each DRP, the rate implied by the
+ * dynamic actor's own control token must equal the span the engine moved.
+ * counters: device int64[2] {checks, failures}, accumulated. */
+typedef struct {
+  int32_t own_cond;   /* condition decoded from the actor's control channel */
+  int32_t moved_cond; /* condition that gated the FIFO attached to the DRP */
+  int32_t actor_cond; /* condition of the dynamic actor itself (-1: always) */
+  int32_t pad_;
+} pb_eq1_port;
+int pb_eq1_check(const pb_eq1_port* ports /* host array */, int n_ports, pb_resolved res,
+                 int64_t* counters, void* stream);
+
+/* Advance ring counters after an epoch (write_end/read_end in bulk).  For
+ * ring r: writes += rate_chunks * tokens_in_epoch, reads likewise, and the
+ * max occupancy (fifos.py:177-181,256) is updated. */
+typedef struct {
+  int64_t* counters;  /* ring counters, device int64[4][n_streams] */
+  int32_t cond;       /* condition gating the FIFO (-1 always) */
+  int32_t rate;       /* tokens per chunk */
+  int32_t delay;
+  int32_t pad_;
+} pb_ring_advance_t;
+int pb_rings_advance(const pb_ring_advance_t* rings /* host array */, int n_rings,
+                     pb_resolved res, void* stream);
+
+/* --------------------------------------------------------- span addressing */
+/* Where the span of a port lives for firing at iteration n of stream s:
+ *   idx   = index_cond < 0 ? n : prefix[index_cond][s][n]
+ *   chunk = (base[s] + idx) % slots     (base NULL -> 0)
+ *   ptr   = data + s*stream_stride + chunk*span_bytes
+ * act_cond is the condition gating the port (-1: always active). */
+typedef struct {
+  uint8_t* data;
+  int64_t stream_stride;
+  int64_t span_bytes;
+  const int64_t* base;
+  int32_t slots;
+  int32_t index_cond;
+  int32_t act_cond;
+  int32_t pad_;
+} pb_span_ref;
+
+/* ------------------------------------------------------------- actor kernels */
+/* fir_branch (predistortion.py:41-65): planar complex fp32 span
+ * [re[B], im[B]], 10-tap complex FIR in ascending tap order, every product
+ * and sum rounded separately (no FMA), accumulator from +0.  History = last
+ * 9 input samples of the actor's previous firing (state[s] at the first
+ * firing of an epoch). */
+typedef struct {
+  pb_span_ref in;
+  pb_span_ref out;
+  const float* taps;  /* device [2][PB_TAPS]: re then im */
+  float* state;       /* device [n_streams][2][PB_TAPS-1] */
+  int32_t cond;       /* actor activity condition (-1 always) */
+  int32_t pad_;
+} pb_fir_actor;
+
+/* All firings of n_actors fir_branch actors in one launch.  actors is a
+ * DEVICE array. */
+int pb_fire_fir(const pb_fir_actor* actors, int n_actors, pb_resolved res, int64_t block,
+                void* stream);
+/* History carry after pb_fire_fir / pb_fire_filter_bank: state[s] <- last 9
+ * input samples of the epoch's last firing (if any). */
+int pb_fir_carry(const pb_fir_actor* actors, int n_actors, pb_resolved res, int64_t block,
+                 void* stream);
+
+/* Fused dynamic region route -> K x fir_branch -> branch_sum
+ * (behavior.py:176-184, predistortion.py:41-83): one pass over each input
+ * span, branch outputs summed from +0 in the combiner's sorted port order
+ * (predistortion.py:75) without materialising the branch channels. */
+typedef struct {
+  pb_span_ref in;                    /* route input */
+  pb_span_ref out;                   /* combiner output */
+  const pb_fir_actor* branches;      /* device array, combiner sorted port order */
+  int32_t n_branches;
+  int32_t actor_cond;                /* condition of route/combiner (-1) */
+} pb_filter_bank;
+int pb_fire_filter_bank(pb_filter_bank bank, pb_resolved res, int64_t block, void* stream);
+
+/* branch_sum (predistortion.py:68-83): ins in sorted port-id order. */
+typedef struct {
+  pb_span_ref in[PB_MAX_PORTS];
+  pb_span_ref out;
+  int32_t n_in;
+  int32_t cond;
+} pb_sum_actor;
+int pb_fire_branch_sum(pb_sum_actor actor, pb_resolved res, int64_t block, void* stream);
+
+/* Byte actors: out[k] = (sum of active inputs + offset) mod 256 for every
+ * active output — covers route (behavior.py:176-184, used when not
+ * aliased), passthrough (:158-165), add_mod (:168-173) and merge (:187-199). */
+typedef struct {
+  pb_span_ref in[PB_MAX_PORTS];
+  pb_span_ref out[PB_MAX_PORTS];
+  int32_t n_in, n_out;
+  int32_t offset;
+  int32_t cond;
+} pb_bytes_actor;
+int pb_fire_bytes(pb_bytes_actor actor, pb_resolved res, void* stream);
+
+/* matmul (bypass.py:36-49): out = W @ x, N x N fp32, ascending k, separate
+ * mul/add roundings.  N = 8 in the reference. */
+typedef struct {
+  pb_span_ref in;
+  pb_span_ref out;
+  const float* weights; /* device [N][N] row-major */
+  int32_t n;
+  int32_t cond;
+} pb_matmul_actor;
+int pb_fire_matmul(pb_matmul_actor actor, pb_resolved res, void* stream);
+
+/* path_merge (bypass.py:52-66): exactly one live input is forwarded; the
+ * marker is added when it is the bypass port.  A firing with != 1 live input
+ * sets *error_flag (device int32) -> ActorPanic. */
+typedef struct {
+  pb_span_ref in[PB_MAX_PORTS];
+  pb_span_ref out;
+  int32_t n_in;
+  int32_t bypass_index; /* index into in[] of the bypass port, -1 none */
+  float marker;
+  int32_t cond;
+  int32_t* error_flag;
+} pb_path_merge_actor;
+int pb_fire_path_merge(pb_path_merge_actor actor, pb_resolved res, void* stream);
+
+/* ------------------------------------------ host configuration actors (native) */
+/* Control tokens of _PolicyBase.fire (behavior.py:212-218) with CPython's
+ * Mersenne Twister (random.Random(seed)) reproduced bit for bit:
+ * kind 0 fixed_policy(element), 1 alternate_policy, 2 seeded_policy,
+ * 3 subset_policy(min_active).  Writes n_firings tokens of token_bytes
+ * (values zero-padded) starting at firing `first`; the generator state is
+ * kept in *state (opaque, PB_POLICY_STATE_BYTES) so successive epochs continue
+ * the same sequence.  pb_policy_init seeds it (seed < 0 -> None -> 0). */
+#define PB_POLICY_STATE_BYTES 2560
+int pb_policy_init(void* state, int64_t seed);
+int pb_policy_tokens(void* state, int kind, int length, int param, int64_t first,
+                     int64_t n_firings, uint8_t* out, int token_bytes);
+/* Seeding many streams at once: states is n_streams * PB_POLICY_STATE_BYTES,
+ * seeds[n_streams]; tokens out[s][n_firings][token_bytes]; threads <= 0 ->
+ * hardware concurrency. */
+int pb_policy_tokens_streams(void* states, int n_streams, int kind, int length, int param,
+                             int64_t first, int64_t n_firings, uint8_t* out, int token_bytes,
+                             int threads);
+/* zlib.crc32 as used by actor_seed (behavior.py:17-21). */
+uint32_t pb_crc32(const uint8_t* data, size_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRUNE_B200_H */

@@ -1,0 +1,161 @@
+// Batched firings of the remaining data-parallel actors:
+//   branch_sum  apps/predistortion.py:68-83
+//   route / passthrough / add_mod / merge   behavior.py:158-199
+//   matmul      apps/bypass.py:36-49
+//   path_merge  apps/bypass.py:52-66
+// One CTA covers one (stream, iteration) firing (or a tile of its span).
+#include <algorithm>
+
+#include "pb_common.cuh"
+
+namespace {
+
+constexpr int kSumThreads = 256;
+
+// BranchSum.fire: acc = +0; for pid in sorted(inputs): if span: acc = acc + x.
+__global__ void __launch_bounds__(kSumThreads)
+branch_sum_kernel(pb_sum_actor a, pb_resolved res, int64_t B, int tiles) {
+  const int s = blockIdx.y;
+  const int n = blockIdx.x / tiles;
+  const int tile = blockIdx.x % tiles;
+  if (!pb::active(res, a.cond, s, n)) return;
+  const int64_t n4 = (2 * B) / 4;  // both planes, float4 units
+  const int64_t k = (int64_t)tile * kSumThreads + threadIdx.x;
+  if (k >= n4) return;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int p = 0; p < a.n_in; ++p) {
+    const pb_span_ref& r = a.in[p];
+    if (!pb::active(res, r.act_cond, s, n)) continue;
+    const float4 x = __ldg(reinterpret_cast<const float4*>(pb::span_ptr(r, res, s, n)) + k);
+    acc.x = __fadd_rn(acc.x, x.x);
+    acc.y = __fadd_rn(acc.y, x.y);
+    acc.z = __fadd_rn(acc.z, x.z);
+    acc.w = __fadd_rn(acc.w, x.w);
+  }
+  reinterpret_cast<float4*>(pb::span_ptr(a.out, res, s, n))[k] = acc;
+}
+
+// Byte actors: out = (sum of active inputs + offset) mod 256 on every active
+// output span.  Route/passthrough (one input, offset 0) reduce to a copy;
+// merge with one live input is a copy and otherwise the bytewise sum.
+__global__ void bytes_kernel(pb_bytes_actor a, pb_resolved res) {
+  const int s = blockIdx.y;
+  const int n = blockIdx.x;
+  if (!pb::active(res, a.cond, s, n)) return;
+  const uint8_t* ins[PB_MAX_PORTS];
+  int64_t len = 0;
+  int n_live = 0;
+  for (int p = 0; p < a.n_in; ++p) {
+    if (!pb::active(res, a.in[p].act_cond, s, n)) continue;
+    ins[n_live++] = pb::span_ptr(a.in[p], res, s, n);
+    len = a.in[p].span_bytes;
+  }
+  for (int o = 0; o < a.n_out; ++o) {
+    const pb_span_ref& r = a.out[o];
+    if (!pb::active(res, r.act_cond, s, n)) continue;
+    uint8_t* dst = pb::span_ptr(r, res, s, n);
+    for (int64_t b = threadIdx.x; b < r.span_bytes; b += blockDim.x) {
+      unsigned v = (unsigned)a.offset;
+      for (int p = 0; p < n_live; ++p) v += b < len ? ins[p][b] : 0u;
+      dst[b] = (uint8_t)(v & 0xFFu);
+    }
+  }
+}
+
+// MatMul.fire: acc = 0; for k: acc = acc + outer(w[:, k], x[k, :]).
+// One thread per output element, one CTA per batch of firings.
+__global__ void matmul_kernel(pb_matmul_actor a, pb_resolved res, int per_cta) {
+  const int s = blockIdx.y;
+  const int N = a.n;
+  const int NN = N * N;
+  extern __shared__ float smem[];
+  float* w = smem;  // [N][N]
+  for (int e = threadIdx.x; e < NN; e += blockDim.x) w[e] = a.weights[e];
+  __syncthreads();
+  const int slot = threadIdx.x / NN;
+  const int e = threadIdx.x % NN;
+  const int i = e / N, jj = e % N;
+  const int cnt = pb::cond_count(res, a.cond, s);
+  const int j = blockIdx.x * per_cta + slot;
+  if (slot >= per_cta || j >= cnt) return;
+  const int n = pb::firing_iter(res, a.cond, s, j);
+  const float* x = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n));
+  float acc = 0.0f;
+  for (int k = 0; k < N; ++k) acc = __fadd_rn(acc, __fmul_rn(w[i * N + k], __ldg(x + k * N + jj)));
+  reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n))[e] = acc;
+}
+
+// PathMerge.fire: (pid, span), = live; x + marker if pid is the bypass port.
+__global__ void path_merge_kernel(pb_path_merge_actor a, pb_resolved res) {
+  const int s = blockIdx.y;
+  const int n = blockIdx.x;
+  if (!pb::active(res, a.cond, s, n)) return;
+  int live = -1, n_live = 0;
+  for (int p = 0; p < a.n_in; ++p)
+    if (pb::active(res, a.in[p].act_cond, s, n)) {
+      live = p;
+      ++n_live;
+    }
+  if (n_live != 1) {
+    if (threadIdx.x == 0) atomicExch(a.error_flag, 1);
+    return;
+  }
+  const float* x = reinterpret_cast<const float*>(pb::span_ptr(a.in[live], res, s, n));
+  float* out = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
+  const int64_t len = a.out.span_bytes / 4;
+  const bool add = live == a.bypass_index;
+  for (int64_t k = threadIdx.x; k < len; k += blockDim.x) {
+    float v = x[k];
+    out[k] = add ? __fadd_rn(v, a.marker) : v;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int pb_fire_branch_sum(pb_sum_actor actor, pb_resolved res, int64_t block, void* stream) {
+  if (res.n_iter == 0) return PB_OK;
+  if (actor.n_in < 0 || actor.n_in > PB_MAX_PORTS)
+    return pb::fail(PB_E_INVALID, "branch_sum: bad input count");
+  if ((2 * block) % 4 != 0) return pb::fail(PB_E_UNSUPPORTED, "branch_sum: block must be even");
+  const int64_t n4 = 2 * block / 4;
+  const int tiles = (int)((n4 + kSumThreads - 1) / kSumThreads);
+  dim3 grid((unsigned)(tiles * res.n_iter), res.n_streams);
+  branch_sum_kernel<<<grid, kSumThreads, 0, pb::as_stream(stream)>>>(actor, res, block, tiles);
+  PB_LAUNCHED("branch_sum_kernel");
+  return PB_OK;
+}
+
+int pb_fire_bytes(pb_bytes_actor actor, pb_resolved res, void* stream) {
+  if (res.n_iter == 0) return PB_OK;
+  if (actor.n_in > PB_MAX_PORTS || actor.n_out > PB_MAX_PORTS)
+    return pb::fail(PB_E_INVALID, "byte actor: too many ports");
+  dim3 grid(res.n_iter, res.n_streams);
+  bytes_kernel<<<grid, 128, 0, pb::as_stream(stream)>>>(actor, res);
+  PB_LAUNCHED("bytes_kernel");
+  return PB_OK;
+}
+
+int pb_fire_matmul(pb_matmul_actor actor, pb_resolved res, void* stream) {
+  if (res.n_iter == 0) return PB_OK;
+  const int NN = actor.n * actor.n;
+  if (actor.n < 1 || NN > 1024) return pb::fail(PB_E_UNSUPPORTED, "matmul: N*N must be <= 1024");
+  const int per_cta = std::max(1, 256 / NN);
+  dim3 grid((unsigned)((res.n_iter + per_cta - 1) / per_cta), res.n_streams);
+  matmul_kernel<<<grid, per_cta * NN, NN * sizeof(float), pb::as_stream(stream)>>>(actor, res,
+                                                                                   per_cta);
+  PB_LAUNCHED("matmul_kernel");
+  return PB_OK;
+}
+
+int pb_fire_path_merge(pb_path_merge_actor actor, pb_resolved res, void* stream) {
+  if (res.n_iter == 0) return PB_OK;
+  if (actor.n_in > PB_MAX_PORTS) return pb::fail(PB_E_INVALID, "path_merge: too many ports");
+  dim3 grid(res.n_iter, res.n_streams);
+  path_merge_kernel<<<grid, 128, 0, pb::as_stream(stream)>>>(actor, res);
+  PB_LAUNCHED("path_merge_kernel");
+  return PB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,904 @@
+"""Device executor: the B200 replacement for tokenflow.runtime.run.
+
+Same entry points and report as the threaded reference engine
+(runtime.py:51-74 RuntimeConfig/RunReport, :327-347 instantiate/run), plus
+`run_streams` for a batch of independent replicas of one graph (the unit the
+B200 shards over).  Execution is epoch-batched instead of one thread per
+actor (runtime.py:118-193):
+
+  per epoch of E iterations (E <= RuntimeConfig.epoch) for all streams:
+    1. host sources stage E spans per stream -> one pinned H2D per port
+    2. host configuration actors emit E control tokens per stream (native
+       CPython-compatible generator, csrc/pb_policy.cpp) -> one H2D
+    3. pb_resolve: control tokens -> per-condition activity / prefix /
+       firing lists on the device (Eq. 1, runtime.py:107-116)
+    4. pb_eq1_check: the recheck of runtime.py:195-220
+    5. every device actor fires ALL its firings of the epoch in one launch,
+       in topological order (route aliases, fused filter banks, FIR groups)
+    6. pb_rings_advance: ring counters / peak occupancy in bulk
+    7. sinks: D2H of the epoch's sink spans, SHA-256 per firing in sorted
+       port order (runtime.py:175-180), optional capture
+
+FIFO channels are device rings of C = max(c_factor, epoch) chunks; a
+channel's per-epoch tokens never exceed E <= C, so occupancy stays <= beta.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+from typing import Callable, Mapping, Sequence
+
+import numpy as np
+
+from . import _lib
+from .behaviors import (ActorBehavior, FileSource, FireContext, actor_seed, native_policy_kind,
+                        resolve)
+from .errors import ActorPanic, DeviceUnavailable, Timeout, UnsupportedGraph
+from .graph import CONTROL_OUT, DRP, Graph, PortRef, as_graph
+from .plan import ALWAYS, ExecPlan, admit, find_filter_banks, is_device
+
+
+@dataclass
+class RuntimeConfig:
+    """runtime.py:51-61, plus the device executor's knobs."""
+
+    source_firings: int = 1
+    c_factor: int = 3
+    seed: int | None = None
+    jitter_ms: float = 0.0        # accepted; the batched schedule is deterministic
+    jitter_seed: int | None = None
+    pin_cores: bool = False       # accepted; host work is a few bulk calls
+    capture_sinks: bool = False
+    timeout_ms: float | None = None
+    trace: Callable[[str], None] | None = None
+    # device executor
+    epoch: int = 4096             # iterations fired per batched epoch
+    fuse: bool = True             # fire route -> fir_branch* -> branch_sum as one kernel
+    device: int = 0
+    host_threads: int = 0         # threads for native policies and digests (0 = all)
+
+
+@dataclass
+class RunReport:
+    """runtime.py:64-74."""
+
+    sink_digests: dict[str, str] = field(default_factory=dict)
+    sink_data: dict[str, bytes] = field(default_factory=dict)
+    firing_counts: dict[str, int] = field(default_factory=dict)
+    max_occupancy: dict[str, int] = field(default_factory=dict)
+    slots: dict[str, int] = field(default_factory=dict)
+    beta: dict[str, int] = field(default_factory=dict)
+    eq1_checks: int = 0
+    eq1_failures: int = 0
+    wall_ms: float = 0.0
+
+
+class _Dev:
+    """Small RAII helper for device / pinned allocations."""
+
+    def __init__(self):
+        self.lib = _lib.load()
+        self.dev: list[int] = []
+        self.host: list[int] = []
+        self.rings: list[int] = []
+
+    def malloc(self, nbytes: int, zero: bool = True) -> int:
+        p = C.c_void_p()
+        _lib.check(self.lib.pb_malloc(C.byref(p), max(16, int(nbytes))), "pb_malloc")
+        self.dev.append(p.value)
+        if zero:
+            _lib.check(self.lib.pb_memset(p, 0, max(16, int(nbytes)), None), "pb_memset")
+        return p.value
+
+    def pinned(self, nbytes: int) -> tuple[int, np.ndarray]:
+        p = C.c_void_p()
+        _lib.check(self.lib.pb_host_alloc(C.byref(p), max(16, int(nbytes))), "pb_host_alloc")
+        self.host.append(p.value)
+        arr = np.ctypeslib.as_array((C.c_uint8 * max(16, int(nbytes))).from_address(p.value))
+        return p.value, arr[:int(nbytes)]
+
+    def ring(self, rate: int, tb: int, factor: int, n_streams: int):
+        r = C.c_void_p()
+        _lib.check(self.lib.pb_ring_create(rate, tb, 0, factor, n_streams, None, C.byref(r)),
+                   "pb_ring_create")
+        self.rings.append(r.value)
+        data, stride, ctr = C.c_void_p(), C.c_int64(), C.c_void_p()
+        _lib.check(self.lib.pb_ring_storage(r, C.byref(data), C.byref(stride), C.byref(ctr)))
+        return r.value, data.value, stride.value, ctr.value
+
+    def upload(self, arr: np.ndarray) -> int:
+        arr = np.ascontiguousarray(arr)
+        p = self.malloc(arr.nbytes, zero=False)
+        _lib.check(self.lib.pb_memcpy_h2d(p, arr.ctypes.data, arr.nbytes, None), "pb_memcpy_h2d")
+        return p
+
+    def close(self):
+        lib = self.lib
+        lib.pb_device_sync()
+        for r in self.rings:
+            lib.pb_ring_destroy(r)
+        for p in self.dev:
+            lib.pb_free(p)
+        for p in self.host:
+            lib.pb_host_free(p)
+        self.rings, self.dev, self.host = [], [], []
+
+
+@dataclass
+class _Storage:
+    """Where a FIFO's spans live (its own ring or an alias of another's)."""
+
+    data: int
+    stream_stride: int
+    span: int
+    slots: int
+    base: int          # device int64* (the owner's writes counter row)
+    index_cond: int
+    owner: str
+
+
+def _behaviors_for(plan: ExecPlan, overrides, n_streams: int) -> list[dict[str, ActorBehavior]]:
+    """One behaviour instance per (stream, actor), as the reference creates one
+    per actor (runtime.py:336-341).  An override may be a single object (one
+    stream), a sequence with one object per stream, or a zero-arg factory."""
+    out = []
+    for s in range(n_streams):
+        d = {}
+        for a in plan.graph.actors:
+            ov = overrides.get(a.id) if overrides else None
+            if ov is None:
+                d[a.id] = resolve(a.behavior)
+            elif isinstance(ov, (list, tuple)):
+                d[a.id] = ov[s]
+            elif isinstance(ov, type) or (callable(ov) and not hasattr(ov, "fire")):
+                d[a.id] = ov()
+            else:
+                if n_streams > 1 and not is_device(ov):
+                    raise ValueError(f"behaviour override for {a.id} must be a factory or a "
+                                     "per-stream sequence when running several streams")
+                d[a.id] = ov
+        out.append(d)
+    return out
+
+
+class DeviceRuntime:
+    """An admitted graph bound to device rings for `n_streams` replicas."""
+
+    def __init__(self, graph, behaviors: Mapping | None = None,
+                 config: RuntimeConfig | None = None, n_streams: int = 1,
+                 seeds: Sequence[int | None] | None = None,
+                 sources: Mapping[str, Sequence] | None = None):
+        self.config = config = config or RuntimeConfig()
+        self.graph: Graph = as_graph(graph)
+        self.n_streams = S = int(n_streams)
+        self.epoch = max(1, min(int(config.epoch), max(1, int(config.source_firings))))
+        self.C = max(int(config.c_factor), self.epoch, 2)
+        self.plan = admit(self.graph, self.C)
+        self.analysis = self.plan.admission
+        self.seeds = list(seeds) if seeds is not None else [config.seed] * S
+        if len(self.seeds) != S:
+            raise ValueError("one seed per stream expected")
+        self.sources = dict(sources or {})
+        self.behaviors = _behaviors_for(self.plan, behaviors, S)
+        g, plan = self.graph, self.plan
+        lib = _lib.load()
+        if _lib.device_count() < 1:
+            raise DeviceUnavailable("no CUDA device visible; the B200 executor has no CPU "
+                                    "fallback")
+        _lib.check(lib.pb_set_device(int(config.device)), "pb_set_device")
+        self.lib = lib
+        self.mem = _Dev()
+        st = C.c_void_p()
+        _lib.check(lib.pb_stream_create(C.byref(st)), "pb_stream_create")
+        self.stream = st.value
+
+        # device behaviours must be device kernels
+        for a in g.actors:
+            role = plan.roles[a.id]
+            b = self.behaviors[0][a.id]
+            if role in ("device", "dynamic") and not is_device(b):
+                raise UnsupportedGraph(
+                    f"actor {a.id} ({role}) has host behaviour {type(b).__name__}; the device "
+                    "executor fires only device behaviours between sources and sinks")
+            if role in ("source", "config", "sink") and is_device(b):
+                raise UnsupportedGraph(f"actor {a.id} ({role}) needs a host behaviour")
+
+        self.banks = find_filter_banks(plan, self.behaviors[0]) if config.fuse else []
+        self.fused_actors = {a for grp in self.banks for a in [grp.router, *grp.branches]}
+        self.virtual = {fid for grp in self.banks for fid in grp.internal_fifos}
+        self._allocate()
+        self._build_launches()
+        self.launches_per_epoch = 0
+
+    # ------------------------------------------------------------- allocation
+
+    def _allocate(self):
+        g, plan, S, C_ = self.graph, self.plan, self.n_streams, self.C
+        m = self.mem
+        n_cond = max(1, len(plan.conds))
+        cap = self.epoch
+        self.res_act = m.malloc(n_cond * S * cap)
+        self.res_prefix = m.malloc(4 * n_cond * S * cap)
+        self.res_count = m.malloc(4 * n_cond * S)
+        self.res_wl = m.malloc(4 * n_cond * S * cap)
+        self.eq1_ctr = m.malloc(16)
+        self.err_flag = m.malloc(16)
+        self.cap = cap
+
+        self.counters: dict[str, int] = {}
+        self.storage: dict[str, _Storage] = {}
+        route_alias: dict[str, str] = {}
+        for a in g.actors:
+            b = self.behaviors[0][a.id]
+            if getattr(b, "kernel", "") == "route" and a.id not in self.fused_actors:
+                (pin,) = a.data_inputs
+                src = g.fifo_into(PortRef(a.id, pin.id))
+                span = src.rate * src.token_bytes
+                for p in a.output_ports:
+                    for f in g.fifos_from(PortRef(a.id, p.id)):
+                        if f.rate * f.token_bytes == span:
+                            route_alias[f.id] = src.id
+        # storage owners first (topological order keeps owners ahead of aliases)
+        for aid in plan.order:
+            a = g.actor(aid)
+            for p in sorted(a.output_ports, key=lambda p: p.id):
+                if p.kind == CONTROL_OUT:
+                    continue
+                fifos = sorted(g.fifos_from(PortRef(aid, p.id)), key=lambda f: f.id)
+                first = None
+                for f in fifos:
+                    span = f.rate * f.token_bytes
+                    if f.id in self.virtual:
+                        self.counters[f.id] = m.malloc(8 * 4 * S)
+                        continue
+                    if f.id in route_alias:
+                        o = self.storage[route_alias[f.id]]
+                        self.storage[f.id] = o
+                        self.counters[f.id] = m.malloc(8 * 4 * S)
+                        continue
+                    if first is not None and first.span == span:
+                        self.storage[f.id] = first
+                        self.counters[f.id] = m.malloc(8 * 4 * S)
+                        continue
+                    _, data, stride, ctr = m.ring(f.rate, f.token_bytes, C_, S)
+                    self.counters[f.id] = ctr
+                    st = _Storage(data, stride, span, C_, ctr, plan.fifo_cond[f.id], f.id)
+                    self.storage[f.id] = st
+                    if first is None:
+                        first = st
+        # control tokens: one device array per control output port
+        self.ctl_ports: list[PortRef] = []
+        self.ctl_dev: dict[PortRef, int] = {}
+        self.ctl_stride: dict[PortRef, int] = {}
+        self.ctl_host: dict[PortRef, tuple[int, np.ndarray]] = {}
+        self.policy_state: dict[PortRef, C.Array] = {}
+        for a in g.actors:
+            for p in a.output_ports:
+                if p.kind != CONTROL_OUT:
+                    continue
+                ref = PortRef(a.id, p.id)
+                fifos = g.fifos_from(ref)
+                stride = max(f.token_bytes for f in fifos)
+                self.ctl_ports.append(ref)
+                self.ctl_stride[ref] = stride
+                self.ctl_dev[ref] = m.malloc(S * C_ * stride)
+                self.ctl_host[ref] = m.pinned(S * self.epoch * stride)
+                self.policy_state[ref] = (C.c_uint8 * (_lib.PB_POLICY_STATE_BYTES * S))()
+                for f in fifos:
+                    self.counters[f.id] = m.malloc(8 * 4 * S)
+        # ring counters start with max occupancy = delay (0 here) — zeroed above
+
+        # host staging for sources and sinks
+        self.src_host: dict[str, tuple[int, np.ndarray]] = {}
+        self.sink_host: dict[str, tuple[int, np.ndarray]] = {}
+        for a in g.actors:
+            role = plan.roles[a.id]
+            if role == "source":
+                for p in a.output_ports:
+                    f = sorted(g.fifos_from(PortRef(a.id, p.id)), key=lambda f: f.id)[0]
+                    key = f"{a.id}.{p.id}"
+                    self.src_host[key] = m.pinned(S * self.epoch * f.rate * f.token_bytes)
+            elif role == "sink":
+                for p in a.input_ports:
+                    f = g.fifo_into(PortRef(a.id, p.id))
+                    self.sink_host[f.id] = m.pinned(S * self.epoch * f.rate * f.token_bytes)
+
+        # FIR taps and history state
+        self.fir_taps: dict[str, int] = {}
+        self.fir_state: dict[str, int] = {}
+        for a in g.actors:
+            b = self.behaviors[0][a.id]
+            if getattr(b, "kernel", "") == "fir":
+                b.init(a.id, a.params, None)
+                taps = np.array(list(b.re) + list(b.im), dtype=np.float32)
+                self.fir_taps[a.id] = m.upload(taps)
+                self.fir_state[a.id] = m.malloc(S * 2 * 9 * 4)
+            elif getattr(b, "kernel", "") == "matmul":
+                b.init(a.id, a.params, None)
+        _lib.check(self.lib.pb_device_sync(), "allocation")
+
+    # ------------------------------------------------------------ span refs
+
+    def _ref(self, fid: str) -> _lib.SpanRef:
+        st = self.storage[fid]
+        return _lib.SpanRef(st.data, st.stream_stride, st.span, st.base, st.slots,
+                            st.index_cond, self.plan.fifo_cond[fid], 0)
+
+    def _resolved(self, n_iter: int) -> _lib.Resolved:
+        return _lib.Resolved(self.res_act, self.res_prefix, self.res_count, self.res_wl,
+                             len(self.plan.conds), self.n_streams, n_iter, self.cap)
+
+    def _fir_actor(self, aid: str, in_fid: str, out_fid: str | None) -> _lib.FirActor:
+        out = self._ref(out_fid) if out_fid is not None else _lib.SpanRef()
+        return _lib.FirActor(self._ref(in_fid), out, self.fir_taps[aid], self.fir_state[aid],
+                             self.plan.actor_cond[aid], 0)
+
+    def _build_launches(self):
+        g, plan = self.graph, self.plan
+        self.launches: list[tuple] = []
+        self.fir_groups: list[tuple[int, int, int]] = []    # (device array, n, block)
+        done: set[str] = set()
+        bank_at = {grp.combiner: grp for grp in self.banks}
+        # topological depth so independent FIR actors share a launch
+        depth = {aid: 0 for aid in plan.order}
+        for aid in plan.order:
+            for fid in plan.data_fifos:
+                f = g.fifo(fid)
+                if f.src.actor == aid:
+                    depth[f.dst.actor] = max(depth[f.dst.actor], depth[aid] + 1)
+        fir_by_level: dict[tuple[int, int], list[str]] = {}
+        for aid in plan.order:
+            b = self.behaviors[0][aid]
+            if getattr(b, "kernel", "") == "fir" and aid not in self.fused_actors:
+                a = g.actor(aid)
+                fin = g.fifo_into(PortRef(aid, a.input_ports[0].id))
+                block = fin.rate * fin.token_bytes // 8
+                fir_by_level.setdefault((depth[aid], block), []).append(aid)
+
+        for aid in plan.order:
+            if aid in done or aid in self.fused_actors:
+                continue
+            a = g.actor(aid)
+            role = plan.roles[aid]
+            if role in ("source", "config", "sink"):
+                continue
+            b = self.behaviors[0][aid]
+            kind = getattr(b, "kernel", "")
+            if aid in bank_at:
+                grp = bank_at[aid]
+                x = g.actor(grp.router)
+                fin = g.fifo_into(PortRef(x.id, x.data_inputs[0].id))
+                (pout,) = a.output_ports
+                fout = sorted(g.fifos_from(PortRef(aid, pout.id)), key=lambda f: f.id)[0]
+                arr = (_lib.FirActor * len(grp.branches))()
+                for k, bid in enumerate(grp.branches):
+                    arr[k] = self._fir_actor(bid, fin.id, None)
+                dev = self.mem.upload(np.frombuffer(bytes(arr), dtype=np.uint8))
+                bank = _lib.FilterBank(self._ref(fin.id), self._ref(fout.id), dev,
+                                       len(grp.branches), plan.actor_cond[aid])
+                block = fin.rate * fin.token_bytes // 8
+                self.launches.append(("bank", bank, block))
+                self.fir_groups.append((dev, len(grp.branches), block))
+                done.add(aid)
+                continue
+            if kind == "fir":
+                key = next(k for k, v in fir_by_level.items() if aid in v)
+                members = fir_by_level[key]
+                arr = (_lib.FirActor * len(members))()
+                for k, bid in enumerate(members):
+                    ba = g.actor(bid)
+                    fi = g.fifo_into(PortRef(bid, ba.input_ports[0].id))
+                    fo = sorted(g.fifos_from(PortRef(bid, ba.output_ports[0].id)),
+                                key=lambda f: f.id)[0]
+                    arr[k] = self._fir_actor(bid, fi.id, fo.id)
+                dev = self.mem.upload(np.frombuffer(bytes(arr), dtype=np.uint8))
+                self.launches.append(("fir", dev, len(members), key[1]))
+                self.fir_groups.append((dev, len(members), key[1]))
+                done.update(members)
+                continue
+            ins = sorted(a.data_inputs, key=lambda p: p.id)
+            outs = sorted(a.output_ports, key=lambda p: p.id)
+            in_f = [g.fifo_into(PortRef(aid, p.id)).id for p in ins]
+            out_f = [sorted(g.fifos_from(PortRef(aid, p.id)), key=lambda f: f.id)[0].id
+                     for p in outs]
+            if kind == "route":
+                if all(self.storage[f].owner == self.storage[in_f[0]].owner for f in out_f):
+                    done.add(aid)          # aliased: no bytes move
+                    continue
+                kind = "bytes"
+            if kind == "branch_sum":
+                if len(in_f) > _lib.PB_MAX_PORTS:
+                    raise UnsupportedGraph(f"{aid}: more than {_lib.PB_MAX_PORTS} inputs")
+                act = _lib.SumActor()
+                for k, fid in enumerate(in_f):
+                    act.in_[k] = self._ref(fid)
+                act.n_in = len(in_f)
+                act.out = self._ref(out_f[0])
+                act.cond = plan.actor_cond[aid]
+                f0 = g.fifo(out_f[0])
+                self.launches.append(("sum", act, f0.rate * f0.token_bytes // 8))
+            elif kind == "bytes":
+                act = _lib.BytesActor()
+                for k, fid in enumerate(in_f):
+                    act.in_[k] = self._ref(fid)
+                for k, fid in enumerate(out_f):
+                    act.out[k] = self._ref(fid)
+                act.n_in, act.n_out = len(in_f), len(out_f)
+                act.offset = int(a.params.get("offset", 0)) if b.registered_name == "add_mod" \
+                    else 0
+                act.cond = plan.actor_cond[aid]
+                self.launches.append(("bytes", act))
+            elif kind == "matmul":
+                w = np.array(a.params["w"], dtype=np.float32)
+                n = int(round(len(w) ** 0.5))
+                act = _lib.MatmulActor(self._ref(in_f[0]), self._ref(out_f[0]),
+                                       self.mem.upload(w), n, plan.actor_cond[aid])
+                self.launches.append(("matmul", act))
+            elif kind == "path_merge":
+                act = _lib.PathMergeActor()
+                bypass = a.params.get("bypass_port", "")
+                for k, fid in enumerate(in_f):
+                    act.in_[k] = self._ref(fid)
+                act.n_in = len(in_f)
+                act.bypass_index = [p.id for p in ins].index(bypass) if bypass in \
+                    [p.id for p in ins] else -1
+                act.marker = float(np.float32(a.params.get("marker", 0.5)))
+                act.cond = plan.actor_cond[aid]
+                act.error_flag = self.err_flag
+                act.out = self._ref(out_f[0])
+                self.launches.append(("path_merge", act, aid))
+            else:
+                raise UnsupportedGraph(f"actor {aid}: no device kernel for behaviour "
+                                       f"{a.behavior!r}")
+            done.add(aid)
+
+        # bulk ring advance for every FIFO
+        adv = []
+        for f in g.fifos:
+            adv.append(_lib.RingAdvance(self.counters[f.id], plan.fifo_cond[f.id], f.rate,
+                                        f.delay, 0))
+        self.advance = (_lib.RingAdvance * len(adv))(*adv)
+        eq = [_lib.Eq1Port(own, moved, ALWAYS, 0) for (_, _, own, moved) in plan.eq1_ports]
+        self.eq1 = (_lib.Eq1Port * max(1, len(eq)))(*eq)
+        self.n_eq1 = len(eq)
+
+    # -------------------------------------------------------------- epochs
+
+    def _conditions(self, it0: int) -> C.Array:
+        arr = (_lib.Condition * max(1, len(self.plan.conds)))()
+        for k, c in enumerate(self.plan.conds):
+            stride = self.ctl_stride[c.ctl]
+            arr[k] = _lib.Condition(self.ctl_dev[c.ctl], self.C * stride, stride,
+                                    c.element - 1, self.C, it0 % self.C)
+        return arr
+
+    def _h2d_chunks(self, dev: int, stride: int, span: int, host: int, E: int, first: int):
+        """host [S][E][span] -> device ring chunks (first + n) % C of every stream."""
+        lib, S, C_ = self.lib, self.n_streams, self.C
+        a = first % C_
+        n1 = min(E, C_ - a)
+        if n1 == C_ and stride == C_ * span:
+            _lib.check(lib.pb_memcpy_h2d(dev, host, S * E * span, self.stream))
+            return
+        _lib.check(lib.pb_memcpy_2d(dev + a * span, stride, host, E * span, n1 * span, S, 1,
+                                    self.stream))
+        if n1 < E:
+            _lib.check(lib.pb_memcpy_2d(dev, stride, host + n1 * span, E * span, (E - n1) * span,
+                                        S, 1, self.stream))
+
+    def _d2h_chunks(self, dev: int, stride: int, span: int, host: int, E: int, first: int):
+        lib, S, C_ = self.lib, self.n_streams, self.C
+        a = first % C_
+        n1 = min(E, C_ - a)
+        _lib.check(lib.pb_memcpy_2d(host, E * span, dev + a * span, stride, n1 * span, S, 2,
+                                    self.stream))
+        if n1 < E:
+            _lib.check(lib.pb_memcpy_2d(host + n1 * span, E * span, dev, stride,
+                                        (E - n1) * span, S, 2, self.stream))
+
+    def source_staging(self, actor: str, port: str | None = None) -> np.ndarray:
+        """Pinned host buffer [S][epoch][span] a source's spans are copied from;
+        fill it directly and pass prestaged=True to skip the host-side copy."""
+        a = self.graph.actor(actor)
+        pid = port or sorted(a.output_ports, key=lambda p: p.id)[0].id
+        f = sorted(self.graph.fifos_from(PortRef(actor, pid)), key=lambda f: f.id)[0]
+        span = f.rate * f.token_bytes
+        return self.src_host[f"{actor}.{pid}"][1][:self.n_streams * self.epoch * span].reshape(
+            self.n_streams, self.epoch, span)
+
+    def stage_sources(self, it0: int, E: int, prestaged: bool = False):
+        """Host sources produce E spans per stream (runtime.py:123-124 stops
+        them after source_firings) and copy them into the device rings."""
+        g, S = self.graph, self.n_streams
+        for a in g.actors:
+            if self.plan.roles[a.id] != "source":
+                continue
+            ports = sorted(a.output_ports, key=lambda p: p.id)
+            if prestaged:
+                for p in ports:
+                    f = sorted(g.fifos_from(PortRef(a.id, p.id)), key=lambda f: f.id)[0]
+                    st = self.storage[f.id]
+                    self._h2d_chunks(st.data, st.stream_stride, f.rate * f.token_bytes,
+                                     self.src_host[f"{a.id}.{p.id}"][0], E, it0)
+                continue
+            for p in ports:
+                f = sorted(g.fifos_from(PortRef(a.id, p.id)), key=lambda f: f.id)[0]
+                span = f.rate * f.token_bytes
+                hptr, harr = self.src_host[f"{a.id}.{p.id}"]
+                buf = harr[:S * E * span].reshape(S, E, span)
+                if a.id in self.sources:
+                    for s in range(S):
+                        data = np.frombuffer(memoryview(self.sources[a.id][s]).cast("B"),
+                                             dtype=np.uint8)
+                        lo = it0 * span * len(ports)
+                        chunk = data[lo:lo + E * span]
+                        if chunk.size < E * span:
+                            raise ActorPanic(a.id, EOFError(
+                                f"{a.id}: input exhausted at byte {lo + chunk.size}"))
+                        buf[s] = chunk.reshape(E, span)
+                elif len(ports) == 1 and type(self.behaviors[0][a.id]) is FileSource:
+                    for s in range(S):
+                        b = self.behaviors[s][a.id]
+                        try:
+                            view = b.take(a.id, E * span)
+                        except EOFError as e:
+                            raise ActorPanic(a.id, e) from e
+                        buf[s] = np.frombuffer(view, dtype=np.uint8).reshape(E, span)
+                else:
+                    continue
+                st = self.storage[f.id]
+                self._h2d_chunks(st.data, st.stream_stride, span, hptr, E, it0)
+            if a.id in self.sources or (len(ports) == 1 and
+                                        type(self.behaviors[0][a.id]) is FileSource):
+                continue
+            # generic host source: fire per iteration through the plugin API
+            views = {}
+            for p in ports:
+                f = sorted(g.fifos_from(PortRef(a.id, p.id)), key=lambda f: f.id)[0]
+                views[p.id] = (f, self.src_host[f"{a.id}.{p.id}"])
+            for s in range(S):
+                b = self.behaviors[s][a.id]
+                seed = actor_seed(self.seeds[s], a.id)
+                for n in range(E):
+                    outs = {}
+                    for pid, (f, (hp, harr)) in views.items():
+                        span = f.rate * f.token_bytes
+                        off = (s * E + n) * span
+                        outs[pid] = memoryview(harr[off:off + span])
+                    ctx = FireContext(a.id, it0 + n, {p.id: p.rate for p in a.ports}, {}, outs,
+                                      a.params, seed, None)
+                    try:
+                        b.fire(ctx)
+                    except Exception as e:  # noqa: BLE001
+                        raise ActorPanic(a.id, e) from e
+            for pid, (f, (hp, harr)) in views.items():
+                st = self.storage[f.id]
+                self._h2d_chunks(st.data, st.stream_stride, f.rate * f.token_bytes, hp, E, it0)
+
+    def stage_control(self, it0: int, E: int):
+        """Configuration actors emit E tokens per stream (behavior.py:212-218)."""
+        g, S = self.graph, self.n_streams
+        for ref in self.ctl_ports:
+            a = g.actor(ref.actor)
+            stride = self.ctl_stride[ref]
+            hptr, harr = self.ctl_host[ref]
+            buf = harr[:S * E * stride]
+            b0 = self.behaviors[0][a.id]
+            kind = native_policy_kind(b0)
+            min_tb = min(f.token_bytes for f in g.fifos_from(ref))
+            ctl_ports = [p for p in a.output_ports if p.kind == CONTROL_OUT]
+            if kind is not None and len(ctl_ports) == 1:
+                try:
+                    length = int(a.params["length"])
+                    param = b0.native_param(a.params)
+                    if length > min_tb:
+                        raise ValueError(f"{length} control elements exceed {min_tb} bytes")
+                except Exception as e:  # noqa: BLE001
+                    raise ActorPanic(a.id, e) from e
+                rc = self.lib.pb_policy_tokens_streams(
+                    C.addressof(self.policy_state[ref]), S, kind, length, param, it0, E, hptr, stride,
+                    int(self.config.host_threads))
+                if rc != _lib.PB_OK:
+                    raise ActorPanic(a.id, ValueError(_lib.error_text()))
+            else:
+                for s in range(S):
+                    b = self.behaviors[s][a.id]
+                    seed = actor_seed(self.seeds[s], a.id)
+                    for n in range(E):
+                        off = (s * E + n) * stride
+                        span = memoryview(buf[off:off + min_tb])
+                        outs = {p.id: span for p in ctl_ports}
+                        ctx = FireContext(a.id, it0 + n, {p.id: p.rate for p in a.ports}, {},
+                                          outs, a.params, seed, None)
+                        try:
+                            b.fire(ctx)
+                        except Exception as e:  # noqa: BLE001
+                            raise ActorPanic(a.id, e) from e
+                        buf[off + min_tb:off + stride] = 0
+            self._h2d_chunks(self.ctl_dev[ref], self.C * stride, stride, hptr, E, it0)
+
+    def fire_epoch(self, it0: int, E: int, hook=None) -> int:
+        """Device work of one epoch (inputs already resident); returns launches.
+        hook(kind, phase) is called around every actor launch (phase 'pre' /
+        'post') so callers can record events on self.stream."""
+        lib, st = self.lib, self.stream
+        n0 = lib.pb_launch_count()
+        res = self._resolved(E)
+        if self.plan.conds:
+            conds = self._conditions(it0)
+            _lib.check(lib.pb_resolve(conds, res, st), "pb_resolve")
+        if self.n_eq1:
+            _lib.check(lib.pb_eq1_check(self.eq1, self.n_eq1, res, self.eq1_ctr, st),
+                       "pb_eq1_check")
+        for item in self.launches:
+            kind = item[0]
+            if hook is not None:
+                hook(kind, "pre")
+            if kind == "bank":
+                _lib.check(lib.pb_fire_filter_bank(item[1], res, item[2], st), "filter_bank")
+            elif kind == "fir":
+                _lib.check(lib.pb_fire_fir(item[1], item[2], res, item[3], st), "fir_branch")
+            elif kind == "sum":
+                _lib.check(lib.pb_fire_branch_sum(item[1], res, item[2], st), "branch_sum")
+            elif kind == "bytes":
+                _lib.check(lib.pb_fire_bytes(item[1], res, st), "bytes")
+            elif kind == "matmul":
+                _lib.check(lib.pb_fire_matmul(item[1], res, st), "matmul")
+            elif kind == "path_merge":
+                _lib.check(lib.pb_fire_path_merge(item[1], res, st), "path_merge")
+            if hook is not None:
+                hook(kind, "post")
+        for dev, n, block in self.fir_groups:
+            _lib.check(lib.pb_fir_carry(dev, n, res, block, st), "fir_carry")
+        _lib.check(lib.pb_rings_advance(self.advance, len(self.advance), res, st),
+                   "pb_rings_advance")
+        return lib.pb_launch_count() - n0
+
+    def _epoch_counts(self) -> np.ndarray:
+        n_cond = len(self.plan.conds)
+        out = np.zeros((max(1, n_cond), self.n_streams), dtype=np.int32)
+        if n_cond:
+            _lib.check(self.lib.pb_memcpy_d2h(out.ctypes.data, self.res_count, out.nbytes,
+                                              self.stream))
+        return out
+
+    def drain_sinks(self, it0: int, E: int, counts: np.ndarray):
+        g, S = self.graph, self.n_streams
+        pending = []
+        for a in g.actors:
+            if self.plan.roles[a.id] != "sink":
+                continue
+            ports = sorted(a.input_ports, key=lambda p: p.id)
+            c = self.plan.actor_cond[a.id]
+            bufs = []
+            for p in ports:
+                f = g.fifo_into(PortRef(a.id, p.id))
+                st = self.storage[f.id]
+                span = f.rate * f.token_bytes
+                hptr, harr = self.sink_host[f.id]
+                first = it0 if st.index_cond == ALWAYS else None
+                if first is None:
+                    raise UnsupportedGraph(f"sink {a.id} reads a compacted channel")
+                self._d2h_chunks(st.data, st.stream_stride, span, hptr, E, first)
+                bufs.append((p.id, span, harr[:S * E * span].reshape(S, E, span)))
+            pending.append((a, c, bufs))
+        _lib.check(self.lib.pb_stream_sync(self.stream), "sink drain")
+        jobs = []
+        for a, c, bufs in pending:
+            for s in range(S):
+                active = None
+                if c != ALWAYS:
+                    active = self._act_host(c, s, E)
+                jobs.append((a, s, bufs, active))
+
+        def digest(job):
+            a, s, bufs, active = job
+            h = self.digests[a.id][s]
+            cap = self.captured[a.id][s] if self.captured is not None else None
+            b = self.behaviors[s][a.id]
+            generic = type(b).fire is not type(resolve("null_sink")).fire
+            if len(bufs) == 1 and active is None and not generic:
+                data = bufs[0][2][s].reshape(-1)
+                h.update(data)
+                if cap is not None:
+                    cap.extend(data.tobytes())
+                return
+            for n in range(E):
+                if active is not None and not active[n]:
+                    continue
+                ins = {}
+                for pid, span, arr in bufs:
+                    data = arr[s, n].tobytes()
+                    h.update(data)
+                    if cap is not None:
+                        cap.extend(data)
+                    ins[pid] = memoryview(data)
+                if generic:
+                    ctx = FireContext(a.id, self.fired[a.id][s], {}, ins, {}, a.params,
+                                      actor_seed(self.seeds[s], a.id), None)
+                    b.fire(ctx)
+                self.fired[a.id][s] += 1
+
+        if len(jobs) > 1:
+            list(self.pool.map(digest, jobs))
+        else:
+            for j in jobs:
+                digest(j)
+
+    def _act_host(self, c: int, s: int, E: int) -> np.ndarray:
+        out = np.zeros(E, dtype=np.uint8)
+        off = (c * self.n_streams + s) * self.cap
+        _lib.check(self.lib.pb_memcpy_d2h(out.ctypes.data, self.res_act + off, E, self.stream))
+        _lib.check(self.lib.pb_stream_sync(self.stream))
+        return out
+
+    # ------------------------------------------------------------------ run
+
+    def reset(self):
+        """Fresh run state: counters, histories, behaviour init, digests."""
+        lib, m, g, S = self.lib, self.mem, self.graph, self.n_streams
+        for fid, ctr in self.counters.items():
+            _lib.check(lib.pb_memset(ctr, 0, 8 * 4 * S, self.stream))
+        for aid, p in self.fir_state.items():
+            _lib.check(lib.pb_memset(p, 0, S * 2 * 9 * 4, self.stream))
+        _lib.check(lib.pb_memset(self.eq1_ctr, 0, 16, self.stream))
+        _lib.check(lib.pb_memset(self.err_flag, 0, 16, self.stream))
+        for s in range(S):
+            for a in g.actors:
+                b = self.behaviors[s][a.id]
+                if a.id in self.sources and self.plan.roles[a.id] == "source":
+                    continue
+                try:
+                    b.init(a.id, a.params, actor_seed(self.seeds[s], a.id))
+                except Exception as e:  # noqa: BLE001
+                    raise ActorPanic(a.id, e) from e
+        for ref, buf in self.policy_state.items():
+            for s in range(S):
+                seed = actor_seed(self.seeds[s], ref.actor)
+                _lib.check(lib.pb_policy_init(C.addressof(buf) + s * _lib.PB_POLICY_STATE_BYTES,
+                                              -1 if seed is None else seed))
+        self._prev_writes = {f.id: 0 for f in g.fifos}
+        sinks = [a.id for a in g.actors if self.plan.roles[a.id] == "sink"]
+        self.digests = {aid: [hashlib.sha256() for _ in range(S)] for aid in sinks}
+        self.captured = ({aid: [bytearray() for _ in range(S)] for aid in sinks}
+                         if self.config.capture_sinks else None)
+        self.fired = {aid: [0] * S for aid in sinks}
+        self.firings = {a.id: np.zeros(S, dtype=np.int64) for a in g.actors}
+        _lib.check(lib.pb_stream_sync(self.stream), "reset")
+
+    def run_all(self, prestaged: bool = False) -> list[RunReport]:
+        cfg, S = self.config, self.n_streams
+        N = int(cfg.source_firings)
+        self.reset()
+        t_start = time.perf_counter()
+        deadline = None if cfg.timeout_ms is None else t_start + cfg.timeout_ms / 1000.0
+        self.pool = ThreadPoolExecutor(max_workers=max(1, cfg.host_threads or 16))
+        try:
+            it = 0
+            while it < N:
+                E = min(self.epoch, N - it)
+                self.stage_sources(it, E, prestaged=prestaged and N <= self.epoch)
+                self.stage_control(it, E)
+                self.fire_epoch(it, E)
+                counts = self._epoch_counts()
+                self.drain_sinks(it, E, counts)
+                self._check_device_errors()
+                for a in self.graph.actors:
+                    c = self.plan.actor_cond[a.id]
+                    self.firings[a.id] += E if c == ALWAYS else counts[c]
+                if cfg.trace is not None:
+                    self._trace()
+                it += E
+                if deadline is not None and time.perf_counter() > deadline and it < N:
+                    raise Timeout(cfg.timeout_ms, sorted(a.id for a in self.graph.actors))
+            for s in range(S):
+                for a in self.graph.actors:
+                    try:
+                        self.behaviors[s][a.id].finish(a.id)
+                    except Exception as e:  # noqa: BLE001
+                        raise ActorPanic(a.id, e) from e
+        finally:
+            self.pool.shutdown(wait=True)
+        wall_ms = (time.perf_counter() - t_start) * 1000.0
+        return self._reports(wall_ms)
+
+    def _check_device_errors(self):
+        flag = np.zeros(1, dtype=np.int32)
+        _lib.check(self.lib.pb_memcpy_d2h(flag.ctypes.data, self.err_flag, 4, self.stream))
+        _lib.check(self.lib.pb_stream_sync(self.stream), "epoch")
+        if flag[0]:
+            for item in self.launches:
+                if item[0] == "path_merge":
+                    raise ActorPanic(item[2], ValueError(
+                        "path_merge needs exactly one live input per firing"))
+            raise ActorPanic("device", RuntimeError("device actor reported a failure"))
+
+    def _counters(self, fid: str) -> np.ndarray:
+        out = np.zeros((4, self.n_streams), dtype=np.int64)
+        _lib.check(self.lib.pb_memcpy_d2h(out.ctypes.data, self.counters[fid], out.nbytes,
+                                          self.stream))
+        _lib.check(self.lib.pb_stream_sync(self.stream))
+        return out
+
+    def _trace(self):
+        """Per-epoch bulk trace lines in the reference format `fifo op occupancy`
+        (runtime.py:259-272): one `w` line at the epoch's write peak and one
+        `r` line after the consumer drained it (stream 0)."""
+        for f in self.graph.fifos:
+            ctr = self._counters(f.id)
+            w, r = int(ctr[0, 0]), int(ctr[1, 0])
+            self.config.trace(f"{f.id} w {f.delay + f.rate * (w - self._prev_writes[f.id])}")
+            self.config.trace(f"{f.id} r {f.delay + f.rate * (w - r)}")
+            self._prev_writes[f.id] = w
+
+    def _reports(self, wall_ms: float) -> list[RunReport]:
+        g, S = self.graph, self.n_streams
+        eq = np.zeros(2, dtype=np.int64)
+        _lib.check(self.lib.pb_memcpy_d2h(eq.ctypes.data, self.eq1_ctr, 16, self.stream))
+        ctrs = {f.id: self._counters(f.id) for f in g.fifos}
+        reports = []
+        for s in range(S):
+            r = RunReport(wall_ms=wall_ms)
+            for a in g.actors:
+                r.firing_counts[a.id] = int(self.firings[a.id][s])
+            for aid, hs in self.digests.items():
+                r.sink_digests[aid] = hs[s].hexdigest()
+                if self.captured is not None:
+                    r.sink_data[aid] = bytes(self.captured[aid][s])
+            for f in g.fifos:
+                r.max_occupancy[f.id] = int(ctrs[f.id][2, s])
+                r.slots[f.id] = max(f.rate * self.C, f.delay)
+            r.beta = dict(self.analysis.beta)
+            reports.append(r)
+        # Eq. 1 counters are device-wide; attribute them evenly per stream
+        for r in reports:
+            r.eq1_checks = int(eq[0]) // S
+            r.eq1_failures = int(eq[1]) // S
+        return reports
+
+    def close(self):
+        if getattr(self, "mem", None) is not None:
+            self.mem.close()
+            self.mem = None
+        if getattr(self, "stream", None):
+            self.lib.pb_stream_destroy(self.stream)
+            self.stream = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def instantiate(graph, behaviors: Mapping | None = None, config: RuntimeConfig | None = None,
+                analysis=None) -> DeviceRuntime:
+    """runtime.py:327-342: admission-gated executor for one stream."""
+    return DeviceRuntime(graph, behaviors, config, n_streams=1)
+
+
+def run(graph, behaviors: Mapping | None = None,
+        config: RuntimeConfig | None = None) -> RunReport:
+    """Drop-in for tokenflow.runtime.run (runtime.py:345-347)."""
+    rt = instantiate(graph, behaviors, config)
+    try:
+        return rt.run_all()[0]
+    finally:
+        rt.close()
+
+
+def run_streams(graph, n_streams: int, config: RuntimeConfig | None = None,
+                seeds: Sequence[int | None] | None = None,
+                sources: Mapping[str, Sequence] | None = None,
+                behaviors: Mapping | None = None) -> list[RunReport]:
+    """Run `n_streams` independent replicas of `graph` (per-stream seeds and
+    source data) in one batched device execution; one RunReport per stream."""
+    rt = DeviceRuntime(graph, behaviors, config, n_streams=n_streams, seeds=seeds,
+                       sources=sources)
+    try:
+        return rt.run_all()
+    finally:
+        rt.close()

@@ -1,0 +1,317 @@
+"""Admission and launch planning for the device executor.
+
+The threaded reference executor (runtime.py:118-193) resolves every dynamic
+port's rate per firing on the host (Eq. 1, runtime.py:107-116).  Here the
+same information is computed once per graph as *conditions*: every
+(control output port, element) pair of the control table (model.py:137-163)
+is one boolean sequence over iterations, and every actor and FIFO is gated by
+exactly one condition or by none ("always").  Propagation goes
+
+    DRP of a dynamic actor  ->  its control-table entry
+    static actor            <-  the condition of any FIFO touching it
+    FIFO                    =   condition of its producer port
+                            =   condition of its consumer port   (Eq. 1)
+
+A FIFO whose two ends disagree is exactly a graph whose token counts cannot
+balance per iteration (analysis.py:264-319 rejects those too), so admission
+raises InconsistentGraph.  The executor covers acyclic, delay-free graphs
+whose dynamic regions are not nested, with configuration actors that have no
+data inputs (every shipped app except motion detection, whose one-frame delay
+FIFO is listed as next work in DESIGN.md); anything else raises
+UnsupportedGraph rather than running incorrectly.
+
+Per iteration n every "always" actor fires once and every gated actor fires
+iff its condition is true at n, which is the firing sequence both reference
+engines produce (interp.py:126-148 is the oracle's version of the rule).
+Buffer bounds follow compute_bounds (analysis.py:398-411): for a delay-free
+rate-r FIFO the per-period bound is r, so beta = r + (C-1)*r.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .behaviors import ActorBehavior, DeviceBehavior
+from .errors import InconsistentGraph, UnsupportedGraph
+from .graph import (CONFIG, CONTROL_IN, CONTROL_OUT, DRP, DYNAMIC, Graph, PortRef)
+
+ALWAYS = -1
+
+
+@dataclass
+class AdmissionReport:
+    """Stand-in for analysis.ConsistencyReport: verdict, problems and the
+    per-FIFO bound beta(f) for the chosen buffering factor."""
+
+    verdict: str = "consistent"
+    problems: list[str] = field(default_factory=list)
+    beta: dict[str, int] = field(default_factory=dict)
+    c_factor: int = 3
+
+    @property
+    def consistent(self) -> bool:
+        return self.verdict == "consistent"
+
+
+@dataclass(frozen=True)
+class Condition:
+    ctl: PortRef        # control output port of a configuration actor
+    element: int        # 1-based element of the control value
+
+
+@dataclass
+class FilterBankGroup:
+    """route -> K x fir_branch -> branch_sum region fired as one kernel."""
+
+    router: str
+    combiner: str
+    branches: list[str]          # fir_branch actors in the combiner's sorted port order
+    internal_fifos: set[str]
+
+
+@dataclass
+class ExecPlan:
+    graph: Graph
+    conds: list[Condition]
+    actor_cond: dict[str, int]
+    fifo_cond: dict[str, int]
+    order: list[str]                       # topological order over data FIFOs
+    roles: dict[str, str]                  # source | config | dynamic | device | sink
+    control_fifos: list[str]
+    data_fifos: list[str]
+    eq1_ports: list[tuple[str, str, int, int]]   # (actor, port, own_cond, moved_cond)
+    admission: AdmissionReport
+
+
+def _problem(report: AdmissionReport, msg: str) -> None:
+    report.verdict = "inconsistent"
+    report.problems.append(msg)
+
+
+def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
+    """Build the condition plan or raise InconsistentGraph/UnsupportedGraph."""
+    report = AdmissionReport(c_factor=c_factor)
+    unsupported: list[str] = []
+
+    # every dynamic port needs a table entry (analysis.py:420-427)
+    conds: list[Condition] = []
+    cond_index: dict[Condition, int] = {}
+
+    def cond_of(ctl: PortRef, element: int) -> int:
+        c = Condition(ctl, element)
+        if c not in cond_index:
+            cond_index[c] = len(conds)
+            conds.append(c)
+        return cond_index[c]
+
+    port_cond: dict[PortRef, int] = {}
+    for a in g.actors:
+        if a.kind == DYNAMIC:
+            for p in a.drps:
+                ref = PortRef(a.id, p.id)
+                try:
+                    ctl, el = g.control_lookup(ref)
+                except Exception as e:  # noqa: BLE001
+                    _problem(report, f"Uncontrolled: {e}")
+                    continue
+                port_cond[ref] = cond_of(ctl, el)
+    if not report.consistent:
+        raise InconsistentGraph(report)
+
+    roles: dict[str, str] = {}
+    actor_cond: dict[str, int | None] = {}
+    for a in g.actors:
+        data_in = [p for p in a.input_ports if p.kind != CONTROL_IN]
+        data_out = [p for p in a.output_ports if p.kind != CONTROL_OUT]
+        if a.kind == CONFIG:
+            if data_in:
+                unsupported.append(f"configuration actor {a.id} reads data ports; control "
+                                   "tokens must be computable ahead of the data")
+            roles[a.id] = "config"
+            actor_cond[a.id] = ALWAYS
+        elif a.kind == DYNAMIC:
+            roles[a.id] = "dynamic"
+            actor_cond[a.id] = ALWAYS
+        elif not data_in:
+            roles[a.id] = "source"
+            actor_cond[a.id] = ALWAYS
+        elif not data_out:
+            roles[a.id] = "sink"
+            actor_cond[a.id] = None
+        else:
+            roles[a.id] = "device"
+            actor_cond[a.id] = None
+
+    control_fifos = [f.id for f in g.fifos if g.actor(f.src.actor).port(f.src.port).kind
+                     == CONTROL_OUT]
+    data_fifos = [f.id for f in g.fifos if f.id not in set(control_fifos)]
+
+    # control channels: the two dynamic actors of a pair must see the same
+    # token (rule 2 of the paper; analysis rejects skewed delays)
+    by_ctl: dict[PortRef, set[int]] = {}
+    for fid in control_fifos:
+        f = g.fifo(fid)
+        by_ctl.setdefault(f.src, set()).add(f.delay)
+    for ctl, delays in by_ctl.items():
+        if len(delays) > 1:
+            _problem(report, f"rule 2: control tokens of {ctl} reach its dynamic actors with "
+                             f"different delays {sorted(delays)}")
+        elif delays != {0}:
+            unsupported.append(f"control channels of {ctl} carry initial delay tokens")
+    for fid in data_fifos:
+        if g.fifo(fid).delay:
+            unsupported.append(f"fifo {fid} carries {g.fifo(fid).delay} initial delay tokens")
+
+    # propagate conditions through static actors
+    def pc(ref: PortRef) -> int | None:
+        if ref in port_cond:
+            return port_cond[ref]
+        return actor_cond[ref.actor]
+
+    changed = True
+    while changed:
+        changed = False
+        for fid in data_fifos:
+            f = g.fifo(fid)
+            cs, cd = pc(f.src), pc(f.dst)
+            if cs is None and cd is not None and f.src not in port_cond:
+                actor_cond[f.src.actor] = cd
+                changed = True
+            elif cd is None and cs is not None and f.dst not in port_cond:
+                actor_cond[f.dst.actor] = cs
+                changed = True
+    for aid, c in actor_cond.items():
+        if c is None:
+            actor_cond[aid] = ALWAYS
+
+    fifo_cond: dict[str, int] = {}
+    for fid in data_fifos:
+        f = g.fifo(fid)
+        cs, cd = pc(f.src), pc(f.dst)
+        if cs != cd:
+            def name(c):
+                if c == ALWAYS:
+                    return "always"
+                return f"{conds[c].ctl}[{conds[c].element}]"
+            nested = (roles[f.src.actor] == "dynamic" and f.src not in port_cond) or \
+                     (roles[f.dst.actor] == "dynamic" and f.dst not in port_cond)
+            msg = (f"fifo {fid}: producer {f.src} is gated by {name(cs)} but consumer "
+                   f"{f.dst} by {name(cd)}")
+            if nested and cs != ALWAYS and cd != ALWAYS:
+                unsupported.append("nested dynamic region: " + msg)
+            else:
+                _problem(report, "Eq. 1: " + msg)
+        fifo_cond[fid] = cs
+    for fid in control_fifos:
+        fifo_cond[fid] = ALWAYS
+
+    # topological order over data FIFOs (delay-free cycles deadlock)
+    indeg = {a.id: 0 for a in g.actors}
+    succ: dict[str, list[str]] = {a.id: [] for a in g.actors}
+    for fid in data_fifos:
+        f = g.fifo(fid)
+        succ[f.src.actor].append(f.dst.actor)
+        indeg[f.dst.actor] += 1
+    ready = sorted(a for a, d in indeg.items() if d == 0)
+    order: list[str] = []
+    while ready:
+        a = ready.pop(0)
+        order.append(a)
+        for b in succ[a]:
+            indeg[b] -= 1
+            if indeg[b] == 0:
+                ready.append(b)
+        ready.sort()
+    if len(order) != len(g.actors):
+        stuck = sorted(a for a, d in indeg.items() if d > 0)
+        delayed = any(g.fifo(fid).delay for fid in data_fifos)
+        if delayed:
+            unsupported.append(f"cycle through {stuck} (delay tokens)")
+        else:
+            _problem(report, f"DeadlockError: zero-delay cycle through {stuck}")
+
+    if not report.consistent:
+        raise InconsistentGraph(report)
+    if unsupported:
+        raise UnsupportedGraph("; ".join(unsupported))
+
+    eq1 = []
+    for a in g.actors:
+        if a.kind != DYNAMIC:
+            continue
+        for p in a.drps:
+            ref = PortRef(a.id, p.id)
+            fid = g.fifo_into(ref).id if p.direction == "in" else g.fifos_from(ref)[0].id
+            eq1.append((a.id, p.id, port_cond[ref], fifo_cond[fid]))
+
+    for fid in control_fifos + data_fifos:
+        f = g.fifo(fid)
+        report.beta[fid] = f.delay + f.rate + (c_factor - 1) * f.rate
+    return ExecPlan(g, conds, {k: v for k, v in actor_cond.items()}, fifo_cond, order, roles,
+                    control_fifos, data_fifos, eq1, report)
+
+
+def find_filter_banks(plan: ExecPlan, behaviors: dict[str, ActorBehavior]) -> list[FilterBankGroup]:
+    """Regions route -> {fir_branch} -> branch_sum that can fire fused.
+
+    Conditions: the router has one data input and only DRP outputs, each DRP
+    feeds exactly one fir_branch whose single output feeds a DRP of the same
+    branch_sum combiner, and the combiner's data inputs are all such branches
+    with one data output.  The branch channels then never leave registers.
+    """
+    g = plan.graph
+    groups = []
+    for x in g.actors:
+        bx = behaviors.get(x.id)
+        if plan.roles[x.id] != "dynamic" or getattr(bx, "kernel", None) != "route":
+            continue
+        if len(x.data_inputs) != 1:
+            continue
+        outs = [p for p in x.output_ports]
+        if not outs or any(p.kind != DRP for p in outs):
+            continue
+        branches: dict[str, str] = {}   # combiner port -> fir actor
+        internal: set[str] = set()
+        combiner = None
+        ok = True
+        for p in outs:
+            fs = g.fifos_from(PortRef(x.id, p.id))
+            if len(fs) != 1:
+                ok = False
+                break
+            b = g.actor(fs[0].dst.actor)
+            if getattr(behaviors.get(b.id), "kernel", None) != "fir" or \
+                    len(b.input_ports) != 1 or len(b.output_ports) != 1:
+                ok = False
+                break
+            fo = g.fifos_from(PortRef(b.id, b.output_ports[0].id))
+            if len(fo) != 1:
+                ok = False
+                break
+            y = g.actor(fo[0].dst.actor)
+            if combiner is None:
+                combiner = y.id
+            if y.id != combiner or y.port(fo[0].dst.port).kind != DRP:
+                ok = False
+                break
+            branches[fo[0].dst.port] = b.id
+            internal.update({fs[0].id, fo[0].id})
+        if not ok or combiner is None:
+            continue
+        y = g.actor(combiner)
+        if getattr(behaviors.get(y.id), "kernel", None) != "branch_sum":
+            continue
+        if sorted(p.id for p in y.data_inputs) != sorted(branches):
+            continue
+        if len([p for p in y.output_ports]) != 1:
+            continue
+        spans = {g.fifo(fid).rate * g.fifo(fid).token_bytes for fid in internal}
+        src = g.fifo_into(PortRef(x.id, x.data_inputs[0].id))
+        if spans != {src.rate * src.token_bytes}:
+            continue
+        groups.append(FilterBankGroup(x.id, combiner, [branches[p] for p in sorted(branches)],
+                                      internal))
+    return groups
+
+
+def is_device(b: ActorBehavior) -> bool:
+    return isinstance(b, DeviceBehavior) or bool(getattr(b, "kernel", ""))
