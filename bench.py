@@ -36,7 +36,7 @@ UNIT = "Msamples/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams", type=int, default=64, help="streams per GPU")
@@ -70,7 +70,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu=timestamp,{self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-i", str(index), "-lms", "50"], stdout=open(self.path, "w"),
+                 "-i", str(index), "-lms", "20"], stdout=open(self.path, "w"),
                 stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
@@ -299,14 +299,15 @@ def main():
 
     # ---- end to end through the public runtime API
     e2e_times = []
-    for k in range(args.e2e_steps + 1):
+    reps = None
+    for k in range(args.e2e_steps + 1 if args.e2e_steps > 0 else 0):
         barrier()
         t0 = time.perf_counter()
         reps = rt.run_all(prestaged=True)
         t1 = time.perf_counter()
         if k:
             e2e_times.append(max_over_ranks(t1 - t0))
-    e2e_s = statistics.median(e2e_times)
+    e2e_s = statistics.median(e2e_times) if e2e_times else float("nan")
     span = 8 * B
     h2d = S * blocks * span + S * blocks * rt.ctl_stride[next(iter(rt.ctl_ports))]
     d2h = S * blocks * span + 4 * len(rt.plan.conds) * S
@@ -319,7 +320,7 @@ def main():
         x0 = pd.stream_input(streams[0], blocks, B)
         sets = od.subset_schedule(pd.stream_seed(streams[0]), blocks, length=K)
         want = hashlib.sha256(od.dpd_stream(x0, sets, K).tobytes()).hexdigest()
-        parity = reps[0].sink_digests["sink"] == want
+        parity = reps[0].sink_digests["sink"] == want if reps else None
 
     peaks = {}
     try:

@@ -1,0 +1,10 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+mkdir -p gpurun_out
+./tools/fp32_probe > gpurun_out/fp32_probe.json 2>&1
+cat gpurun_out/fp32_probe.json
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -30 > gpurun_out/pytest_gpu.txt
+cat gpurun_out/pytest_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
+timeout 600 python bench.py --steps 20 --warmup 3 --skip-cpu > gpurun_out/bench1.json 2> gpurun_out/bench1.err
+tail -5 gpurun_out/bench1.err; cat gpurun_out/bench1.json
