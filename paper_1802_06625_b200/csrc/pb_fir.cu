@@ -11,8 +11,20 @@
 // time with the sample broadcast to both lanes, two scalar FADDs combine the
 // cross terms and one FADD2 accumulates {acc_r, acc_i}.  ptxas fuses a
 // mul.rn.f32x2 feeding an add.rn.f32x2 into FFMA2 even with -fmad=false, so
-// the products never feed a paired add directly (checked in the SASS: no
-// FFMA/FFMA2 in these kernels).
+// the products never feed a paired add directly (SASS of this file has no
+// FFMA/FFMA2; tests/test_native_host.py::test_no_fma_in_fir_kernels checks).
+//
+// Kernel structure (persistent, warp-specialised):
+//   warp 0   producer: walks the work items (stream, iteration, tile), waits
+//            for a free stage, streams the tile of both sample planes into
+//            shared memory with cp.async.bulk (TMA bulk copy, completion on
+//            the stage's mbarrier) and resolves the firing on the side: the
+//            active branches in the combiner's port order and, for the first
+//            tile of a span, each branch's 9-sample history.
+//   warps 1-4 consumers: wait for a full stage, run the FIR of every active
+//            branch over 8 consecutive outputs per thread, sum (bank) or
+//            store per branch, release the stage.
+// kStages stages keep the next tiles in flight while the FP32 pipe works.
 #include <algorithm>
 
 #include "pb_common.cuh"
@@ -23,11 +35,75 @@ typedef unsigned long long u64;
 
 constexpr int kTaps = PB_TAPS;
 constexpr int kHist = PB_TAPS - 1;
-constexpr int kThreads = 128;
+constexpr int kConsumerWarps = 4;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kThreads = kConsumers + 32;        // + producer warp
 constexpr int kPerThread = 8;                    // consecutive outputs per thread
-constexpr int kTile = kThreads * kPerThread;     // outputs per CTA tile
+constexpr int kTile = kConsumers * kPerThread;   // outputs per work item
 constexpr int kPad = 12;                         // halo slots in front of the tile (>= 9, x4)
 constexpr int kWin = kPerThread + kPad;          // per-thread window (20 samples)
+constexpr int kStages = 3;
+constexpr int kMaxBr = PB_MAX_BRANCHES;
+
+struct __align__(16) StageBuf {
+  float re[kPad + kTile];
+  float im[kPad + kTile];
+};
+
+struct __align__(16) Desc {
+  u64 out;        // output span tile base (float*), bank mode and per-actor mode
+  int valid;      // 0 terminates the consumers
+  int t0;
+  int n_act;
+  int first;      // tile 0: window entries before the span come from hist
+  int8_t br[kMaxBr];
+  float hist[kMaxBr][2][kHist];
+};
+
+struct __align__(16) Smem {
+  StageBuf buf[kStages];
+  Desc desc[kStages];
+  float4 taps[kMaxBr][kTaps];   // {cr, ci, ci, cr}
+  u64 full[kStages];
+  u64 empty[kStages];
+};
+
+// ----------------------------------------------------------- PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(u64* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+      smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(u64* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 
 __device__ __forceinline__ u64 pack2(float lo, float hi) {
   u64 r;
@@ -48,86 +124,42 @@ __device__ __forceinline__ u64 fadd2(u64 a, u64 b) {
   return r;
 }
 
-struct Taps {
-  u64 p[kTaps];  // {cr, ci}
-  u64 q[kTaps];  // {ci, cr}
-};
+// ------------------------------------------------------------- FIR math
 
-__device__ __forceinline__ void load_taps(const float* taps, Taps& tp) {
+// y[v] for the thread's 8 outputs; w*[i] holds sample (first output) - kPad + i.
+__device__ __forceinline__ void fir8(const float (&wr)[kWin], const float (&wi)[kWin],
+                                     const float4* __restrict__ taps, u64 (&y)[kPerThread]) {
+#pragma unroll
+  for (int v = 0; v < kPerThread; ++v) y[v] = pack2(0.0f, 0.0f);
 #pragma unroll
   for (int t = 0; t < kTaps; ++t) {
-    float cr = __ldg(taps + t), ci = __ldg(taps + kTaps + t);
-    tp.p[t] = pack2(cr, ci);
-    tp.q[t] = pack2(ci, cr);
-  }
-}
-
-// One output sample: returns {acc_r, acc_i} packed.  wr/wi index i holds
-// sample (first output of the thread) - kPad + i.
-template <int V>
-__device__ __forceinline__ u64 fir_point(const float (&wr)[kWin], const float (&wi)[kWin],
-                                         const Taps& tp) {
-  u64 acc = pack2(0.0f, 0.0f);
+    const float4 c = taps[t];
+    const u64 P = pack2(c.x, c.y);  // {cr, ci}
+    const u64 Q = pack2(c.z, c.w);  // {ci, cr}
 #pragma unroll
-  for (int t = 0; t < kTaps; ++t) {
-    const float xr = wr[kPad + V - t], xi = wi[kPad + V - t];
-    u64 P = fmul2(tp.p[t], pack2(xr, xr));  // {cr*xr, ci*xr}
-    u64 Q = fmul2(tp.q[t], pack2(xi, xi));  // {ci*xi, cr*xi}
-    float prr, pir, qii, qri;
-    unpack2(P, prr, pir);
-    unpack2(Q, qii, qri);
-    const float u = __fsub_rn(prr, qii);  // cr*xr - ci*xi
-    const float w = __fadd_rn(qri, pir);  // cr*xi + ci*xr
-    acc = fadd2(acc, pack2(u, w));
-  }
-  return acc;
-}
-
-template <int V>
-struct Unroll {
-  __device__ __forceinline__ static void run(const float (&wr)[kWin], const float (&wi)[kWin],
-                                             const Taps& tp, u64 (&y)[kPerThread]) {
-    Unroll<V - 1>::run(wr, wi, tp, y);
-    y[V - 1] = fir_point<V - 1>(wr, wi, tp);
-  }
-};
-template <>
-struct Unroll<0> {
-  __device__ __forceinline__ static void run(const float (&)[kWin], const float (&)[kWin],
-                                             const Taps&, u64 (&)[kPerThread]) {}
-};
-
-// Stage tile [t0, t0+kTile) of both planes (clamped to B) into shared memory
-// behind kPad halo slots.  Returns nothing; halo filled separately.
-__device__ __forceinline__ void stage_tile(const float* __restrict__ span, int64_t B, int t0,
-                                           float* sr, float* si) {
-  // 2 planes x kTile floats = 2*kTile/4 float4
-  const float4* pr = reinterpret_cast<const float4*>(span + t0);
-  const float4* pi = reinterpret_cast<const float4*>(span + B + t0);
-  const int64_t rem = B - t0;
-  const int n4 = (int)(rem < kTile ? rem : kTile) / 4;
-  for (int k = threadIdx.x; k < n4; k += kThreads) {
-    float4 a = __ldg(pr + k);
-    float4 b = __ldg(pi + k);
-    reinterpret_cast<float4*>(sr + kPad)[k] = a;
-    reinterpret_cast<float4*>(si + kPad)[k] = b;
+    for (int v = 0; v < kPerThread; ++v) {
+      const float xr = wr[kPad + v - t], xi = wi[kPad + v - t];
+      float prr, pir, qii, qri;
+      unpack2(fmul2(P, pack2(xr, xr)), prr, pir);  // {cr*xr, ci*xr}
+      unpack2(fmul2(Q, pack2(xi, xi)), qii, qri);  // {ci*xi, cr*xi}
+      y[v] = fadd2(y[v], pack2(__fsub_rn(prr, qii), __fadd_rn(qri, pir)));
+    }
   }
 }
 
-__device__ __forceinline__ void load_window(const float* sr, const float* si, float (&wr)[kWin],
+__device__ __forceinline__ void load_window(const StageBuf& sb, int ct, float (&wr)[kWin],
                                             float (&wi)[kWin]) {
-  const float4* a = reinterpret_cast<const float4*>(sr + kPerThread * threadIdx.x);
-  const float4* b = reinterpret_cast<const float4*>(si + kPerThread * threadIdx.x);
+  const float4* a = reinterpret_cast<const float4*>(sb.re + kPerThread * ct);
+  const float4* b = reinterpret_cast<const float4*>(sb.im + kPerThread * ct);
 #pragma unroll
   for (int k = 0; k < kWin / 4; ++k) {
-    float4 x = a[k], y = b[k];
+    float4 x = a[k], z = b[k];
     wr[4 * k + 0] = x.x; wr[4 * k + 1] = x.y; wr[4 * k + 2] = x.z; wr[4 * k + 3] = x.w;
-    wi[4 * k + 0] = y.x; wi[4 * k + 1] = y.y; wi[4 * k + 2] = y.z; wi[4 * k + 3] = y.w;
+    wi[4 * k + 0] = z.x; wi[4 * k + 1] = z.y; wi[4 * k + 2] = z.z; wi[4 * k + 3] = z.w;
   }
 }
 
-__device__ __forceinline__ void store_out(float* __restrict__ out, int64_t B, int n0,
-                                          const u64 (&y)[kPerThread]) {
+__device__ __forceinline__ void store8(float* out, int64_t B, int n0, const u64 (&y)[kPerThread]) {
   float r[kPerThread], i[kPerThread];
 #pragma unroll
   for (int v = 0; v < kPerThread; ++v) unpack2(y[v], r[v], i[v]);
@@ -140,8 +172,8 @@ __device__ __forceinline__ void store_out(float* __restrict__ out, int64_t B, in
   }
 }
 
-// History source of a fir_branch firing: state (first firing of the epoch) or
-// the last kHist samples of the actor's previous input span.
+// History of a fir_branch firing j: state (first firing of the epoch) or the
+// last kHist samples of the actor's previous input span.
 __device__ __forceinline__ void history_ptrs(const pb_fir_actor& a, const pb_resolved& res, int s,
                                              int j, int64_t B, const float*& hr,
                                              const float*& hi) {
@@ -149,60 +181,187 @@ __device__ __forceinline__ void history_ptrs(const pb_fir_actor& a, const pb_res
     hr = a.state + (int64_t)s * 2 * kHist;
     hi = hr + kHist;
   } else {
-    int np = pb::firing_iter(res, a.cond, s, j - 1);
+    const int np = pb::firing_iter(res, a.cond, s, j - 1);
     const float* prev = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, np));
     hr = prev + B - kHist;
     hi = prev + 2 * B - kHist;
   }
 }
 
-// ------------------------------------------------- per-actor batched firings
-
+// ---------------------------------------------------------------- kernel
+//
+// kBank = true : items (s, n, tile) of the fused route -> fir* -> branch_sum
+//                region; output = sum over active branches (combiner order)
+// kBank = false: items (actor, s, j, tile) of per-actor batched firings;
+//                output = the actor's own output span
+template <bool kBank>
 __global__ void __launch_bounds__(kThreads, 4)
-fir_kernel(const pb_fir_actor* __restrict__ actors, pb_resolved res, int64_t B, int tiles) {
-  const pb_fir_actor& a = actors[blockIdx.z];
-  const int s = blockIdx.y;
-  const int j = blockIdx.x / tiles;
-  const int tile = blockIdx.x % tiles;
-  if (j >= pb::cond_count(res, a.cond, s)) return;
-  const int n = pb::firing_iter(res, a.cond, s, j);
-  const int t0 = tile * kTile;
+fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actors, int n_actors,
+               pb_resolved res, int64_t B, int tiles) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  const pb_fir_actor* br = kBank ? bank.branches : actors;
+  const int nb = kBank ? bank.n_branches : n_actors;
 
-  __shared__ __align__(16) float sr[kPad + kTile];
-  __shared__ __align__(16) float si[kPad + kTile];
-
-  const float* in = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n));
-  float* out = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
-  stage_tile(in, B, t0, sr, si);
-  if (threadIdx.x < kHist) {
-    const int k = threadIdx.x;
-    float hr_v, hi_v;
-    if (t0 > 0) {
-      hr_v = in[t0 - kHist + k];
-      hi_v = in[B + t0 - kHist + k];
-    } else {
-      const float *hr, *hi;
-      history_ptrs(a, res, s, j, B, hr, hi);
-      hr_v = hr[k];
-      hi_v = hi[k];
-    }
-    sr[kPad - kHist + k] = hr_v;
-    si[kPad - kHist + k] = hi_v;
-  } else if (threadIdx.x < kPad) {
-    sr[threadIdx.x - kHist] = 0.f;
-    si[threadIdx.x - kHist] = 0.f;
+  for (int e = threadIdx.x; e < nb * kTaps; e += blockDim.x) {
+    const int b = e / kTaps, t = e % kTaps;
+    const float cr = br[b].taps[t], ci = br[b].taps[kTaps + t];
+    sm.taps[b][t] = make_float4(cr, ci, ci, cr);
   }
-  Taps tp;
-  load_taps(a.taps, tp);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kStages; ++k) {
+      mbar_init(&sm.full[k], 2);
+      mbar_init(&sm.empty[k], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
 
-  const int n0 = t0 + kPerThread * threadIdx.x;
-  if (n0 >= B) return;
-  float wr[kWin], wi[kWin];
-  load_window(sr, si, wr, wi);
-  u64 y[kPerThread];
-  Unroll<kPerThread>::run(wr, wi, tp, y);
-  store_out(out, B, n0, y);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t per_unit = (int64_t)res.n_iter * tiles;  // items per (actor, stream)
+  const int64_t total = (kBank ? 1 : (int64_t)n_actors) * res.n_streams * per_unit;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    int k = 0;
+    for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
+      bool have;
+      int a = 0, s, it, tile, n = 0;
+      {
+        int64_t r = w;
+        if (!kBank) {
+          a = (int)(r / ((int64_t)res.n_streams * per_unit));
+          r %= (int64_t)res.n_streams * per_unit;
+        }
+        s = (int)(r / per_unit);
+        r %= per_unit;
+        it = (int)(r / tiles);
+        tile = (int)(r % tiles);
+        if (kBank) {
+          n = it;
+          have = pb::active(res, bank.actor_cond, s, n);
+        } else {
+          have = it < pb::cond_count(res, actors[a].cond, s);
+          n = have ? pb::firing_iter(res, actors[a].cond, s, it) : 0;
+        }
+      }
+      if (have) {
+        const int stage = k % kStages;
+        const uint32_t phase = (k / kStages) & 1;
+        mbar_wait(&sm.empty[stage], phase ^ 1);
+        Desc& d = sm.desc[stage];
+        StageBuf& sb = sm.buf[stage];
+        const pb_span_ref& in_ref = kBank ? bank.in : actors[a].in;
+        const float* in = reinterpret_cast<const float*>(pb::span_ptr(in_ref, res, s, n));
+        const int t0 = tile * kTile;
+        const int64_t rem = B - t0;
+        const int len = (int)(rem < kTile ? rem : kTile);
+        if (lane == 0) {
+          const int lead = t0 > 0 ? kPad : 0;  // tile > 0: halo from the same span
+          const uint32_t bytes = (uint32_t)(len + lead) * 4u;
+          mbar_arrive_tx(&sm.full[stage], 2 * bytes);
+          bulk_g2s(sb.re + kPad - lead, in + t0 - lead, bytes, &sm.full[stage]);
+          bulk_g2s(sb.im + kPad - lead, in + B + t0 - lead, bytes, &sm.full[stage]);
+        }
+        // resolve the firing: active branches (lane b <-> branch b, combiner
+        // order) and their histories for the first tile
+        bool act = false;
+        int j = 0;
+        if (kBank) {
+          if (lane < nb) {
+            const pb_fir_actor& fa = br[lane];
+            act = pb::active(res, fa.cond, s, n);
+            if (act && t0 == 0)
+              j = fa.cond < 0 ? n
+                              : res.prefix[((int64_t)fa.cond * res.n_streams + s) * res.cap + n];
+          }
+        } else {
+          act = lane == 0;
+          j = it;
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, act);
+        if (act) {
+          const int rank = __popc(mask & ((1u << lane) - 1u));
+          d.br[rank] = (int8_t)(kBank ? lane : a);
+          if (t0 == 0) {
+            const float *hr, *hi;
+            history_ptrs(br[kBank ? lane : a], res, s, j, B, hr, hi);
+#pragma unroll
+            for (int q = 0; q < kHist; ++q) {
+              d.hist[rank][0][q] = hr[q];
+              d.hist[rank][1][q] = hi[q];
+            }
+          }
+        }
+        if (lane == 0) {
+          const pb_span_ref& out_ref = kBank ? bank.out : actors[a].out;
+          float* out = reinterpret_cast<float*>(pb::span_ptr(out_ref, res, s, n));
+          d.out = reinterpret_cast<u64>(out);
+          d.valid = 1;
+          d.t0 = t0;
+          d.n_act = __popc(mask);
+          d.first = t0 == 0;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.full[stage]);
+        ++k;
+      }
+    }
+    // terminator: consumers leave after the last produced stage
+    {
+      const int stage = k % kStages;
+      mbar_wait(&sm.empty[stage], ((k / kStages) & 1) ^ 1);
+      if (lane == 0) {
+        sm.desc[stage].valid = 0;
+        mbar_arrive_tx(&sm.full[stage], 0);
+        mbar_arrive(&sm.full[stage]);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int ct = threadIdx.x - 32;
+  for (int k = 0;; ++k) {
+    const int stage = k % kStages;
+    mbar_wait(&sm.full[stage], (k / kStages) & 1);
+    const Desc& d = sm.desc[stage];
+    if (!d.valid) break;
+    const int n0 = d.t0 + kPerThread * ct;
+    const int n_act = d.n_act;
+    float* out = reinterpret_cast<float*>(d.out);
+    if (n0 < B) {
+      float wr[kWin], wi[kWin];
+      load_window(sm.buf[stage], ct, wr, wi);
+      const bool patch = d.first && ct * kPerThread < kPad;
+      u64 acc[kPerThread];
+#pragma unroll
+      for (int v = 0; v < kPerThread; ++v) acc[v] = pack2(0.0f, 0.0f);
+      for (int r = 0; r < n_act; ++r) {
+        if (patch) {
+#pragma unroll
+          for (int i = 0; i < kPad; ++i) {
+            const int m = kPerThread * ct - kPad + i;  // sample index relative to the span
+            if (m < 0 && m >= -kHist) {
+              wr[i] = d.hist[r][0][m + kHist];
+              wi[i] = d.hist[r][1][m + kHist];
+            }
+          }
+        }
+        u64 y[kPerThread];
+        fir8(wr, wi, sm.taps[d.br[r]], y);
+        if (kBank) {
+#pragma unroll
+          for (int v = 0; v < kPerThread; ++v) acc[v] = fadd2(acc[v], y[v]);
+        } else {
+          store8(out, B, n0, y);
+        }
+      }
+      if (kBank) store8(out, B, n0, acc);
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.empty[stage]);
+  }
 }
 
 __global__ void fir_carry_kernel(const pb_fir_actor* __restrict__ actors, pb_resolved res,
@@ -217,94 +376,38 @@ __global__ void fir_carry_kernel(const pb_fir_actor* __restrict__ actors, pb_res
   a.state[(int64_t)s * 2 * kHist + plane * kHist + k] = in[plane * B + B - kHist + k];
 }
 
-// --------------------------------------------------------- fused filter bank
-
-__global__ void __launch_bounds__(kThreads, 4)
-filter_bank_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, int tiles) {
-  const int s = blockIdx.y;
-  const int n = blockIdx.x / tiles;
-  const int tile = blockIdx.x % tiles;
-  if (n >= res.n_iter) return;
-  if (!pb::active(res, bank.actor_cond, s, n)) return;
-  const int t0 = tile * kTile;
-
-  __shared__ __align__(16) float sr[kPad + kTile];
-  __shared__ __align__(16) float si[kPad + kTile];
-  __shared__ float hist[PB_MAX_BRANCHES][2][kHist];
-
-  const float* in = reinterpret_cast<const float*>(pb::span_ptr(bank.in, res, s, n));
-  float* out = reinterpret_cast<float*>(pb::span_ptr(bank.out, res, s, n));
-  stage_tile(in, B, t0, sr, si);
-  if (t0 > 0) {
-    if (threadIdx.x < kHist) {
-      const int k = threadIdx.x;
-      sr[kPad - kHist + k] = in[t0 - kHist + k];
-      si[kPad - kHist + k] = in[B + t0 - kHist + k];
-    }
-  } else {
-    // per-branch history: only branches active at this iteration matter
-    for (int e = threadIdx.x; e < bank.n_branches * 2 * kHist; e += kThreads) {
-      const int b = e / (2 * kHist), plane = (e / kHist) & 1, k = e % kHist;
-      const pb_fir_actor& a = bank.branches[b];
-      float v = 0.f;
-      if (pb::active(res, a.cond, s, n)) {
-        const int j = a.cond < 0 ? n
-                                 : res.prefix[((int64_t)a.cond * res.n_streams + s) * res.cap + n];
-        const float *hr, *hi;
-        history_ptrs(a, res, s, j, B, hr, hi);
-        v = plane ? hi[k] : hr[k];
-      }
-      hist[b][plane][k] = v;
-    }
-  }
-  if (threadIdx.x < kPad - kHist) {
-    sr[threadIdx.x] = 0.f;
-    si[threadIdx.x] = 0.f;
-  }
-  __syncthreads();
-
-  const int n0 = t0 + kPerThread * threadIdx.x;
-  if (n0 >= B) return;
-  float wr[kWin], wi[kWin];
-  load_window(sr, si, wr, wi);
-  // samples of the window that lie before the span start come from the
-  // branch's own history (tile 0, threads 0 and 1 only)
-  const bool patch = (n0 - kPad) < 0;
-
-  u64 sum[kPerThread];
-#pragma unroll
-  for (int v = 0; v < kPerThread; ++v) sum[v] = pack2(0.0f, 0.0f);
-
-  for (int b = 0; b < bank.n_branches; ++b) {
-    const pb_fir_actor& a = bank.branches[b];
-    if (!pb::active(res, a.cond, s, n)) continue;  // uniform across the CTA
-    if (patch) {
-#pragma unroll
-      for (int i = 0; i < kPad; ++i) {
-        const int m = n0 - kPad + i;  // sample index relative to span start
-        if (m < 0 && m >= -kHist) {
-          wr[i] = hist[b][0][m + kHist];
-          wi[i] = hist[b][1][m + kHist];
-        }
-      }
-    }
-    Taps tp;
-    load_taps(a.taps, tp);
-    u64 y[kPerThread];
-    Unroll<kPerThread>::run(wr, wi, tp, y);
-#pragma unroll
-    for (int v = 0; v < kPerThread; ++v) sum[v] = fadd2(sum[v], y[v]);
-  }
-  store_out(out, B, n0, sum);
+int check_block(int64_t B) {
+  if (B % kPerThread != 0 || B < kPad)
+    return pb::fail(PB_E_UNSUPPORTED, "fir_branch block length " + std::to_string(B) +
+                                          " must be a multiple of 8 and >= 12");
+  return PB_OK;
 }
 
-int check_span(int64_t span_bytes, int64_t* B) {
-  if (span_bytes % 8 != 0)
-    return pb::fail(PB_E_UNSUPPORTED, "fir_branch span must hold complex fp32 planes");
-  *B = span_bytes / 8;
-  if (*B % kPerThread != 0 || *B < kPad)
-    return pb::fail(PB_E_UNSUPPORTED, "fir_branch block length " + std::to_string(*B) +
-                                          " must be a multiple of 8 and >= 12");
+template <bool kBank>
+int launch(const pb_filter_bank& bank, const pb_fir_actor* actors, int n_actors,
+           const pb_resolved& res, int64_t B, cudaStream_t st) {
+  const int tiles = (int)((B + kTile - 1) / kTile);
+  const size_t smem = sizeof(Smem);
+  static bool configured = false;
+  if (!configured) {
+    PB_CUDA(cudaFuncSetAttribute(fir_persistent<kBank>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  static int sms = 0, per_sm = 0;
+  if (sms == 0) {
+    int dev = 0;
+    PB_CUDA(cudaGetDevice(&dev));
+    PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    PB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fir_persistent<kBank>,
+                                                          kThreads, smem));
+    per_sm = std::max(per_sm, 1);
+  }
+  const int64_t items =
+      (kBank ? 1 : (int64_t)n_actors) * res.n_streams * (int64_t)res.n_iter * tiles;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)sms * per_sm));
+  fir_persistent<kBank><<<grid, kThreads, smem, st>>>(bank, actors, n_actors, res, B, tiles);
+  PB_LAUNCHED(kBank ? "fir_persistent<bank>" : "fir_persistent<actors>");
   return PB_OK;
 }
 
@@ -315,14 +418,13 @@ extern "C" {
 int pb_fire_fir(const pb_fir_actor* actors, int n_actors, pb_resolved res, int64_t block,
                 void* stream) {
   if (n_actors == 0 || res.n_iter == 0) return PB_OK;
-  int64_t B = block;
-  int rc = check_span(block * 8, &B);
+  if (n_actors > kMaxBr)
+    return pb::fail(PB_E_UNSUPPORTED, "pb_fire_fir: at most " + std::to_string(kMaxBr) +
+                                          " actors per launch");
+  int rc = check_block(block);
   if (rc) return rc;
-  const int tiles = (int)((B + kTile - 1) / kTile);
-  dim3 grid((unsigned)(tiles * res.n_iter), res.n_streams, n_actors);
-  fir_kernel<<<grid, kThreads, 0, pb::as_stream(stream)>>>(actors, res, B, tiles);
-  PB_LAUNCHED("fir_kernel");
-  return PB_OK;
+  pb_filter_bank none{};
+  return launch<false>(none, actors, n_actors, res, block, pb::as_stream(stream));
 }
 
 int pb_fir_carry(const pb_fir_actor* actors, int n_actors, pb_resolved res, int64_t block,
@@ -336,17 +438,12 @@ int pb_fir_carry(const pb_fir_actor* actors, int n_actors, pb_resolved res, int6
 
 int pb_fire_filter_bank(pb_filter_bank bank, pb_resolved res, int64_t block, void* stream) {
   if (res.n_iter == 0) return PB_OK;
-  if (bank.n_branches < 1 || bank.n_branches > PB_MAX_BRANCHES)
-    return pb::fail(PB_E_UNSUPPORTED, "filter bank needs 1.." + std::to_string(PB_MAX_BRANCHES) +
+  if (bank.n_branches < 1 || bank.n_branches > kMaxBr)
+    return pb::fail(PB_E_UNSUPPORTED, "filter bank needs 1.." + std::to_string(kMaxBr) +
                                           " branches");
-  int64_t B = block;
-  int rc = check_span(block * 8, &B);
+  int rc = check_block(block);
   if (rc) return rc;
-  const int tiles = (int)((B + kTile - 1) / kTile);
-  dim3 grid((unsigned)(tiles * res.n_iter), res.n_streams);
-  filter_bank_kernel<<<grid, kThreads, 0, pb::as_stream(stream)>>>(bank, res, B, tiles);
-  PB_LAUNCHED("filter_bank_kernel");
-  return PB_OK;
+  return launch<true>(bank, nullptr, 0, res, block, pb::as_stream(stream));
 }
 
 }  // extern "C"

@@ -357,6 +357,12 @@ class DeviceRuntime:
                 fin = g.fifo_into(PortRef(aid, a.input_ports[0].id))
                 block = fin.rate * fin.token_bytes // 8
                 fir_by_level.setdefault((depth[aid], block), []).append(aid)
+        # one launch covers at most PB_MAX_BRANCHES actors
+        chunks: dict[tuple, list[str]] = {}
+        for (lvl, block), members in fir_by_level.items():
+            for c0 in range(0, len(members), _lib.PB_MAX_BRANCHES):
+                chunks[(lvl, block, c0)] = members[c0:c0 + _lib.PB_MAX_BRANCHES]
+        fir_by_level = {(k[0], k[1], k[2]): v for k, v in chunks.items()}
 
         for aid in plan.order:
             if aid in done or aid in self.fused_actors:

@@ -161,3 +161,26 @@ def test_crc32_matches_zlib():
     for text in [b"", b"conf", b"src", b"a much longer actor identifier"]:
         buf = C.create_string_buffer(text)
         assert lib.pb_crc32(buf, len(text)) == zlib.crc32(text)
+
+
+def test_no_fma_in_fir_kernels():
+    """Bit-exactness needs every FIR product rounded on its own: the SASS of
+    the FIR / filter-bank / sum / matmul kernels must hold no FFMA/FFMA2."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(tool).exists():
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True,
+                          check=True).stdout
+    fn, bad, seen = None, [], set()
+    for line in sass.splitlines():
+        if "Function :" in line:
+            fn = line.split("Function :")[1].strip()
+            continue
+        if fn and any(k in fn for k in ("fir_persistent", "branch_sum", "matmul")):
+            seen.add(fn)
+            if "FFMA" in line or "HFMA2.MMA" in line:
+                bad.append((fn, line.strip()))
+    assert len(seen) >= 4 and not bad, bad[:5]
+    assert "FMUL2" in sass and "FADD2" in sass
