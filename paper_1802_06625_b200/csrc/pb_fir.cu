@@ -42,7 +42,7 @@ constexpr int kPerThread = 8;                    // consecutive outputs per thre
 constexpr int kTile = kConsumers * kPerThread;   // outputs per work item
 constexpr int kPad = 12;                         // halo slots in front of the tile (>= 9, x4)
 constexpr int kWin = kPerThread + kPad;          // per-thread window (20 samples)
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr int kMaxBr = PB_MAX_BRANCHES;
 
 struct __align__(16) StageBuf {
@@ -172,22 +172,6 @@ __device__ __forceinline__ void store8(float* out, int64_t B, int n0, const u64 
   }
 }
 
-// History of a fir_branch firing j: state (first firing of the epoch) or the
-// last kHist samples of the actor's previous input span.
-__device__ __forceinline__ void history_ptrs(const pb_fir_actor& a, const pb_resolved& res, int s,
-                                             int j, int64_t B, const float*& hr,
-                                             const float*& hi) {
-  if (j == 0) {
-    hr = a.state + (int64_t)s * 2 * kHist;
-    hi = hr + kHist;
-  } else {
-    const int np = pb::firing_iter(res, a.cond, s, j - 1);
-    const float* prev = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, np));
-    hr = prev + B - kHist;
-    hi = prev + 2 * B - kHist;
-  }
-}
-
 // ---------------------------------------------------------------- kernel
 //
 // kBank = true : items (s, n, tile) of the fused route -> fir* -> branch_sum
@@ -223,89 +207,116 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
+    // Contiguous tile range per CTA: the tiles of one span are consecutive,
+    // so a span's firing (active branches, histories) is resolved once, and
+    // consecutive spans of one stream let each lane track when its branch
+    // last fired (its history source) without global lookups.
+    const int64_t w0 = total * blockIdx.x / gridDim.x;
+    const int64_t w1 = total * (blockIdx.x + 1) / gridDim.x;
     int k = 0;
-    for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
-      bool have;
-      int a = 0, s, it, tile, n = 0;
-      {
-        int64_t r = w;
-        if (!kBank) {
-          a = (int)(r / ((int64_t)res.n_streams * per_unit));
-          r %= (int64_t)res.n_streams * per_unit;
-        }
-        s = (int)(r / per_unit);
-        r %= per_unit;
-        it = (int)(r / tiles);
-        tile = (int)(r % tiles);
+    int64_t cur_unit = -1;
+    int cur_it = -1;
+    int n = 0;
+    bool have = false;
+    unsigned mask = 0;
+    int prev_n = -2;   // lane b: iteration branch b last fired at (-1: none yet, -2: unknown)
+    for (int64_t w = w0; w < w1; ++w) {
+      int64_t r = w;
+      int a = 0;
+      if (!kBank) {
+        a = (int)(r / ((int64_t)res.n_streams * per_unit));
+        r %= (int64_t)res.n_streams * per_unit;
+      }
+      const int s = (int)(r / per_unit);
+      r %= per_unit;
+      const int it = (int)(r / tiles);
+      const int tile = (int)(r % tiles);
+      const int64_t unit = (int64_t)a * res.n_streams + s;
+      if (unit != cur_unit || it != cur_it) {
+        // ---- new span: resolve its firing
+        if (unit != cur_unit) prev_n = -2;
+        cur_unit = unit;
+        cur_it = it;
+        bool act = false;
         if (kBank) {
           n = it;
           have = pb::active(res, bank.actor_cond, s, n);
+          if (have && lane < nb) act = pb::active(res, br[lane].cond, s, n);
         } else {
           have = it < pb::cond_count(res, actors[a].cond, s);
           n = have ? pb::firing_iter(res, actors[a].cond, s, it) : 0;
+          act = have && lane == 0;
         }
+        mask = __ballot_sync(0xffffffffu, act);
       }
-      if (have) {
-        const int stage = k % kStages;
-        const uint32_t phase = (k / kStages) & 1;
-        mbar_wait(&sm.empty[stage], phase ^ 1);
-        Desc& d = sm.desc[stage];
-        StageBuf& sb = sm.buf[stage];
-        const pb_span_ref& in_ref = kBank ? bank.in : actors[a].in;
-        const float* in = reinterpret_cast<const float*>(pb::span_ptr(in_ref, res, s, n));
-        const int t0 = tile * kTile;
-        const int64_t rem = B - t0;
-        const int len = (int)(rem < kTile ? rem : kTile);
-        if (lane == 0) {
-          const int lead = t0 > 0 ? kPad : 0;  // tile > 0: halo from the same span
-          const uint32_t bytes = (uint32_t)(len + lead) * 4u;
-          mbar_arrive_tx(&sm.full[stage], 2 * bytes);
-          bulk_g2s(sb.re + kPad - lead, in + t0 - lead, bytes, &sm.full[stage]);
-          bulk_g2s(sb.im + kPad - lead, in + B + t0 - lead, bytes, &sm.full[stage]);
-        }
-        // resolve the firing: active branches (lane b <-> branch b, combiner
-        // order) and their histories for the first tile
-        bool act = false;
-        int j = 0;
-        if (kBank) {
-          if (lane < nb) {
-            const pb_fir_actor& fa = br[lane];
-            act = pb::active(res, fa.cond, s, n);
-            if (act && t0 == 0)
-              j = fa.cond < 0 ? n
-                              : res.prefix[((int64_t)fa.cond * res.n_streams + s) * res.cap + n];
+      if (!have) continue;
+      const int stage = k % kStages;
+      mbar_wait(&sm.empty[stage], ((k / kStages) & 1) ^ 1);
+      Desc& d = sm.desc[stage];
+      StageBuf& sb = sm.buf[stage];
+      const pb_span_ref& in_ref = kBank ? bank.in : actors[a].in;
+      const float* in = reinterpret_cast<const float*>(pb::span_ptr(in_ref, res, s, n));
+      const int t0 = tile * kTile;
+      const int64_t rem = B - t0;
+      const int len = (int)(rem < kTile ? rem : kTile);
+      if (lane == 0) {
+        const int lead = t0 > 0 ? kPad : 0;  // tile > 0: halo from the same span
+        const uint32_t bytes = (uint32_t)(len + lead) * 4u;
+        mbar_arrive_tx(&sm.full[stage], 2 * bytes);
+        bulk_g2s(sb.re + kPad - lead, in + t0 - lead, bytes, &sm.full[stage]);
+        bulk_g2s(sb.im + kPad - lead, in + B + t0 - lead, bytes, &sm.full[stage]);
+      }
+      const bool act = (mask >> lane) & 1u;
+      if (act) {
+        const int rank = __popc(mask & ((1u << lane) - 1u));
+        d.br[rank] = (int8_t)(kBank ? lane : a);
+        if (t0 == 0) {
+          const pb_fir_actor& fa = br[kBank ? lane : a];
+          int src = prev_n;  // iteration of the branch's previous firing
+          if (src == -2) {
+            const int j = kBank ? (fa.cond < 0 ? n
+                                   : res.prefix[((int64_t)fa.cond * res.n_streams + s) * res.cap + n])
+                                : it;
+            src = j == 0 ? -1 : pb::firing_iter(res, fa.cond, s, j - 1);
           }
-        } else {
-          act = lane == 0;
-          j = it;
-        }
-        const unsigned mask = __ballot_sync(0xffffffffu, act);
-        if (act) {
-          const int rank = __popc(mask & ((1u << lane) - 1u));
-          d.br[rank] = (int8_t)(kBank ? lane : a);
-          if (t0 == 0) {
-            const float *hr, *hi;
-            history_ptrs(br[kBank ? lane : a], res, s, j, B, hr, hi);
+          const float *hr, *hi;
+          if (src < 0) {
+            hr = fa.state + (int64_t)s * 2 * kHist;
+            hi = hr + kHist;
+          } else {
+            const float* prev = reinterpret_cast<const float*>(pb::span_ptr(fa.in, res, s, src));
+            hr = prev + B - kHist;
+            hi = prev + 2 * B - kHist;
+          }
+          float h[2 * kHist];
 #pragma unroll
-            for (int q = 0; q < kHist; ++q) {
-              d.hist[rank][0][q] = hr[q];
-              d.hist[rank][1][q] = hi[q];
-            }
+          for (int q = 0; q < kHist; ++q) {
+            h[q] = hr[q];
+            h[kHist + q] = hi[q];
+          }
+#pragma unroll
+          for (int q = 0; q < kHist; ++q) {
+            d.hist[rank][0][q] = h[q];
+            d.hist[rank][1][q] = h[kHist + q];
           }
         }
-        if (lane == 0) {
-          const pb_span_ref& out_ref = kBank ? bank.out : actors[a].out;
-          float* out = reinterpret_cast<float*>(pb::span_ptr(out_ref, res, s, n));
-          d.out = reinterpret_cast<u64>(out);
-          d.valid = 1;
-          d.t0 = t0;
-          d.n_act = __popc(mask);
-          d.first = t0 == 0;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.full[stage]);
-        ++k;
       }
+      if (lane == 0) {
+        const pb_span_ref& out_ref = kBank ? bank.out : actors[a].out;
+        float* out = reinterpret_cast<float*>(pb::span_ptr(out_ref, res, s, n));
+        d.out = reinterpret_cast<u64>(out);
+        d.valid = 1;
+        d.t0 = t0;
+        d.n_act = __popc(mask);
+        d.first = t0 == 0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.full[stage]);
+      // the span's last tile: its active branches have now fired at n
+      if (tile == tiles - 1 || w + 1 == w1) {
+        if (act) prev_n = n;
+      }
+      ++k;
     }
     // terminator: consumers leave after the last produced stage
     {
