@@ -233,6 +233,8 @@ typedef struct {
   const pb_fir_actor* branches;      /* device array, combiner sorted port order */
   int32_t n_branches;
   int32_t actor_cond;                /* condition of route/combiner (-1) */
+  uint32_t* sched;                   /* device uint32[2], zeroed once: dynamic work
+                                        counter reset by the last CTA; NULL = static */
 } pb_filter_bank;
 int pb_fire_filter_bank(pb_filter_bank bank, pb_resolved res, int64_t block, void* stream);
 

@@ -71,7 +71,7 @@ class FirActor(C.Structure):
 
 class FilterBank(C.Structure):
     _fields_ = [("in_", SpanRef), ("out", SpanRef), ("branches", vp), ("n_branches", i32),
-                ("actor_cond", i32)]
+                ("actor_cond", i32), ("sched", vp)]
 
 
 class SumActor(C.Structure):

@@ -44,6 +44,7 @@ constexpr int kPad = 12;                         // halo slots in front of the t
 constexpr int kWin = kPerThread + kPad;          // per-thread window (20 samples)
 constexpr int kStages = 4;
 constexpr int kMaxBr = PB_MAX_BRANCHES;
+constexpr int kChunkSpans = 4;               // spans per dynamic work grab
 
 struct __align__(16) StageBuf {
   float re[kPad + kTile];
@@ -211,8 +212,13 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
     // so a span's firing (active branches, histories) is resolved once, and
     // consecutive spans of one stream let each lane track when its branch
     // last fired (its history source) without global lookups.
-    const int64_t w0 = total * blockIdx.x / gridDim.x;
-    const int64_t w1 = total * (blockIdx.x + 1) / gridDim.x;
+    // Bank launches with a scheduler pointer grab chunks of kChunkSpans spans
+    // dynamically (the active-branch count per span varies 1..K, so static
+    // ranges leave a tail); otherwise each CTA takes one contiguous range.
+    const bool dynamic = kBank && bank.sched != nullptr;
+    const int64_t chunk = dynamic ? (int64_t)kChunkSpans * tiles : 0;
+    int64_t w0 = total * blockIdx.x / gridDim.x;
+    int64_t w1 = total * (blockIdx.x + 1) / gridDim.x;
     int k = 0;
     int64_t cur_unit = -1;
     int cur_it = -1;
@@ -220,6 +226,16 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
     bool have = false;
     unsigned mask = 0;
     int prev_n = -2;   // lane b: iteration branch b last fired at (-1: none yet, -2: unknown)
+    for (;;) {
+    if (dynamic) {
+      int64_t c = 0;
+      if (lane == 0) c = atomicAdd(bank.sched, 1u);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      w0 = c * chunk;
+      if (w0 >= total) break;
+      w1 = min(total, w0 + chunk);
+      cur_unit = -1;   // chunks are not contiguous with the previous one
+    }
     for (int64_t w = w0; w < w1; ++w) {
       int64_t r = w;
       int a = 0;
@@ -317,6 +333,18 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
         if (act) prev_n = n;
       }
       ++k;
+    }
+    if (!dynamic) break;
+    }
+    if (dynamic && lane == 0) {
+      // the last CTA out resets the scheduler for the next launch
+      __threadfence();
+      const unsigned done = atomicAdd(bank.sched + 1, 1u);
+      if (done == gridDim.x - 1) {
+        bank.sched[0] = 0;
+        bank.sched[1] = 0;
+        __threadfence();
+      }
     }
     // terminator: consumers leave after the last produced stage
     {

@@ -384,7 +384,8 @@ class DeviceRuntime:
                     arr[k] = self._fir_actor(bid, fin.id, None)
                 dev = self.mem.upload(np.frombuffer(bytes(arr), dtype=np.uint8))
                 bank = _lib.FilterBank(self._ref(fin.id), self._ref(fout.id), dev,
-                                       len(grp.branches), plan.actor_cond[aid])
+                                       len(grp.branches), plan.actor_cond[aid],
+                                       self.mem.malloc(16))
                 block = fin.rate * fin.token_bytes // 8
                 self.launches.append(("bank", bank, block))
                 self.fir_groups.append((dev, len(grp.branches), block))
