@@ -82,6 +82,9 @@ int pb_event_create(void** event);
 int pb_event_destroy(void* event);
 int pb_event_record(void* event, void* stream);
 int pb_event_elapsed_ms(void* start, void* end, float* ms);
+int pb_event_sync(void* event);
+/* make `stream` wait for `event` (cudaStreamWaitEvent) */
+int pb_stream_wait(void* stream, void* event);
 /* Number of device kernels this library has launched (process lifetime). */
 int64_t pb_launch_count(void);
 

@@ -118,6 +118,8 @@ SIGNATURES = {
     "pb_event_destroy": (C.c_int, [vp]),
     "pb_event_record": (C.c_int, [vp, vp]),
     "pb_event_elapsed_ms": (C.c_int, [vp, vp, C.POINTER(C.c_float)]),
+    "pb_event_sync": (C.c_int, [vp]),
+    "pb_stream_wait": (C.c_int, [vp, vp]),
     "pb_launch_count": (i64, []),
     "pb_layout_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(Plan)]),
     "pb_writer_gate": (i64, [i64, C.c_int, C.c_int, C.c_int, C.c_int]),

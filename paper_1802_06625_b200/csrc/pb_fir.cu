@@ -25,7 +25,10 @@
 //            branch over 8 consecutive outputs per thread, sum (bank) or
 //            store per branch, release the stage.
 // kStages stages keep the next tiles in flight while the FP32 pipe works.
+#include <stdlib.h>
+
 #include <algorithm>
+#include <string>
 
 #include "pb_common.cuh"
 
@@ -89,13 +92,16 @@ __device__ __forceinline__ void mbar_arrive_tx(u64* bar, uint32_t bytes) {
       "r"(bytes)
       : "memory");
 }
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the
+// phase completes (or the hint elapses) instead of spinning on issue slots
+// the FP32 consumers need.
 __device__ __forceinline__ void mbar_wait(u64* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, u64* bar) {
@@ -148,6 +154,28 @@ __device__ __forceinline__ void fir8(const float (&wr)[kWin], const float (&wi)[
   }
 }
 
+// Same roundings with scalar FMUL/FADD only (8 issue slots per tap-output
+// instead of 5, same FP32 pipe cycles); selected with kScalarMath.
+__device__ __forceinline__ void fir8_scalar(const float (&wr)[kWin], const float (&wi)[kWin],
+                                            const float4* __restrict__ taps,
+                                            u64 (&y)[kPerThread]) {
+  float yr[kPerThread], yi[kPerThread];
+#pragma unroll
+  for (int v = 0; v < kPerThread; ++v) yr[v] = yi[v] = 0.0f;
+#pragma unroll
+  for (int t = 0; t < kTaps; ++t) {
+    const float4 c = taps[t];
+#pragma unroll
+    for (int v = 0; v < kPerThread; ++v) {
+      const float xr = wr[kPad + v - t], xi = wi[kPad + v - t];
+      yr[v] = __fadd_rn(yr[v], __fsub_rn(__fmul_rn(c.x, xr), __fmul_rn(c.y, xi)));
+      yi[v] = __fadd_rn(yi[v], __fadd_rn(__fmul_rn(c.x, xi), __fmul_rn(c.y, xr)));
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < kPerThread; ++v) y[v] = pack2(yr[v], yi[v]);
+}
+
 __device__ __forceinline__ void load_window(const StageBuf& sb, int ct, float (&wr)[kWin],
                                             float (&wi)[kWin]) {
   const float4* a = reinterpret_cast<const float4*>(sb.re + kPerThread * ct);
@@ -179,7 +207,7 @@ __device__ __forceinline__ void store8(float* out, int64_t B, int n0, const u64 
 //                region; output = sum over active branches (combiner order)
 // kBank = false: items (actor, s, j, tile) of per-actor batched firings;
 //                output = the actor's own output span
-template <bool kBank>
+template <bool kBank, bool kScalarMath>
 __global__ void __launch_bounds__(kThreads, 4)
 fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actors, int n_actors,
                pb_resolved res, int64_t B, int tiles) {
@@ -388,7 +416,10 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
           }
         }
         u64 y[kPerThread];
-        fir8(wr, wi, sm.taps[d.br[r]], y);
+        if (kScalarMath)
+          fir8_scalar(wr, wi, sm.taps[d.br[r]], y);
+        else
+          fir8(wr, wi, sm.taps[d.br[r]], y);
         if (kBank) {
 #pragma unroll
           for (int v = 0; v < kPerThread; ++v) acc[v] = fadd2(acc[v], y[v]);
@@ -422,14 +453,14 @@ int check_block(int64_t B) {
   return PB_OK;
 }
 
-template <bool kBank>
-int launch(const pb_filter_bank& bank, const pb_fir_actor* actors, int n_actors,
-           const pb_resolved& res, int64_t B, cudaStream_t st) {
+template <bool kBank, bool kScalarMath>
+int launch_variant(const pb_filter_bank& bank, const pb_fir_actor* actors, int n_actors,
+                   const pb_resolved& res, int64_t B, cudaStream_t st) {
   const int tiles = (int)((B + kTile - 1) / kTile);
   const size_t smem = sizeof(Smem);
   static bool configured = false;
   if (!configured) {
-    PB_CUDA(cudaFuncSetAttribute(fir_persistent<kBank>,
+    PB_CUDA(cudaFuncSetAttribute(fir_persistent<kBank, kScalarMath>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
@@ -438,16 +469,33 @@ int launch(const pb_filter_bank& bank, const pb_fir_actor* actors, int n_actors,
     int dev = 0;
     PB_CUDA(cudaGetDevice(&dev));
     PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    PB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fir_persistent<kBank>,
+    PB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fir_persistent<kBank, kScalarMath>,
                                                           kThreads, smem));
     per_sm = std::max(per_sm, 1);
   }
   const int64_t items =
       (kBank ? 1 : (int64_t)n_actors) * res.n_streams * (int64_t)res.n_iter * tiles;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)sms * per_sm));
-  fir_persistent<kBank><<<grid, kThreads, smem, st>>>(bank, actors, n_actors, res, B, tiles);
+  fir_persistent<kBank, kScalarMath><<<grid, kThreads, smem, st>>>(bank, actors, n_actors, res, B, tiles);
   PB_LAUNCHED(kBank ? "fir_persistent<bank>" : "fir_persistent<actors>");
   return PB_OK;
+}
+
+// PB_FIR_MATH=scalar selects the scalar FMUL/FADD mix (A/B measurements).
+bool scalar_math() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PB_FIR_MATH");
+    v = (e && std::string(e) == "scalar") ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <bool kBank>
+int launch(const pb_filter_bank& bank, const pb_fir_actor* actors, int n_actors,
+           const pb_resolved& res, int64_t B, cudaStream_t st) {
+  return scalar_math() ? launch_variant<kBank, true>(bank, actors, n_actors, res, B, st)
+                       : launch_variant<kBank, false>(bank, actors, n_actors, res, B, st);
 }
 
 }  // namespace

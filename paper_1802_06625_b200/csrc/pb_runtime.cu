@@ -163,6 +163,16 @@ int pb_event_elapsed_ms(void* start, void* end, float* ms) {
   return PB_OK;
 }
 
+int pb_event_sync(void* event) {
+  PB_CUDA(cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(event)));
+  return PB_OK;
+}
+
+int pb_stream_wait(void* stream, void* event) {
+  PB_CUDA(cudaStreamWaitEvent(pb::as_stream(stream), reinterpret_cast<cudaEvent_t>(event), 0));
+  return PB_OK;
+}
+
 // ------------------------------------------------------------ capacity plan
 
 int pb_layout_plan(int rate, int delay, int factor, int token_bytes, pb_plan* out) {

@@ -59,6 +59,7 @@ class RuntimeConfig:
     fuse: bool = True             # fire route -> fir_branch* -> branch_sum as one kernel
     device: int = 0
     host_threads: int = 0         # threads for native policies and digests (0 = all)
+    pipeline: int = 8             # sub-epochs overlapping H2D / kernels / D2H / hashing (1 = off)
 
 
 @dataclass
@@ -194,6 +195,10 @@ class DeviceRuntime:
         st = C.c_void_p()
         _lib.check(lib.pb_stream_create(C.byref(st)), "pb_stream_create")
         self.stream = st.value
+        for name in ("copy_in", "copy_out"):
+            _lib.check(lib.pb_stream_create(C.byref(st)), "pb_stream_create")
+            setattr(self, name, st.value)
+        self._events: list[int] = []
 
         # device behaviours must be device kernels
         for a in g.actors:
@@ -482,29 +487,34 @@ class DeviceRuntime:
                                     c.element - 1, self.C, it0 % self.C)
         return arr
 
-    def _h2d_chunks(self, dev: int, stride: int, span: int, host: int, E: int, first: int):
-        """host [S][E][span] -> device ring chunks (first + n) % C of every stream."""
+    def _h2d_chunks(self, dev: int, stride: int, span: int, host: int, E: int, first: int,
+                    host_pitch: int | None = None, stream: int | None = None):
+        """host rows [S][E spans] (row pitch host_pitch) -> device ring chunks
+        (first + n) % C of every stream."""
         lib, S, C_ = self.lib, self.n_streams, self.C
+        st = self.stream if stream is None else stream
+        hp = E * span if host_pitch is None else host_pitch
         a = first % C_
         n1 = min(E, C_ - a)
-        if n1 == C_ and stride == C_ * span:
-            _lib.check(lib.pb_memcpy_h2d(dev, host, S * E * span, self.stream))
+        if n1 == C_ and stride == C_ * span and hp == E * span:
+            _lib.check(lib.pb_memcpy_h2d(dev, host, S * E * span, st))
             return
-        _lib.check(lib.pb_memcpy_2d(dev + a * span, stride, host, E * span, n1 * span, S, 1,
-                                    self.stream))
+        _lib.check(lib.pb_memcpy_2d(dev + a * span, stride, host, hp, n1 * span, S, 1, st))
         if n1 < E:
-            _lib.check(lib.pb_memcpy_2d(dev, stride, host + n1 * span, E * span, (E - n1) * span,
-                                        S, 1, self.stream))
+            _lib.check(lib.pb_memcpy_2d(dev, stride, host + n1 * span, hp, (E - n1) * span,
+                                        S, 1, st))
 
-    def _d2h_chunks(self, dev: int, stride: int, span: int, host: int, E: int, first: int):
+    def _d2h_chunks(self, dev: int, stride: int, span: int, host: int, E: int, first: int,
+                    host_pitch: int | None = None, stream: int | None = None):
         lib, S, C_ = self.lib, self.n_streams, self.C
+        st = self.stream if stream is None else stream
+        hp = E * span if host_pitch is None else host_pitch
         a = first % C_
         n1 = min(E, C_ - a)
-        _lib.check(lib.pb_memcpy_2d(host, E * span, dev + a * span, stride, n1 * span, S, 2,
-                                    self.stream))
+        _lib.check(lib.pb_memcpy_2d(host, hp, dev + a * span, stride, n1 * span, S, 2, st))
         if n1 < E:
-            _lib.check(lib.pb_memcpy_2d(host + n1 * span, E * span, dev, stride,
-                                        (E - n1) * span, S, 2, self.stream))
+            _lib.check(lib.pb_memcpy_2d(host + n1 * span, hp, dev, stride,
+                                        (E - n1) * span, S, 2, st))
 
     def source_staging(self, actor: str, port: str | None = None) -> np.ndarray:
         """Pinned host buffer [S][epoch][span] a source's spans are copied from;
@@ -776,6 +786,178 @@ class DeviceRuntime:
         self.firings = {a.id: np.zeros(S, dtype=np.int64) for a in g.actors}
         _lib.check(lib.pb_stream_sync(self.stream), "reset")
 
+    # ------------------------------------------------------ pipelined run
+
+    def _pipelinable(self, prestaged: bool) -> bool:
+        """Bulk-only graphs (bulk sources, native policies, single-port
+        always-active digest sinks) run with overlapped copies and hashing."""
+        g = self.graph
+        if self.config.trace is not None or self.config.pipeline == 1:
+            return False
+        for a in g.actors:
+            role = self.plan.roles[a.id]
+            b = self.behaviors[0][a.id]
+            if role == "source":
+                if len(a.output_ports) != 1:
+                    return False
+                if not (prestaged or a.id in self.sources or type(b) is FileSource):
+                    return False
+            elif role == "config":
+                ctl = [p for p in a.output_ports if p.kind == CONTROL_OUT]
+                if native_policy_kind(b) is None or len(ctl) != 1 or len(a.output_ports) != 1:
+                    return False
+            elif role == "sink":
+                if len(a.input_ports) != 1 or self.plan.actor_cond[a.id] != ALWAYS:
+                    return False
+                if type(b).fire is not type(resolve("null_sink")).fire:
+                    return False
+        return True
+
+    def _event(self) -> int:
+        e = C.c_void_p()
+        _lib.check(self.lib.pb_event_create(C.byref(e)))
+        self._events.append(e.value)
+        return e.value
+
+    def _run_pipelined(self, prestaged: bool, N: int, deadline) -> None:
+        """Sub-epoch software pipeline over three CUDA streams:
+
+            copy-in  : H2D of chunk c's source spans and control tokens
+            compute  : resolve + actor launches + carry + advance of chunk c
+            copy-out : D2H of chunk c's sink spans
+            host     : SHA-256 of chunk c per stream (hashlib releases the GIL)
+
+        Chunk c+R reuses chunk c's ring chunks and host window slots (R =
+        epoch // sub), so each stage waits on the matching event of c-R.
+        """
+        lib, g, S = self.lib, self.graph, self.n_streams
+        E = self.epoch
+        depth = int(self.config.pipeline) if self.config.pipeline > 1 else 8
+        sub = max(1, E // depth)
+        while E % sub:
+            sub -= 1
+        R = E // sub
+        chunks = [(it, min(sub, N - it)) for it in range(0, N, sub)]
+        self._events = []
+        h2d_ev = [self._event() for _ in chunks]
+        comp_ev = [self._event() for _ in chunks]
+        d2h_ev = [self._event() for _ in chunks]
+        n_cond = len(self.plan.conds)
+        counts = np.zeros((len(chunks), max(1, n_cond), S), dtype=np.int32)
+        src = [(a, sorted(g.fifos_from(PortRef(a.id, a.output_ports[0].id)),
+                          key=lambda f: f.id)[0])
+               for a in g.actors if self.plan.roles[a.id] == "source"]
+        sinks = [(a, g.fifo_into(PortRef(a.id, a.input_ports[0].id)))
+                 for a in g.actors if self.plan.roles[a.id] == "sink"]
+        hash_pool = self.pool
+        coord = ThreadPoolExecutor(max_workers=1)
+        hash_done = []
+
+        def hash_chunk(c, it0, n):
+            _lib.check(lib.pb_event_sync(d2h_ev[c]))
+            w = it0 % E
+
+            def one(job):
+                a, f, s = job
+                span = f.rate * f.token_bytes
+                arr = self.sink_host[f.id][1][:S * E * span].reshape(S, E, span)
+                data = arr[s, w:w + n].reshape(-1)
+                self.digests[a.id][s].update(data)
+                if self.captured is not None:
+                    self.captured[a.id][s].extend(data.tobytes())
+            list(hash_pool.map(one, [(a, f, s) for a, f in sinks for s in range(S)]))
+
+        try:
+            for c, (it0, n) in enumerate(chunks):
+                w = it0 % E
+                if c >= R:
+                    _lib.check(lib.pb_event_sync(h2d_ev[c - R]))       # host window reuse
+                    _lib.check(lib.pb_stream_wait(self.copy_in, comp_ev[c - R]))
+                # sources
+                for a, f in src:
+                    span = f.rate * f.token_bytes
+                    hptr, harr = self.src_host[f"{a.id}.{a.output_ports[0].id}"]
+                    if not prestaged:
+                        buf = harr[:S * E * span].reshape(S, E, span)
+                        for s in range(S):
+                            if a.id in self.sources:
+                                data = np.frombuffer(memoryview(self.sources[a.id][s]).cast("B"),
+                                                     dtype=np.uint8)[it0 * span:(it0 + n) * span]
+                            else:
+                                try:
+                                    data = np.frombuffer(self.behaviors[s][a.id].take(
+                                        a.id, n * span), dtype=np.uint8)
+                                except EOFError as e:
+                                    raise ActorPanic(a.id, e) from e
+                            if data.size < n * span:
+                                raise ActorPanic(a.id, EOFError(
+                                    f"{a.id}: input exhausted at byte {it0 * span + data.size}"))
+                            buf[s, w:w + n] = data.reshape(n, span)
+                    st = self.storage[f.id]
+                    self._h2d_chunks(st.data, st.stream_stride, span, hptr + w * span, n, it0,
+                                     host_pitch=E * span, stream=self.copy_in)
+                # control tokens (native generators), dense per chunk slot
+                for ref in self.ctl_ports:
+                    a = g.actor(ref.actor)
+                    stride = self.ctl_stride[ref]
+                    hptr, harr = self.ctl_host[ref]
+                    b0 = self.behaviors[0][a.id]
+                    min_tb = min(f.token_bytes for f in g.fifos_from(ref))
+                    try:
+                        length = int(a.params["length"])
+                        param = b0.native_param(a.params)
+                        if length > min_tb:
+                            raise ValueError(f"{length} control elements exceed {min_tb} bytes")
+                    except Exception as e:  # noqa: BLE001
+                        raise ActorPanic(a.id, e) from e
+                    slot = hptr + (c % R) * S * sub * stride
+                    rc = lib.pb_policy_tokens_streams(
+                        C.addressof(self.policy_state[ref]), S, native_policy_kind(b0), length,
+                        param, it0, n, slot, stride, int(self.config.host_threads))
+                    if rc != _lib.PB_OK:
+                        raise ActorPanic(a.id, ValueError(_lib.error_text()))
+                    self._h2d_chunks(self.ctl_dev[ref], self.C * stride, stride, slot, n, it0,
+                                     stream=self.copy_in)
+                _lib.check(lib.pb_event_record(h2d_ev[c], self.copy_in))
+                # compute
+                _lib.check(lib.pb_stream_wait(self.stream, h2d_ev[c]))
+                if c >= R:
+                    _lib.check(lib.pb_stream_wait(self.stream, d2h_ev[c - R]))
+                self.fire_epoch(it0, n)
+                if n_cond:
+                    _lib.check(lib.pb_memcpy_d2h(counts[c].ctypes.data, self.res_count,
+                                                 n_cond * S * 4, self.stream))
+                _lib.check(lib.pb_event_record(comp_ev[c], self.stream))
+                # copy out (the host window slot must have been hashed)
+                if c >= R:
+                    hash_done[c - R].result()
+                _lib.check(lib.pb_stream_wait(self.copy_out, comp_ev[c]))
+                for a, f in sinks:
+                    st = self.storage[f.id]
+                    span = f.rate * f.token_bytes
+                    hptr = self.sink_host[f.id][0]
+                    self._d2h_chunks(st.data, st.stream_stride, span, hptr + w * span, n, it0,
+                                     host_pitch=E * span, stream=self.copy_out)
+                _lib.check(lib.pb_event_record(d2h_ev[c], self.copy_out))
+                hash_done.append(coord.submit(hash_chunk, c, it0, n))
+                if deadline is not None and time.perf_counter() > deadline and c + 1 < len(chunks):
+                    raise Timeout(self.config.timeout_ms, sorted(a.id for a in g.actors))
+            for fut in hash_done:
+                fut.result()
+        finally:
+            coord.shutdown(wait=True)
+            lib.pb_stream_sync(self.copy_in)
+            lib.pb_stream_sync(self.stream)
+            lib.pb_stream_sync(self.copy_out)
+            for e in self._events:
+                lib.pb_event_destroy(e)
+            self._events = []
+        self._check_device_errors()
+        for c, (it0, n) in enumerate(chunks):
+            for a in g.actors:
+                cc = self.plan.actor_cond[a.id]
+                self.firings[a.id] += n if cc == ALWAYS else counts[c, cc]
+
     def run_all(self, prestaged: bool = False) -> list[RunReport]:
         cfg, S = self.config, self.n_streams
         N = int(cfg.source_firings)
@@ -784,7 +966,11 @@ class DeviceRuntime:
         deadline = None if cfg.timeout_ms is None else t_start + cfg.timeout_ms / 1000.0
         self.pool = ThreadPoolExecutor(max_workers=max(1, cfg.host_threads or 16))
         try:
-            it = 0
+            if self._pipelinable(prestaged and N <= self.epoch):
+                self._run_pipelined(prestaged and N <= self.epoch, N, deadline)
+                it = N
+            else:
+                it = 0
             while it < N:
                 E = min(self.epoch, N - it)
                 self.stage_sources(it, E, prestaged=prestaged and N <= self.epoch)
@@ -870,9 +1056,10 @@ class DeviceRuntime:
         if getattr(self, "mem", None) is not None:
             self.mem.close()
             self.mem = None
-        if getattr(self, "stream", None):
-            self.lib.pb_stream_destroy(self.stream)
-            self.stream = None
+        for name in ("stream", "copy_in", "copy_out"):
+            if getattr(self, name, None):
+                self.lib.pb_stream_destroy(getattr(self, name))
+                setattr(self, name, None)
 
     def __del__(self):
         try:
