@@ -328,8 +328,7 @@ def main():
         hbm_peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
     except Exception:  # noqa: BLE001
         hbm_peak, peak_src = 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
-    alg_bytes = 16 * S * blocks * B          # fused bank: 8 B read + 8 B written per sample
-    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    achieved = None
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
@@ -338,8 +337,28 @@ def main():
                 "dram_bytes_per_launch")
         except Exception:  # noqa: BLE001
             traffic = None
-    # FP32 issue view: 10 taps x (2 FMUL2 + 2 FADD + 1 FADD2) per branch-sample
-    kbar = K * 0.75 if K == 4 else None
+    # FP32 view: the bit-exact FIR forbids FMA, so each active branch-sample
+    # costs 80 rounded FP32 ops (10 taps x 4 mul + 2 add/sub + 2 accumulate)
+    # plus 2 for the branch sum; the active branch count comes from the
+    # device-resolved control tokens of this workload.
+    counts = np.zeros((len(rt.plan.conds), S), dtype=np.int32)
+    lib.pb_memcpy_d2h(counts.ctypes.data, rt.res_count, counts.nbytes, rt.stream)
+    lib.pb_stream_sync(rt.stream)
+    branch_samples = int(counts.sum()) * B
+    if args.no_fuse:
+        alg_bytes = 16 * branch_samples      # per fir_branch firing: 8 B read + 8 B written
+        fp32_ops = 80 * branch_samples
+    else:
+        alg_bytes = 16 * S * blocks * B      # fused bank: 8 B read + 8 B written per sample
+        fp32_ops = 82 * branch_samples
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    probe = {}
+    try:
+        probe = json.loads((ROOT / "profiles" / "r1_fp32_probe.json").read_text())
+    except Exception:  # noqa: BLE001
+        pass
+    fp32_peak = 1e12 * max(probe.get("fmul_tops", 0), probe.get("fadd_tops", 0)) or \
+        148 * 128 * 1.965e9
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
@@ -370,6 +389,12 @@ def main():
                          "kernel": "filter_bank_kernel" if not args.no_fuse else "fir_kernel",
                          "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": alg_bytes,
                          "peak_source": peak_src},
+            "fp32": {"achieved": fp32_ops / (kern_ms / 1e3) / 1e12, "unit": "TFLOP/s",
+                     "peak": fp32_peak / 1e12, "frac": fp32_ops / (kern_ms / 1e3) / fp32_peak,
+                     "ops_per_launch": fp32_ops, "mean_active_branches":
+                     int(counts.sum()) / (S * blocks),
+                     "note": "non-FMA FP32 lane ops; peak = profiles/r1_fp32_probe.json "
+                             "(measured FMUL/FADD throughput)"},
             "clocks": clk,
             "e2e": {"value": samples / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s,

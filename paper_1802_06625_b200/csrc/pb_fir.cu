@@ -481,12 +481,15 @@ int launch_variant(const pb_filter_bank& bank, const pb_fir_actor* actors, int n
   return PB_OK;
 }
 
-// PB_FIR_MATH=scalar selects the scalar FMUL/FADD mix (A/B measurements).
+// Scalar FMUL/FADD is the default: on B200 the paired FMUL2/FADD2 ops give
+// no FP32 lane throughput (profiles/r1_fp32_probe.json) and the scalar mix
+// measured 3% faster in this kernel (profiles/r1_fir_mix.json).
+// PB_FIR_MATH=paired selects the FMUL2/FADD2 mix for A/B measurements.
 bool scalar_math() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("PB_FIR_MATH");
-    v = (e && std::string(e) == "scalar") ? 1 : 0;
+    v = (e && std::string(e) == "paired") ? 0 : 1;
   }
   return v == 1;
 }
