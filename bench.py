@@ -297,6 +297,11 @@ def main():
     value = samples / (ms_step / 1e3) / 1e6
     clk = clocks.summary()
 
+    # active firings of this workload (resolved on the device by the timed steps)
+    counts = np.zeros((len(rt.plan.conds), S), dtype=np.int32)
+    lib.pb_memcpy_d2h(counts.ctypes.data, rt.res_count, counts.nbytes, rt.stream)
+    lib.pb_stream_sync(rt.stream)
+
     # ---- end to end through the public runtime API
     e2e_times = []
     reps = None
@@ -341,9 +346,6 @@ def main():
     # costs 80 rounded FP32 ops (10 taps x 4 mul + 2 add/sub + 2 accumulate)
     # plus 2 for the branch sum; the active branch count comes from the
     # device-resolved control tokens of this workload.
-    counts = np.zeros((len(rt.plan.conds), S), dtype=np.int32)
-    lib.pb_memcpy_d2h(counts.ctypes.data, rt.res_count, counts.nbytes, rt.stream)
-    lib.pb_stream_sync(rt.stream)
     branch_samples = int(counts.sum()) * B
     if args.no_fuse:
         alg_bytes = 16 * branch_samples      # per fir_branch firing: 8 B read + 8 B written
