@@ -297,6 +297,27 @@ def main():
     value = samples / (ms_step / 1e3) / 1e6
     clk = clocks.summary()
 
+    # tolerance mode (FMA taps, <= 1e-5): same workload, fused kernel only
+    tol = None
+    if not args.no_fuse:
+        rt.set_fir_math(_lib.PB_FIR_FMA)
+        for _ in range(3):
+            rt.fire_epoch(0, blocks)
+        _lib.check(lib.pb_stream_sync(rt.stream))
+        t0e, t1e = new_event(), new_event()
+        lib.pb_event_record(t0e, rt.stream)
+        for _ in range(max(10, args.steps // 4)):
+            rt.fire_epoch(0, blocks)
+        lib.pb_event_record(t1e, rt.stream)
+        _lib.check(lib.pb_stream_sync(rt.stream))
+        _lib.check(lib.pb_event_elapsed_ms(t0e, t1e, C.byref(ms)))
+        tol_ms = max_over_ranks(ms.value / max(10, args.steps // 4))
+        tol = {"value": samples / (tol_ms / 1e3) / 1e6, "unit": UNIT, "ms_per_step": tol_ms,
+               "hbm_frac_of_step": 16 * S * blocks * B / (tol_ms / 1e3) / 1e9 / 6528.1,
+               "tolerance": "max |y - y_exact| / max(1, |y_exact|) <= 1e-5 "
+                            "(tests/test_dpd_gpu.py::test_tolerance_mode_within_1e5)"}
+        rt.set_fir_math(_lib.PB_FIR_EXACT)
+
     # active firings of this workload (resolved on the device by the timed steps)
     counts = np.zeros((len(rt.plan.conds), S), dtype=np.int32)
     lib.pb_memcpy_d2h(counts.ctypes.data, rt.res_count, counts.nbytes, rt.stream)
@@ -403,6 +424,7 @@ def main():
                     "includes": "H2D pinned inputs, native control actors, device firings, "
                                 "sink D2H, SHA-256 per stream"},
             "gpu_launches": launches,
+            "tolerance_mode": tol,
             "parity_stream0": parity,
             "cpu_baseline": cpu,
         }

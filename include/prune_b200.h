@@ -217,10 +217,19 @@ typedef struct {
   int32_t pad_;
 } pb_fir_actor;
 
+/* FIR arithmetic modes.  EXACT reproduces FirBranch.fire bit for bit (every
+ * product and sum rounded, scalar FMUL/FADD); EXACT_PAIRED is the same
+ * roundings with FMUL2/FADD2; FMA contracts each tap into fused multiply-adds
+ * (one rounding per tap term, about half the FP32 work) and is accurate to
+ * ~1e-7 relative, inside the 1e-5 tolerance the north star states. */
+#define PB_FIR_EXACT 0
+#define PB_FIR_EXACT_PAIRED 1
+#define PB_FIR_FMA 2
+
 /* All firings of n_actors fir_branch actors in one launch.  actors is a
  * DEVICE array. */
 int pb_fire_fir(const pb_fir_actor* actors, int n_actors, pb_resolved res, int64_t block,
-                void* stream);
+                int math, void* stream);
 /* History carry after pb_fire_fir / pb_fire_filter_bank: state[s] <- last 9
  * input samples of the epoch's last firing (if any). */
 int pb_fir_carry(const pb_fir_actor* actors, int n_actors, pb_resolved res, int64_t block,
@@ -238,6 +247,8 @@ typedef struct {
   int32_t actor_cond;                /* condition of route/combiner (-1) */
   uint32_t* sched;                   /* device uint32[2], zeroed once: dynamic work
                                         counter reset by the last CTA; NULL = static */
+  int32_t math;                      /* PB_FIR_* arithmetic mode */
+  int32_t pad_;
 } pb_filter_bank;
 int pb_fire_filter_bank(pb_filter_bank bank, pb_resolved res, int64_t block, void* stream);
 

@@ -26,6 +26,9 @@ PB_E_UNSUPPORTED = -7
 PB_E_ACTOR = -8
 
 PB_TAPS = 10
+PB_FIR_EXACT = 0
+PB_FIR_EXACT_PAIRED = 1
+PB_FIR_FMA = 2
 PB_MAX_BRANCHES = 32
 PB_MAX_PORTS = 16
 PB_POLICY_STATE_BYTES = 2560
@@ -71,7 +74,7 @@ class FirActor(C.Structure):
 
 class FilterBank(C.Structure):
     _fields_ = [("in_", SpanRef), ("out", SpanRef), ("branches", vp), ("n_branches", i32),
-                ("actor_cond", i32), ("sched", vp)]
+                ("actor_cond", i32), ("sched", vp), ("math", i32), ("pad_", i32)]
 
 
 class SumActor(C.Structure):
@@ -139,7 +142,7 @@ SIGNATURES = {
     "pb_resolve": (C.c_int, [C.POINTER(Condition), Resolved, vp]),
     "pb_eq1_check": (C.c_int, [C.POINTER(Eq1Port), C.c_int, Resolved, vp, vp]),
     "pb_rings_advance": (C.c_int, [C.POINTER(RingAdvance), C.c_int, Resolved, vp]),
-    "pb_fire_fir": (C.c_int, [vp, C.c_int, Resolved, i64, vp]),
+    "pb_fire_fir": (C.c_int, [vp, C.c_int, Resolved, i64, C.c_int, vp]),
     "pb_fir_carry": (C.c_int, [vp, C.c_int, Resolved, i64, vp]),
     "pb_fire_filter_bank": (C.c_int, [FilterBank, Resolved, i64, vp]),
     "pb_fire_branch_sum": (C.c_int, [SumActor, Resolved, i64, vp]),

@@ -25,8 +25,6 @@
 //            branch over 8 consecutive outputs per thread, sum (bank) or
 //            store per branch, release the stage.
 // kStages stages keep the next tiles in flight while the FP32 pipe works.
-#include <stdlib.h>
-
 #include <algorithm>
 #include <string>
 
@@ -176,6 +174,27 @@ __device__ __forceinline__ void fir8_scalar(const float (&wr)[kWin], const float
   for (int v = 0; v < kPerThread; ++v) y[v] = pack2(yr[v], yi[v]);
 }
 
+// Tolerance mode: one fused multiply-add per tap term (4 FFMA per
+// tap-output instead of 8 rounded ops); not bit-exact.
+__device__ __forceinline__ void fir8_fma(const float (&wr)[kWin], const float (&wi)[kWin],
+                                         const float4* __restrict__ taps, u64 (&y)[kPerThread]) {
+  float yr[kPerThread], yi[kPerThread];
+#pragma unroll
+  for (int v = 0; v < kPerThread; ++v) yr[v] = yi[v] = 0.0f;
+#pragma unroll
+  for (int t = 0; t < kTaps; ++t) {
+    const float4 c = taps[t];
+#pragma unroll
+    for (int v = 0; v < kPerThread; ++v) {
+      const float xr = wr[kPad + v - t], xi = wi[kPad + v - t];
+      yr[v] = __fmaf_rn(-c.y, xi, __fmaf_rn(c.x, xr, yr[v]));
+      yi[v] = __fmaf_rn(c.y, xr, __fmaf_rn(c.x, xi, yi[v]));
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < kPerThread; ++v) y[v] = pack2(yr[v], yi[v]);
+}
+
 __device__ __forceinline__ void load_window(const StageBuf& sb, int ct, float (&wr)[kWin],
                                             float (&wi)[kWin]) {
   const float4* a = reinterpret_cast<const float4*>(sb.re + kPerThread * ct);
@@ -207,7 +226,7 @@ __device__ __forceinline__ void store8(float* out, int64_t B, int n0, const u64 
 //                region; output = sum over active branches (combiner order)
 // kBank = false: items (actor, s, j, tile) of per-actor batched firings;
 //                output = the actor's own output span
-template <bool kBank, bool kScalarMath>
+template <bool kBank, int kMath>
 __global__ void __launch_bounds__(kThreads, 4)
 fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actors, int n_actors,
                pb_resolved res, int64_t B, int tiles) {
@@ -416,10 +435,12 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
           }
         }
         u64 y[kPerThread];
-        if (kScalarMath)
+        if (kMath == PB_FIR_EXACT)
           fir8_scalar(wr, wi, sm.taps[d.br[r]], y);
-        else
+        else if (kMath == PB_FIR_EXACT_PAIRED)
           fir8(wr, wi, sm.taps[d.br[r]], y);
+        else
+          fir8_fma(wr, wi, sm.taps[d.br[r]], y);
         if (kBank) {
 #pragma unroll
           for (int v = 0; v < kPerThread; ++v) acc[v] = fadd2(acc[v], y[v]);
@@ -453,14 +474,14 @@ int check_block(int64_t B) {
   return PB_OK;
 }
 
-template <bool kBank, bool kScalarMath>
+template <bool kBank, int kMath>
 int launch_variant(const pb_filter_bank& bank, const pb_fir_actor* actors, int n_actors,
                    const pb_resolved& res, int64_t B, cudaStream_t st) {
   const int tiles = (int)((B + kTile - 1) / kTile);
   const size_t smem = sizeof(Smem);
   static bool configured = false;
   if (!configured) {
-    PB_CUDA(cudaFuncSetAttribute(fir_persistent<kBank, kScalarMath>,
+    PB_CUDA(cudaFuncSetAttribute(fir_persistent<kBank, kMath>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
@@ -469,36 +490,34 @@ int launch_variant(const pb_filter_bank& bank, const pb_fir_actor* actors, int n
     int dev = 0;
     PB_CUDA(cudaGetDevice(&dev));
     PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    PB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fir_persistent<kBank, kScalarMath>,
+    PB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fir_persistent<kBank, kMath>,
                                                           kThreads, smem));
     per_sm = std::max(per_sm, 1);
   }
   const int64_t items =
       (kBank ? 1 : (int64_t)n_actors) * res.n_streams * (int64_t)res.n_iter * tiles;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)sms * per_sm));
-  fir_persistent<kBank, kScalarMath><<<grid, kThreads, smem, st>>>(bank, actors, n_actors, res, B, tiles);
+  fir_persistent<kBank, kMath><<<grid, kThreads, smem, st>>>(bank, actors, n_actors, res, B, tiles);
   PB_LAUNCHED(kBank ? "fir_persistent<bank>" : "fir_persistent<actors>");
   return PB_OK;
 }
 
-// Scalar FMUL/FADD is the default: on B200 the paired FMUL2/FADD2 ops give
-// no FP32 lane throughput (profiles/r1_fp32_probe.json) and the scalar mix
-// measured 3% faster in this kernel (profiles/r1_fir_mix.json).
-// PB_FIR_MATH=paired selects the FMUL2/FADD2 mix for A/B measurements.
-bool scalar_math() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("PB_FIR_MATH");
-    v = (e && std::string(e) == "paired") ? 0 : 1;
-  }
-  return v == 1;
-}
-
+// Scalar FMUL/FADD is the exact default: on B200 the paired FMUL2/FADD2 ops
+// give no FP32 lane throughput (profiles/r1_fp32_probe.json) and the scalar
+// mix measured 3% faster in this kernel (profiles/r1_fir_mix.json).
 template <bool kBank>
 int launch(const pb_filter_bank& bank, const pb_fir_actor* actors, int n_actors,
-           const pb_resolved& res, int64_t B, cudaStream_t st) {
-  return scalar_math() ? launch_variant<kBank, true>(bank, actors, n_actors, res, B, st)
-                       : launch_variant<kBank, false>(bank, actors, n_actors, res, B, st);
+           const pb_resolved& res, int64_t B, int math, cudaStream_t st) {
+  switch (math) {
+    case PB_FIR_EXACT:
+      return launch_variant<kBank, PB_FIR_EXACT>(bank, actors, n_actors, res, B, st);
+    case PB_FIR_EXACT_PAIRED:
+      return launch_variant<kBank, PB_FIR_EXACT_PAIRED>(bank, actors, n_actors, res, B, st);
+    case PB_FIR_FMA:
+      return launch_variant<kBank, PB_FIR_FMA>(bank, actors, n_actors, res, B, st);
+    default:
+      return pb::fail(PB_E_INVALID, "unknown FIR math mode " + std::to_string(math));
+  }
 }
 
 }  // namespace
@@ -506,7 +525,7 @@ int launch(const pb_filter_bank& bank, const pb_fir_actor* actors, int n_actors,
 extern "C" {
 
 int pb_fire_fir(const pb_fir_actor* actors, int n_actors, pb_resolved res, int64_t block,
-                void* stream) {
+                int math, void* stream) {
   if (n_actors == 0 || res.n_iter == 0) return PB_OK;
   if (n_actors > kMaxBr)
     return pb::fail(PB_E_UNSUPPORTED, "pb_fire_fir: at most " + std::to_string(kMaxBr) +
@@ -514,7 +533,7 @@ int pb_fire_fir(const pb_fir_actor* actors, int n_actors, pb_resolved res, int64
   int rc = check_block(block);
   if (rc) return rc;
   pb_filter_bank none{};
-  return launch<false>(none, actors, n_actors, res, block, pb::as_stream(stream));
+  return launch<false>(none, actors, n_actors, res, block, math, pb::as_stream(stream));
 }
 
 int pb_fir_carry(const pb_fir_actor* actors, int n_actors, pb_resolved res, int64_t block,
@@ -533,7 +552,7 @@ int pb_fire_filter_bank(pb_filter_bank bank, pb_resolved res, int64_t block, voi
                                           " branches");
   int rc = check_block(block);
   if (rc) return rc;
-  return launch<true>(bank, nullptr, 0, res, block, pb::as_stream(stream));
+  return launch<true>(bank, nullptr, 0, res, block, bank.math, pb::as_stream(stream));
 }
 
 }  // extern "C"

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes as C
 import hashlib
+import os
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -60,6 +61,7 @@ class RuntimeConfig:
     device: int = 0
     host_threads: int = 0         # threads for native policies and digests (0 = all)
     pipeline: int = 8             # sub-epochs overlapping H2D / kernels / D2H / hashing (1 = off)
+    exact: bool = True            # False: FIR taps as fused multiply-adds (<= 1e-5, not bit-exact)
 
 
 @dataclass
@@ -211,6 +213,9 @@ class DeviceRuntime:
             if role in ("source", "config", "sink") and is_device(b):
                 raise UnsupportedGraph(f"actor {a.id} ({role}) needs a host behaviour")
 
+        self.fir_math = _lib.PB_FIR_EXACT if config.exact else _lib.PB_FIR_FMA
+        if config.exact and os.environ.get("PB_FIR_MATH") == "paired":
+            self.fir_math = _lib.PB_FIR_EXACT_PAIRED
         self.banks = find_filter_banks(plan, self.behaviors[0]) if config.fuse else []
         self.fused_actors = {a for grp in self.banks for a in [grp.router, *grp.branches]}
         self.virtual = {fid for grp in self.banks for fid in grp.internal_fifos}
@@ -390,7 +395,7 @@ class DeviceRuntime:
                 dev = self.mem.upload(np.frombuffer(bytes(arr), dtype=np.uint8))
                 bank = _lib.FilterBank(self._ref(fin.id), self._ref(fout.id), dev,
                                        len(grp.branches), plan.actor_cond[aid],
-                                       self.mem.malloc(16))
+                                       self.mem.malloc(16), self.fir_math, 0)
                 block = fin.rate * fin.token_bytes // 8
                 self.launches.append(("bank", bank, block))
                 self.fir_groups.append((dev, len(grp.branches), block))
@@ -657,7 +662,8 @@ class DeviceRuntime:
             if kind == "bank":
                 _lib.check(lib.pb_fire_filter_bank(item[1], res, item[2], st), "filter_bank")
             elif kind == "fir":
-                _lib.check(lib.pb_fire_fir(item[1], item[2], res, item[3], st), "fir_branch")
+                _lib.check(lib.pb_fire_fir(item[1], item[2], res, item[3], self.fir_math, st),
+                           "fir_branch")
             elif kind == "sum":
                 _lib.check(lib.pb_fire_branch_sum(item[1], res, item[2], st), "branch_sum")
             elif kind == "bytes":
@@ -673,6 +679,14 @@ class DeviceRuntime:
         _lib.check(lib.pb_rings_advance(self.advance, len(self.advance), res, st),
                    "pb_rings_advance")
         return lib.pb_launch_count() - n0
+
+    def set_fir_math(self, math: int) -> None:
+        """Switch the FIR arithmetic mode (PB_FIR_EXACT / _EXACT_PAIRED / _FMA)
+        of every FIR launch of this runtime."""
+        self.fir_math = int(math)
+        for item in self.launches:
+            if item[0] == "bank":
+                item[1].math = self.fir_math
 
     def _epoch_counts(self) -> np.ndarray:
         n_cond = len(self.plan.conds)

@@ -114,3 +114,30 @@ def test_fir_kernel_bitexact_static_chain(block):
         yr, yi, hr, hi = od.fir_block(x[n, 0], x[n, 1], cr, ci, hr, hi)
         want.append(np.stack([yr, yi]))
     assert rep.sink_data["sink"] == np.stack(want).tobytes()
+
+
+TOLERANCE = 1e-5   # north star: max-abs/relative error <= 1e-5 for DPD
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+def test_tolerance_mode_within_1e5(fuse):
+    """RuntimeConfig(exact=False): FIR taps as fused multiply-adds.  Not
+    bit-exact by design; every sample within 1e-5 of the exact reference
+    (relative to max(1, |y|)) and control / firing counts still exact."""
+    S, blocks, B = 3, 20, 4096
+    xs = [pd.stream_input(s, blocks, B) for s in range(S)]
+    reps = run_streams(pd.build_description(B, 4), S,
+                       RuntimeConfig(source_firings=blocks, exact=False, fuse=fuse,
+                                     capture_sinks=True),
+                       seeds=[1000 + s for s in range(S)],
+                       sources={"src": [x.tobytes() for x in xs]})
+    worst = 0.0
+    for s in range(S):
+        sets = od.subset_schedule(1000 + s, blocks)
+        want = od.dpd_stream(xs[s], sets, 4).astype(np.float64)
+        got = np.frombuffer(reps[s].sink_data["sink"], np.float32).reshape(want.shape)
+        err = np.abs(got - want) / np.maximum(1.0, np.abs(want))
+        worst = max(worst, float(err.max()))
+        assert reps[s].firing_counts == od.firing_counts(sets, 4)
+    assert worst <= TOLERANCE, worst
+    assert worst > 0.0   # genuinely the contracted arithmetic

@@ -1,0 +1,98 @@
+"""Admission (plan.admit) on the reference's graphs: conditions, rejections."""
+import json
+
+import pytest
+
+from paper_1802_06625_b200 import InconsistentGraph, UnsupportedGraph, admit, as_graph
+from paper_1802_06625_b200.apps import predistortion as pd
+from paper_1802_06625_b200.graph import DanglingPort, DuplicateId, RateMismatch
+
+
+def test_dpd_conditions_and_bounds():
+    p = admit(as_graph(pd.build_description()), c_factor=3)
+    assert [c.element for c in p.conds] == [1, 2, 3, 4]
+    assert {a: c for a, c in p.actor_cond.items() if c >= 0} == {"b1": 0, "b2": 1, "b3": 2,
+                                                                 "b4": 3}
+    assert p.fifo_cond["f_in3"] == p.fifo_cond["f_fir3"] == 2
+    assert p.fifo_cond["f_src"] == p.fifo_cond["f_out"] == -1
+    assert len(p.eq1_ports) == 8
+    assert all(v == 3 for v in p.admission.beta.values())   # rate + (C-1)*rate
+
+
+def test_rule2_skewed_control_rejected():
+    # test_acceptance.py:195-203: a delay on c_split only
+    desc = pd.build_description()
+    for f in desc["fifos"]:
+        if f["id"] == "c_split":
+            f["delay"] = 1
+    with pytest.raises(InconsistentGraph, match="rule 2"):
+        admit(as_graph(desc))
+
+
+def test_eq1_mismatch_rejected():
+    desc = pd.build_description()
+    # feed branch b2 from the d1 dynamic port: b2's consumer side is gated by
+    # element 2, its producer side by element 1
+    for f in desc["fifos"]:
+        if f["id"] == "f_in2":
+            f["src"] = "split.d1"
+        if f["id"] == "f_in1":
+            f["src"] = "split.d2"
+    with pytest.raises(InconsistentGraph, match="Eq. 1"):
+        admit(as_graph(desc))
+
+
+def test_data_delay_is_unsupported_not_wrong(golden):
+    desc = golden["fixtures"]["static_chain"]["description"]
+    desc = json.loads(json.dumps(desc))
+    desc["fifos"][1]["delay"] = 2
+    with pytest.raises(UnsupportedGraph, match="delay"):
+        admit(as_graph(desc))
+
+
+def test_zero_delay_cycle_deadlocks():
+    desc = {"name": "cyc", "actors": [
+        {"id": "a", "kind": "static", "behavior": "passthrough",
+         "ports": [{"id": "in", "dir": "in"}, {"id": "out", "dir": "out"}]},
+        {"id": "b", "kind": "static", "behavior": "passthrough",
+         "ports": [{"id": "in", "dir": "in"}, {"id": "out", "dir": "out"}]}],
+        "fifos": [{"id": "ab", "src": "a.out", "dst": "b.in"},
+                  {"id": "ba", "src": "b.out", "dst": "a.in"}], "control": {}}
+    with pytest.raises(InconsistentGraph, match="Deadlock"):
+        admit(as_graph(desc))
+
+
+@pytest.mark.parametrize("key", ["static_chain", "broadcast_two_sinks", "clean_single_chain",
+                                 "clean_two_component", "gated_pipeline", "rate_pair_atr3"])
+def test_reference_fixtures_admitted(golden, key):
+    admit(as_graph(golden["fixtures"][key]["description"]))
+
+
+def test_structural_errors_match_reference_classes():
+    desc = pd.build_description()
+    bad = json.loads(json.dumps(desc))
+    bad["actors"].append(bad["actors"][0])
+    with pytest.raises(DuplicateId):
+        as_graph(bad)
+    bad = json.loads(json.dumps(desc))
+    bad["fifos"][0]["dst"] = "split.nope"
+    with pytest.raises(DanglingPort):
+        as_graph(bad)
+    bad = json.loads(json.dumps(desc))
+    bad["fifos"][0]["rate"] = 2
+    with pytest.raises(RateMismatch):
+        as_graph(bad)
+
+
+def test_reference_graph_object_converts(golden):
+    import sys
+    from pathlib import Path
+    ref = Path("/root/repo/oracle/_ref")
+    if not (ref / "tokenflow").is_dir():
+        pytest.skip("reference not installed in oracle/_ref")
+    sys.path.insert(0, str(ref))
+    from tokenflow.model import build_graph
+    desc = pd.build_description(4096, 10)
+    g_ref = build_graph(desc)
+    g = as_graph(g_ref)
+    assert g.description() == as_graph(desc).description()
