@@ -298,6 +298,55 @@ typedef struct {
 } pb_path_merge_actor;
 int pb_fire_path_merge(pb_path_merge_actor actor, pb_resolved res, void* stream);
 
+/* ------------------------------------------------ CNN actors (vision example) */
+/* The paper's adaptive DNN is not in the reference
+ * package; these actors and their oracle (oracle/cnn.py) are builder-defined.
+ * Tokens are NHWC fp32 frames; `frames` = frames per firing (port rate). */
+
+/* conv2d_relu_pool: 5x5 conv (zero pad), bias, ReLU, 2x2 max pool, 32 output
+ * channels, as a tcgen05 implicit GEMM (split-TF32, fp32 accumulate in TMEM).
+ * weights: host-prepared per 32-wide K chunk (K = 25*cin ordered ky,kx,ci):
+ * [hi 32x32][lo 32x32] in the UMMA K-major core-matrix layout (see
+ * paper_1802_06625_b200/cnn_weights.py). */
+typedef struct {
+  pb_span_ref in;
+  pb_span_ref out;
+  const float* weights;
+  const float* bias;       /* [32] */
+  int32_t frames;
+  int32_t h, w, cin, cout, pad;
+  int32_t cond;
+  int32_t pad_;
+} pb_conv_actor;
+int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream);
+
+/* dense: out[f] = W x[f] + b, W row-major [nout][nin] (fp32 FMA). */
+typedef struct {
+  pb_span_ref in;
+  pb_span_ref out;
+  const float* weights;
+  const float* bias;
+  int32_t frames, nin, nout, cond;
+} pb_dense_actor;
+int pb_fire_dense(pb_dense_actor actor, pb_resolved res, void* stream);
+
+/* classify_merge: live chain input -> W5 relu(W4 relu(x) + b4) + b5; live
+ * bypass input -> every logit = marker; != 1 live input sets *error_flag. */
+typedef struct {
+  pb_span_ref chain;
+  pb_span_ref bypass;
+  pb_span_ref out;
+  const float* w4;
+  const float* b4;
+  const float* w5;
+  const float* b5;
+  int32_t frames, nin, nhid, nout;
+  float marker;
+  int32_t cond;
+  int32_t* error_flag;
+} pb_classify_actor;
+int pb_fire_classify(pb_classify_actor actor, pb_resolved res, void* stream);
+
 /* ------------------------------------------ host configuration actors (native) */
 /* Control tokens of _PolicyBase.fire (behavior.py:212-218) with CPython's
  * Mersenne Twister (random.Random(seed)) reproduced bit for bit:

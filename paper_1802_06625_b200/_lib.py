@@ -96,6 +96,24 @@ class PathMergeActor(C.Structure):
                 ("error_flag", vp)]
 
 
+class ConvActor(C.Structure):
+    _fields_ = [("in_", SpanRef), ("out", SpanRef), ("weights", vp), ("bias", vp),
+                ("frames", i32), ("h", i32), ("w", i32), ("cin", i32), ("cout", i32),
+                ("pad", i32), ("cond", i32), ("pad_", i32)]
+
+
+class DenseActor(C.Structure):
+    _fields_ = [("in_", SpanRef), ("out", SpanRef), ("weights", vp), ("bias", vp),
+                ("frames", i32), ("nin", i32), ("nout", i32), ("cond", i32)]
+
+
+class ClassifyActor(C.Structure):
+    _fields_ = [("chain", SpanRef), ("bypass", SpanRef), ("out", SpanRef), ("w4", vp),
+                ("b4", vp), ("w5", vp), ("b5", vp), ("frames", i32), ("nin", i32),
+                ("nhid", i32), ("nout", i32), ("marker", C.c_float), ("cond", i32),
+                ("error_flag", vp)]
+
+
 # name -> (restype, argtypes); every symbol include/prune_b200.h declares
 SIGNATURES = {
     "pb_abi_version": (C.c_int, []),
@@ -149,6 +167,9 @@ SIGNATURES = {
     "pb_fire_bytes": (C.c_int, [BytesActor, Resolved, vp]),
     "pb_fire_matmul": (C.c_int, [MatmulActor, Resolved, vp]),
     "pb_fire_path_merge": (C.c_int, [PathMergeActor, Resolved, vp]),
+    "pb_fire_conv_pool": (C.c_int, [ConvActor, Resolved, vp]),
+    "pb_fire_dense": (C.c_int, [DenseActor, Resolved, vp]),
+    "pb_fire_classify": (C.c_int, [ClassifyActor, Resolved, vp]),
     "pb_policy_init": (C.c_int, [vp, i64]),
     "pb_policy_tokens": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, i64, i64, vp, C.c_int]),
     "pb_policy_tokens_streams": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, i64, i64,

@@ -467,6 +467,39 @@ class DeviceRuntime:
                 act.error_flag = self.err_flag
                 act.out = self._ref(out_f[0])
                 self.launches.append(("path_merge", act, aid))
+            elif kind == "conv":
+                from .cnn_weights import conv_device_layout
+                b.init(aid, a.params, None)
+                fi = g.fifo(in_f[0])
+                if fi.token_bytes != b.h * b.w * b.cin * 4:
+                    raise UnsupportedGraph(f"{aid}: token is not one {b.h}x{b.w}x{b.cin} frame")
+                act = _lib.ConvActor(self._ref(in_f[0]), self._ref(out_f[0]),
+                                     self.mem.upload(conv_device_layout(b.weights)),
+                                     self.mem.upload(b.bias), fi.rate, b.h, b.w, b.cin,
+                                     b.cout, b.pad, plan.actor_cond[aid], 0)
+                self.launches.append(("conv", act))
+            elif kind == "dense":
+                b.init(aid, a.params, None)
+                fi = g.fifo(in_f[0])
+                act = _lib.DenseActor(self._ref(in_f[0]), self._ref(out_f[0]),
+                                      self.mem.upload(b.weights), self.mem.upload(b.bias),
+                                      fi.rate, b.nin, b.nout, plan.actor_cond[aid])
+                self.launches.append(("dense", act))
+            elif kind == "classify":
+                b.init(aid, a.params, None)
+                bypass = a.params.get("bypass_port", "")
+                names = [p.id for p in ins]
+                if len(in_f) != 2 or bypass not in names:
+                    raise UnsupportedGraph(f"{aid}: classify_merge needs a chain and a bypass input")
+                chain_f = in_f[1 - names.index(bypass)]
+                bypass_f = in_f[names.index(bypass)]
+                act = _lib.ClassifyActor(
+                    self._ref(chain_f), self._ref(bypass_f), self._ref(out_f[0]),
+                    self.mem.upload(b.w4), self.mem.upload(b.b4), self.mem.upload(b.w5),
+                    self.mem.upload(b.b5), g.fifo(out_f[0]).rate, b.nin, b.nhid, b.nout,
+                    float(np.float32(a.params.get("marker", -1.0))), plan.actor_cond[aid],
+                    self.err_flag)
+                self.launches.append(("classify", act, aid))
             else:
                 raise UnsupportedGraph(f"actor {aid}: no device kernel for behaviour "
                                        f"{a.behavior!r}")
@@ -672,6 +705,12 @@ class DeviceRuntime:
                 _lib.check(lib.pb_fire_matmul(item[1], res, st), "matmul")
             elif kind == "path_merge":
                 _lib.check(lib.pb_fire_path_merge(item[1], res, st), "path_merge")
+            elif kind == "conv":
+                _lib.check(lib.pb_fire_conv_pool(item[1], res, st), "conv2d_relu_pool")
+            elif kind == "dense":
+                _lib.check(lib.pb_fire_dense(item[1], res, st), "dense")
+            elif kind == "classify":
+                _lib.check(lib.pb_fire_classify(item[1], res, st), "classify_merge")
             if hook is not None:
                 hook(kind, "post")
         for dev, n, block in self.fir_groups:
@@ -782,6 +821,8 @@ class DeviceRuntime:
                 b = self.behaviors[s][a.id]
                 if a.id in self.sources and self.plan.roles[a.id] == "source":
                     continue
+                if is_device(b):
+                    continue   # stateless kernels, configured at build time
                 try:
                     b.init(a.id, a.params, actor_seed(self.seeds[s], a.id))
                 except Exception as e:  # noqa: BLE001
@@ -1018,9 +1059,9 @@ class DeviceRuntime:
         _lib.check(self.lib.pb_stream_sync(self.stream), "epoch")
         if flag[0]:
             for item in self.launches:
-                if item[0] == "path_merge":
+                if item[0] in ("path_merge", "classify"):
                     raise ActorPanic(item[2], ValueError(
-                        "path_merge needs exactly one live input per firing"))
+                        f"{item[0]} needs exactly one live input per firing"))
             raise ActorPanic("device", RuntimeError("device actor reported a failure"))
 
     def _counters(self, fid: str) -> np.ndarray:

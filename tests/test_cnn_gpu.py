@@ -1,0 +1,81 @@
+"""Vision graph (CNN actors on tcgen05) vs the builder oracle (oracle/cnn.py).
+
+Parity is UNPINNED against the reference (it ships no DNN); the stated
+tolerance is the north star's: logits within 1e-3 (absolute, logits are
+O(1)) and the same top-1 class; conv/pool tokens within 1e-4 relative to
+max(1, |y|) (split-TF32 ~ fp32).  Control behaviour (which firings bypass)
+and firing counts are exact."""
+import numpy as np
+import pytest
+
+from oracle import cnn as oc
+from paper_1802_06625_b200 import RuntimeConfig, run_streams
+from paper_1802_06625_b200.apps import vision
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_TOL = 1e-3
+ACT_TOL = 1e-4
+
+
+def chain_desc(layers, R):
+    """src -> l1 [-> l2] -> sink: exposes the conv tokens at a sink."""
+    full = vision.build_description(R)
+    acts = {a["id"]: a for a in full["actors"]}
+    fifos = {f["id"]: f for f in full["fifos"]}
+    actors = [acts["src"]] + [acts[l] for l in layers] + [acts["sink"]]
+    chain = [
+        {"id": "a0", "src": "src.out", "dst": f"{layers[0]}.in", "rate": R,
+         "token_bytes": vision.FRAME_BYTES}]
+    tb = {"l1": fifos["f_l2"]["token_bytes"], "l2": fifos["f_l3"]["token_bytes"]}
+    for i, l in enumerate(layers):
+        dst = f"{layers[i + 1]}.in" if i + 1 < len(layers) else "sink.in"
+        chain.append({"id": f"a{i + 1}", "src": f"{l}.out", "dst": dst, "rate": R,
+                      "token_bytes": tb[l]})
+    return {"name": "chain", "actors": actors, "fifos": chain, "control": {}}
+
+
+def rel_err(got, want):
+    return float((np.abs(got - want) / np.maximum(1.0, np.abs(want))).max())
+
+
+@pytest.mark.parametrize("layers,shape", [(["l1"], (52, 52, 32)), (["l1", "l2"], (24, 24, 32))])
+def test_conv_pool_tokens(layers, shape):
+    R, firings = 3, 3
+    x = vision.make_frames(0, R * firings)
+    desc = chain_desc(layers, R)
+    (rep,) = run_streams(desc, 1, RuntimeConfig(source_firings=firings, capture_sinks=True),
+                         sources={"src": [x.tobytes()]})
+    got = np.frombuffer(rep.sink_data["sink"], np.float32).reshape(R * firings, *shape)
+    p = oc.graph_params(vision.build_description(R))
+    want = oc.conv_relu_pool(x, *p["l1"])
+    if "l2" in layers:
+        want = oc.conv_relu_pool(want.astype(np.float32), *p["l2"])
+    err = rel_err(got, want)
+    assert err <= ACT_TOL, err
+    assert rep.firing_counts["sink"] == firings
+
+
+@pytest.mark.parametrize("epoch", [4096, 3])
+def test_vision_graph_logits(epoch):
+    R, firings, S = 4, 6, 2
+    xs = [vision.make_frames(s, R * firings) for s in range(S)]
+    desc = vision.build_description(R)
+    reps = run_streams(desc, S, RuntimeConfig(source_firings=firings, capture_sinks=True,
+                                              epoch=epoch),
+                       seeds=[5, 6], sources={"src": [x.tobytes() for x in xs]})
+    p = oc.graph_params(desc)
+    for s in range(S):
+        logits = np.frombuffer(reps[s].sink_data["sink"], np.float32).reshape(firings, R, 4)
+        for j in range(firings):
+            if j % 2 == 0:   # alternate_policy: element 1 (process) on even firings
+                want = oc.forward(xs[s][j * R:(j + 1) * R], p)["logits"]
+                err = float(np.abs(logits[j] - want).max())
+                assert err <= LOGIT_TOL, (s, j, err)
+                assert (logits[j].argmax(-1) == want.argmax(-1)).all()
+            else:
+                assert (logits[j] == np.float32(p["marker"])).all()
+        fc = reps[s].firing_counts
+        assert fc["l1"] == fc["l2"] == fc["l3"] == firings // 2
+        assert fc["join"] == fc["sink"] == firings
+        assert reps[s].eq1_checks == 4 * firings and reps[s].eq1_failures == 0
