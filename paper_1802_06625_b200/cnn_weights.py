@@ -3,7 +3,7 @@
 The paper's adaptive DNN has no published weights; the
 reference package replaces it with 8x8 matmuls.  Weights here
 are He-normal from a seed (`he_normal`), so a graph description only carries
-seeds and shapes (or explicit lists for small tests).
+seeds and shapes (or explicit `weights`/`bias` lists).
 
 `conv_device_layout` prepares a conv weight matrix W[cout][K] (K = 25*cin in
 (ky, kx, ci) order) for the tcgen05 kernel: per 32-wide K chunk, the TF32
@@ -29,10 +29,11 @@ def small_bias(seed: int, rows: int) -> np.ndarray:
 
 
 def layer_params(params, rows: int, fan_in: int) -> tuple[np.ndarray, np.ndarray]:
-    """Weights W[rows][fan_in] and bias[rows] from explicit lists or a seed."""
-    if "w" in params:
-        w = np.asarray(params["w"], dtype=np.float32).reshape(rows, fan_in)
-        b = np.asarray(params.get("b", [0.0] * rows), dtype=np.float32)
+    """Weights W[rows][fan_in] and bias[rows] from explicit lists
+    (params["weights"], params["bias"]) or He-normal from params["seed"]."""
+    if "weights" in params:
+        w = np.asarray(params["weights"], dtype=np.float32).reshape(rows, fan_in)
+        b = np.asarray(params.get("bias") or [0.0] * rows, dtype=np.float32)
         return w, b
     seed = int(params["seed"])
     return he_normal(seed, rows, fan_in), small_bias(seed, rows)
