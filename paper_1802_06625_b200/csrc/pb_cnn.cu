@@ -30,16 +30,19 @@ constexpr int kRows = 128;            // conv pixels per tile (GEMM M)
 constexpr int kPool = kRows / 4;      // pooled pixels per tile
 constexpr int kCout = 32;             // GEMM N
 constexpr int kKC = 32;               // K per chunk
-constexpr int kStages = 2;
 constexpr int kThreadsConv = 128;
 constexpr int kChunkFloats = kRows * kKC;        // A plane per chunk
 constexpr int kWChunkFloats = kCout * kKC;       // W plane per chunk
+constexpr int kRawStride = kKC + 4;              // padded raw row (conflict-free LDS.128)
+constexpr int kAhead = 4;                        // chunks in flight ahead of the split
+constexpr int kRing = kAhead + 2;                // raw/W ring slots
+constexpr int kStages = 2;                       // split A planes (MMA operands)
 
 struct __align__(1024) ConvSmem {
-  float a_hi[kStages][kChunkFloats];
+  float a_hi[kStages][kChunkFloats];             // UMMA operand, K-major core layout
   float a_lo[kStages][kChunkFloats];
-  float w_hi[kStages][kWChunkFloats];
-  float w_lo[kStages][kWChunkFloats];
+  float w[kRing][2][kWChunkFloats];              // pre-split weights (hi, lo), cp.async ring
+  float raw[kRing][kRows * kRawStride];          // gathered im2col rows, cp.async ring
   uint64_t mma_done[kStages];
   uint32_t tmem_base;
 };
@@ -78,6 +81,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// cp.async with zero fill: copies src_bytes (0 or size) and zero-fills the rest
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ int core_off(int row, int k) {  // float offset in a plane
   return ((row >> 3) * (kKC / 4) + (k >> 2)) * 32 + (row & 7) * 4 + (k & 3);
 }
@@ -87,24 +107,107 @@ __device__ __forceinline__ void split(float x, float& hi, float& lo) {
   lo = __fsub_rn(x, hi);
 }
 
-__global__ void __launch_bounds__(kThreadsConv, 2)
+// Geometry of one conv layer launch.
+struct ConvGeom {
+  int H, W, Cin, pad, Ho, Wo, Hp, Wp, K, n_chunks;
+  int64_t per_frame, per_unit, tiles_per_unit, total, in_frame, out_frame;
+};
+
+__device__ __forceinline__ ConvGeom geom(const pb_conv_actor& a, const pb_resolved& res) {
+  ConvGeom g;
+  g.H = a.h; g.W = a.w; g.Cin = a.cin; g.pad = a.pad;
+  g.Ho = g.H + 2 * g.pad - 4; g.Wo = g.W + 2 * g.pad - 4;
+  g.Hp = g.Ho / 2; g.Wp = g.Wo / 2;
+  g.K = 25 * g.Cin;
+  g.n_chunks = (g.K + kKC - 1) / kKC;
+  g.per_frame = (int64_t)g.Hp * g.Wp;
+  g.per_unit = (int64_t)a.frames * g.per_frame;
+  g.tiles_per_unit = (g.per_unit + kPool - 1) / kPool;
+  g.total = (int64_t)res.n_streams * res.n_iter * g.tiles_per_unit;
+  g.in_frame = (int64_t)g.H * g.W * g.Cin;
+  g.out_frame = g.per_frame * kCout;
+  return g;
+}
+
+// This thread's GEMM row of tile w: its input frame base and conv pixel.
+struct RowCtx {
+  const float* fin;   // input frame (nullptr: the tile is skipped)
+  float* out;         // output span of the firing
+  int64_t g;          // pooled pixel index within the firing
+  bool ok;
+  int oy, ox;
+};
+
+__device__ __forceinline__ bool tile_live(const pb_conv_actor& a, const pb_resolved& res,
+                                          const ConvGeom& G, int64_t w) {
+  const int64_t unit = w / G.tiles_per_unit;
+  const int s = (int)(unit / res.n_iter), j = (int)(unit % res.n_iter);
+  return j < pb::cond_count(res, a.cond, s);
+}
+
+__device__ __forceinline__ RowCtx row_ctx(const pb_conv_actor& a, const pb_resolved& res,
+                                          const ConvGeom& G, int64_t w, int tid) {
+  RowCtx r;
+  const int64_t unit = w / G.tiles_per_unit, tile = w % G.tiles_per_unit;
+  const int s = (int)(unit / res.n_iter), j = (int)(unit % res.n_iter);
+  const int n = pb::firing_iter(res, a.cond, s, j);
+  const float* in = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n));
+  r.out = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
+  r.g = tile * kPool + (tid >> 2);
+  r.ok = r.g < G.per_unit;
+  int frame = 0;
+  r.oy = r.ox = 0;
+  if (r.ok) {
+    frame = (int)(r.g / G.per_frame);
+    const int p = (int)(r.g % G.per_frame);
+    r.oy = 2 * (p / G.Wp) + ((tid >> 1) & 1);
+    r.ox = 2 * (p % G.Wp) + (tid & 1);
+  }
+  r.fin = in + frame * G.in_frame;
+  return r;
+}
+
+// Issue the asynchronous gather of chunk c of this thread's row (and its
+// share of the chunk's pre-split weights) into ring slot `slot`.
+__device__ __forceinline__ void prefetch(ConvSmem& sm, const pb_conv_actor& a, const ConvGeom& G,
+                                         const RowCtx& r, int c, int slot, int tid) {
+  float* dst = sm.raw[slot] + tid * kRawStride;
+  const int k0 = c * kKC;
+  if (G.Cin % kKC == 0) {
+    const int tap = k0 / G.Cin, ci0 = k0 % G.Cin;
+    const int iy = r.oy + tap / 5 - G.pad, ix = r.ox + tap % 5 - G.pad;
+    const bool ok = r.ok && iy >= 0 && iy < G.H && ix >= 0 && ix < G.W;
+    const float* src = ok ? r.fin + ((int64_t)iy * G.W + ix) * G.Cin + ci0 : r.fin;
+#pragma unroll
+    for (int q = 0; q < kKC / 4; ++q) cp_async16(dst + 4 * q, src + 4 * q, ok);
+  } else {
+#pragma unroll 8
+    for (int kk = 0; kk < kKC; ++kk) {
+      const int k = k0 + kk;
+      bool ok = r.ok && k < G.K;
+      const float* src = r.fin;
+      if (ok) {
+        const int tap = k / G.Cin, ci = k % G.Cin;
+        const int iy = r.oy + tap / 5 - G.pad, ix = r.ox + tap % 5 - G.pad;
+        ok = iy >= 0 && iy < G.H && ix >= 0 && ix < G.W;
+        if (ok) src = r.fin + ((int64_t)iy * G.W + ix) * G.Cin + ci;
+      }
+      cp_async4(dst + kk, src, ok);
+    }
+  }
+  const float4* wsrc = reinterpret_cast<const float4*>(a.weights + (int64_t)c * 2 * kWChunkFloats);
+  float4* wdst = reinterpret_cast<float4*>(&sm.w[slot][0][0]);
+#pragma unroll
+  for (int e = tid; e < 2 * kWChunkFloats / 4; e += kThreadsConv) cp_async16(wdst + e, wsrc + e, true);
+}
+
+__global__ void __launch_bounds__(kThreadsConv, 1)
 conv_pool_kernel(pb_conv_actor a, pb_resolved res) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   ConvSmem& sm = *reinterpret_cast<ConvSmem*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  const int H = a.h, W = a.w, Cin = a.cin, pad = a.pad;
-  const int Ho = H + 2 * pad - 4, Wo = W + 2 * pad - 4;
-  const int Hp = Ho / 2, Wp = Wo / 2;
-  const int K = 25 * Cin;
-  const int n_chunks = (K + kKC - 1) / kKC;
-  const int64_t per_frame = (int64_t)Hp * Wp;
-  const int64_t per_unit = (int64_t)a.frames * per_frame;          // pooled pixels per firing
-  const int64_t tiles_per_unit = (per_unit + kPool - 1) / kPool;
-  const int64_t total = (int64_t)res.n_streams * res.n_iter * tiles_per_unit;
-  const int64_t in_frame_floats = (int64_t)H * W * Cin;
-  const int64_t out_frame_floats = per_frame * kCout;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const ConvGeom G = geom(a, res);
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -122,100 +225,77 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = sm.tmem_base;
 
-  uint32_t issued[kStages] = {0, 0};   // commits issued per stage (phase tracking)
-  int stage = 0;
-
-  for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
-    const int64_t unit = w / tiles_per_unit;
-    const int64_t tile = w % tiles_per_unit;
-    const int s = (int)(unit / res.n_iter);
-    const int j = (int)(unit % res.n_iter);
-    if (j >= pb::cond_count(res, a.cond, s)) continue;   // uniform across the CTA
-    const int n = pb::firing_iter(res, a.cond, s, j);
-    const float* in = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n));
-    float* out = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
-
-    // this thread's GEMM row: pooled pixel q = tid/4, window position tid%4
-    const int64_t g = tile * kPool + (tid >> 2);
-    const bool row_ok = g < per_unit;
-    int frame = 0, oy = 0, ox = 0;
-    if (row_ok) {
-      frame = (int)(g / per_frame);
-      const int p = (int)(g % per_frame);
-      oy = 2 * (p / Wp) + ((tid >> 1) & 1);
-      ox = 2 * (p % Wp) + (tid & 1);
+  // The CTA's work is a linear sequence of (tile, chunk) steps over its live
+  // tiles; the prefetcher runs kAhead steps ahead of the consumer.
+  int64_t pf_tile = blockIdx.x - (int64_t)gridDim.x;   // prefetch cursor
+  int pf_chunk = G.n_chunks;
+  RowCtx pf_row{};
+  auto advance_pf = [&]() -> bool {   // move the prefetch cursor one step
+    if (++pf_chunk >= G.n_chunks) {
+      pf_chunk = 0;
+      do {
+        pf_tile += gridDim.x;
+      } while (pf_tile < G.total && !tile_live(a, res, G, pf_tile));
+      if (pf_tile >= G.total) return false;
+      pf_row = row_ctx(a, res, G, pf_tile, tid);
     }
-    const float* fin = in + frame * in_frame_floats;
+    return true;
+  };
+  int64_t step_pf = 0;   // steps issued
+  bool pf_more = true;
+  for (int d = 0; d < kAhead; ++d) {
+    pf_more = pf_more && advance_pf();
+    if (pf_more) prefetch(sm, a, G, pf_row, pf_chunk, (int)(step_pf % kRing), tid);
+    cp_commit();
+    ++step_pf;
+  }
 
-    for (int c = 0; c < n_chunks; ++c) {
-      // the stage's previous MMAs must have drained before it is rewritten
+  int64_t tile = blockIdx.x - (int64_t)gridDim.x;
+  int64_t step = 0;
+  uint32_t issued[kStages] = {0, 0};
+  for (;;) {
+    do {
+      tile += gridDim.x;
+    } while (tile < G.total && !tile_live(a, res, G, tile));
+    if (tile >= G.total) break;
+    const RowCtx r = row_ctx(a, res, G, tile, tid);
+    for (int c = 0; c < G.n_chunks; ++c, ++step) {
+      const int stage = (int)(step & 1);
+      const int slot = (int)(step % kRing);
+      // the MMAs of step-2 used A stage `stage` and ring slot (step-2)%kRing
       if (issued[stage] > 0) mbar_wait(&sm.mma_done[stage], (issued[stage] - 1) & 1);
+      // refill the freed ring slot kAhead steps ahead
+      pf_more = pf_more && advance_pf();
+      if (pf_more) prefetch(sm, a, G, pf_row, pf_chunk, (int)(step_pf % kRing), tid);
+      cp_commit();
+      ++step_pf;
+      cp_wait<kAhead>();    // this step's group has landed (own row + own W share)
+      // split the own row into the MMA operand planes
+      const float* raw = sm.raw[slot] + tid * kRawStride;
       float* ahi = sm.a_hi[stage];
       float* alo = sm.a_lo[stage];
-      // ---- im2col gather of 32 K values for this row
-      const int k0 = c * kKC;
-      if (Cin % kKC == 0) {
-        // one (ky, kx) tap per chunk: 32 contiguous channels
-        const int tap = k0 / Cin, ci0 = k0 % Cin;
-        const int iy = oy + tap / 5 - pad, ix = ox + tap % 5 - pad;
-        const bool ok = row_ok && iy >= 0 && iy < H && ix >= 0 && ix < W;
-        const float4* src = reinterpret_cast<const float4*>(fin + ((int64_t)iy * W + ix) * Cin + ci0);
 #pragma unroll
-        for (int q = 0; q < kKC / 4; ++q) {
-          float4 v = ok ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-          float4 h, l;
-          split(v.x, h.x, l.x);
-          split(v.y, h.y, l.y);
-          split(v.z, h.z, l.z);
-          split(v.w, h.w, l.w);
-          const int off = core_off(tid, 4 * q);
-          *reinterpret_cast<float4*>(ahi + off) = h;
-          *reinterpret_cast<float4*>(alo + off) = l;
-        }
-      } else {
-#pragma unroll 4
-        for (int q = 0; q < kKC / 4; ++q) {
-          float v[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int k = k0 + 4 * q + e;
-            float x = 0.f;
-            if (row_ok && k < K) {
-              const int tap = k / Cin, ci = k % Cin;
-              const int iy = oy + tap / 5 - pad, ix = ox + tap % 5 - pad;
-              if (iy >= 0 && iy < H && ix >= 0 && ix < W) x = __ldg(fin + ((int64_t)iy * W + ix) * Cin + ci);
-            }
-            v[e] = x;
-          }
-          float4 h, l;
-          split(v[0], h.x, l.x);
-          split(v[1], h.y, l.y);
-          split(v[2], h.z, l.z);
-          split(v[3], h.w, l.w);
-          const int off = core_off(tid, 4 * q);
-          *reinterpret_cast<float4*>(ahi + off) = h;
-          *reinterpret_cast<float4*>(alo + off) = l;
-        }
-      }
-      // ---- weights of this chunk (pre-split, pre-laid-out on the host)
-      {
-        const float4* whi = reinterpret_cast<const float4*>(a.weights + (int64_t)c * 2 * kWChunkFloats);
-        const float4* wlo = whi + kWChunkFloats / 4;
-        float4* dhi = reinterpret_cast<float4*>(sm.w_hi[stage]);
-        float4* dlo = reinterpret_cast<float4*>(sm.w_lo[stage]);
-        for (int e = tid; e < kWChunkFloats / 4; e += kThreadsConv) {
-          dhi[e] = __ldg(whi + e);
-          dlo[e] = __ldg(wlo + e);
-        }
+      for (int q = 0; q < kKC / 4; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(raw + 4 * q);
+        float4 h, l;
+        split(v.x, h.x, l.x);
+        split(v.y, h.y, l.y);
+        split(v.z, h.z, l.z);
+        split(v.w, h.w, l.w);
+        const int off = core_off(tid, 4 * q);
+        *reinterpret_cast<float4*>(ahi + off) = h;
+        *reinterpret_cast<float4*>(alo + off) = l;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
+      __syncthreads();   // all rows split, all W shares landed
       if (tid == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;");
+        const float* whi = sm.w[slot][0];
+        const float* wlo = sm.w[slot][1];
 #pragma unroll
         for (int ks = 0; ks < kKC / 8; ++ks) {
           const uint64_t dah = sdesc(ahi + ks * 64), dal = sdesc(alo + ks * 64);
-          const uint64_t dwh = sdesc(sm.w_hi[stage] + ks * 64), dwl = sdesc(sm.w_lo[stage] + ks * 64);
+          const uint64_t dwh = sdesc(whi + ks * 64), dwl = sdesc(wlo + ks * 64);
           mma_tf32(tmem, dah, dwh, (c | ks) ? 1u : 0u);
           mma_tf32(tmem, dah, dwl, 1u);
           mma_tf32(tmem, dal, dwh, 1u);
@@ -226,35 +306,36 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res) {
             : "memory");
       }
       issued[stage] += 1;
-      stage ^= 1;
     }
-    // ---- epilogue: wait for the tile's last commit (it covers all MMAs)
-    const int last = stage ^ 1;
+    // ---- epilogue: the tile's last commit covers all of its MMAs
+    const int last = (int)((step - 1) & 1);
     mbar_wait(&sm.mma_done[last], (issued[last] - 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    uint32_t r[32];
+    uint32_t v32[32];
     const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
         "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "=r"(v32[0]), "=r"(v32[1]), "=r"(v32[2]), "=r"(v32[3]), "=r"(v32[4]), "=r"(v32[5]),
+          "=r"(v32[6]), "=r"(v32[7]), "=r"(v32[8]), "=r"(v32[9]), "=r"(v32[10]), "=r"(v32[11]),
+          "=r"(v32[12]), "=r"(v32[13]), "=r"(v32[14]), "=r"(v32[15]), "=r"(v32[16]),
+          "=r"(v32[17]), "=r"(v32[18]), "=r"(v32[19]), "=r"(v32[20]), "=r"(v32[21]),
+          "=r"(v32[22]), "=r"(v32[23]), "=r"(v32[24]), "=r"(v32[25]), "=r"(v32[26]),
+          "=r"(v32[27]), "=r"(v32[28]), "=r"(v32[29]), "=r"(v32[30]), "=r"(v32[31])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     float v[32];
 #pragma unroll
     for (int ch = 0; ch < 32; ++ch) {
-      float x = fmaxf(__fadd_rn(__uint_as_float(r[ch]), __ldg(a.bias + ch)), 0.0f);
+      float x = fmaxf(__fadd_rn(__uint_as_float(v32[ch]), __ldg(a.bias + ch)), 0.0f);
       x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 1));
       x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 2));
       v[ch] = x;
     }
-    if ((tid & 3) == 0 && row_ok) {
-      const int p = (int)(g % per_frame);
-      float4* dst = reinterpret_cast<float4*>(out + frame * out_frame_floats + (int64_t)p * kCout);
+    if ((tid & 3) == 0 && r.ok) {
+      const int frame = (int)(r.g / G.per_frame);
+      const int p = (int)(r.g % G.per_frame);
+      float4* dst = reinterpret_cast<float4*>(r.out + frame * G.out_frame + (int64_t)p * kCout);
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -263,6 +344,7 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res) {
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
   }
+  cp_wait<0>();
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0)
@@ -384,7 +466,7 @@ int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream) {
     PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     configured = true;
   }
-  conv_pool_kernel<<<2 * sms, kThreadsConv, smem, pb::as_stream(stream)>>>(actor, res);
+  conv_pool_kernel<<<sms, kThreadsConv, smem, pb::as_stream(stream)>>>(actor, res);
   PB_LAUNCHED("conv_pool_kernel");
   return PB_OK;
 }
