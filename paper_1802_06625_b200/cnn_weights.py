@@ -6,17 +6,13 @@ are He-normal from a seed (`he_normal`), so a graph description only carries
 seeds and shapes (or explicit `weights`/`bias` lists).
 
 `conv_device_layout` prepares a conv weight matrix W[cout][K] (K = 25*cin in
-(ky, kx, ci) order) for the tcgen05 kernel: per 32-wide K chunk, the TF32
-"hi" part (low 13 mantissa bits cleared) and the exact remainder "lo", each
-as a 32x32 K-major UMMA operand in core-matrix order [row/8][k/4][row%8][k%4]
-(csrc/pb_cnn.cu).
+(ky, kx, ci) order) for the tcgen05 kernel: per 16-wide K-step, the bf16
+"hi" part and the bf16-rounded remainder "lo" stacked as one 64-row UMMA B
+operand in core-matrix order [row/8][k/8][row%8][k%8] (csrc/pb_cnn.cu).
 """
 from __future__ import annotations
 
 import numpy as np
-
-KC = 32
-
 
 def he_normal(seed: int, rows: int, fan_in: int) -> np.ndarray:
     rng = np.random.default_rng(seed)
@@ -39,29 +35,46 @@ def layer_params(params, rows: int, fan_in: int) -> tuple[np.ndarray, np.ndarray
     return he_normal(seed, rows, fan_in), small_bias(seed, rows)
 
 
-def tf32_split(x: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
-    bits = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
-    hi = (bits & np.uint32(0xFFFFE000)).view(np.float32)
-    lo = (x.astype(np.float32) - hi).astype(np.float32)
+def bf16_rn(x: np.ndarray) -> np.ndarray:
+    """Round fp32 to bf16 (round-to-nearest-even), returned as fp32 values."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((b + 0x7FFF + ((b >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32)
+
+
+def bf16_split(x: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """x = hi + lo + O(2^-17 |x|), hi and lo bf16 (the kernel's converter)."""
+    x = np.asarray(x, dtype=np.float32)
+    hi = bf16_rn(x)
+    lo = bf16_rn((x - hi).astype(np.float32))
     return hi, lo
 
 
-def core_layout(tile: np.ndarray) -> np.ndarray:
-    """[rows][KC] -> UMMA K-major no-swizzle order [row/8][k/4][row%8][k%4]."""
-    rows = tile.shape[0]
-    t = tile.reshape(rows // 8, 8, KC // 4, 4)          # [r8][r%8][k4][k%4]
-    return np.ascontiguousarray(t.transpose(0, 2, 1, 3)).reshape(-1)
+def conv_steps(w: np.ndarray, cin: int) -> np.ndarray:
+    """W[32][25*cin] ((ky,kx,ci) order) -> the kernel's K-steps [steps][32][16].
+    cin == 3: step ky holds (kx, ci) at index kx*3+ci (15 used, 1 zero);
+    cin % 16 == 0: step (ky, kx, kc) holds channels 16kc..16kc+15."""
+    cout = w.shape[0]
+    wt = np.asarray(w, np.float32).reshape(cout, 5, 5, cin)
+    if cin == 3:
+        out = np.zeros((5, cout, 16), np.float32)
+        out[:, :, :15] = wt.reshape(cout, 5, 15).transpose(1, 0, 2)
+        return out
+    if cin % 16:
+        raise ValueError("conv: Cin must be 3 or a multiple of 16")
+    kc = cin // 16
+    return np.ascontiguousarray(
+        wt.reshape(cout, 25, kc, 16).transpose(1, 2, 0, 3)).reshape(25 * kc, cout, 16)
 
 
-def conv_device_layout(w: np.ndarray) -> np.ndarray:
-    """W[cout][K] -> per chunk [hi core][lo core], K zero-padded to 32."""
-    cout, K = w.shape
-    chunks = (K + KC - 1) // KC
-    wp = np.zeros((cout, chunks * KC), np.float32)
-    wp[:, :K] = w
-    hi, lo = tf32_split(wp)
-    out = []
-    for c in range(chunks):
-        out.append(core_layout(hi[:, c * KC:(c + 1) * KC]))
-        out.append(core_layout(lo[:, c * KC:(c + 1) * KC]))
-    return np.concatenate(out)
+def conv_device_layout(w: np.ndarray, cin: int) -> np.ndarray:
+    """Per K-step a 2 KB UMMA B operand [wh; wl] (64 rows x 16 bf16) in the
+    K-major no-swizzle core layout [row/8][kblock][row%8][8] (csrc/pb_cnn.cu).
+    Returned as uint16 bf16 bits."""
+    steps = conv_steps(w, cin)
+    hi, lo = bf16_split(steps)
+    both = np.concatenate([hi, lo], axis=1)                   # [S][64][16]
+    bits = (both.view(np.uint32) >> 16).astype(np.uint16)
+    S = bits.shape[0]
+    core = bits.reshape(S, 8, 8, 2, 8).transpose(0, 1, 3, 2, 4)   # [S][r/8][kb][r%8][8]
+    return np.ascontiguousarray(core).reshape(-1)

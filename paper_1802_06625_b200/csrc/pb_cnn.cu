@@ -4,351 +4,409 @@
 // oracle/cnn.py) and parity is stated as a tolerance, not bit-exactness.
 //
 // conv_pool_kernel: 5x5 convolution (NHWC fp32, zero padding) + bias + ReLU
-// + 2x2 max-pool as an implicit GEMM on tcgen05:
-//   D[128 conv pixels x 32 channels] += A[128 x K] * W[32 x K]^T,
-//   K = 25*Cin ordered (ky, kx, ci), chunks of 32.
-// Rows are 32 pooled pixels x their 4 conv pixels, so a pool window is 4
-// consecutive TMEM lanes of one warp.  Accuracy: split TF32 (3 MMAs,
-// hi*hi + hi*lo + lo*hi with x = hi + lo exactly), ~1e-6 relative.
-//   * all 4 warps gather the im2col chunk (hi and lo planes) into shared
-//     memory in the UMMA K-major no-swizzle core-matrix layout
-//     [row/8][k/4][row%8][k%4] (LBO = K-direction core stride 128 B,
-//     SBO = row-direction core stride 1024 B; probed in tools/umma_probe.cu);
-//   * weights are pre-split on the host into the same layout per chunk;
-//   * one thread issues 12 tcgen05.mma (kind::tf32, M=128 N=32 K=8) per
-//     chunk and commits them to the stage's mbarrier; two stages overlap the
-//     next gather with the running MMAs;
-//   * epilogue: tcgen05.ld 32 columns per lane, bias, ReLU, max over the
-//     four lanes of a window (warp shuffles), one 128 B NHWC store.
+// + 2x2 max-pool as an implicit GEMM on tcgen05 (kind::f16, bf16 operands,
+// fp32 accumulation in TMEM), persistent and warp-specialised:
+//
+//   * GEMM tile: M = 128 conv pixels laid out as 16 image rows x 8 columns,
+//     N = 32 output channels, K = 25 * Cin.  A 2x2 pool window is then two
+//     neighbouring lanes of two neighbouring 8-lane groups of ONE warp.
+//   * Accuracy: split bf16 ("bf16x3"): x = xh + xl, w = wh + wl (each bf16,
+//     round-to-nearest), D = xh*wh + xl*wh + xh*wl; the dropped xl*wl and
+//     the rounding of xl are ~2^-17 relative per product.  The B operand of
+//     the xh MMA is [wh; wl] (N = 64), so three products cost two MMAs;
+//     the epilogue adds the two 32-column halves.
+//   * No im2col: the converter warps stage each super-tile's input patch in
+//     shared memory ONCE, as bf16 hi / lo 16-byte "entry planes" in the UMMA
+//     K-major no-swizzle core layout, and every tap's A operand is just a
+//     shifted descriptor into that patch: rows of a core matrix are
+//     consecutive entries (16 B apart), SBO = one patch row (next image
+//     row), LBO = the plane stride (next 8 K elements).
+//       mode 1 (Cin % 16 == 0, layer 2): entry = one pixel, plane q holds
+//         channels 8q..8q+7; a K-step is one tap x 16 channels.
+//       mode 0 (Cin == 3, layer 1): entry (y, x) holds the 5*Cin values
+//         x[y][x..x+4][0..Cin) (zero-padded to 16); a K-step is one kernel
+//         row ky, so 5 MMA pairs cover the whole 5x5xCin window.
+//     Probed on hardware in tools/conv_probe.cu (window modes 0-2).
+//   * Roles: warps 0-3 epilogue (TMEM lane quarters), warp 4 MMA issue
+//     (one elected lane), warps 5-8 converters (global fp32 -> bf16 hi/lo
+//     patch).  Patches and TMEM accumulators are double-buffered and handed
+//     over with mbarriers (converters -> MMA: 128 arrivals; MMA -> converter
+//     and epilogue: tcgen05.commit; epilogue -> MMA: 128 arrivals).
+//   * All weights stay resident in shared memory for the whole launch.
 #include <algorithm>
+
+#include <cuda_bf16.h>
 
 #include "pb_common.cuh"
 
 namespace {
 
-constexpr int kRows = 128;            // conv pixels per tile (GEMM M)
-constexpr int kPool = kRows / 4;      // pooled pixels per tile
-constexpr int kCout = 32;             // GEMM N
-constexpr int kKC = 32;               // K per chunk
-constexpr int kThreadsConv = 128;
-constexpr int kChunkFloats = kRows * kKC;        // A plane per chunk
-constexpr int kWChunkFloats = kCout * kKC;       // W plane per chunk
-constexpr int kRawStride = kKC + 4;              // padded raw row (conflict-free LDS.128)
-constexpr int kAhead = 4;                        // chunks in flight ahead of the split
-constexpr int kRing = kAhead + 2;                // raw/W ring slots
-constexpr int kStages = 2;                       // split A planes (MMA operands)
-
-struct __align__(1024) ConvSmem {
-  float a_hi[kStages][kChunkFloats];             // UMMA operand, K-major core layout
-  float a_lo[kStages][kChunkFloats];
-  float w[kRing][2][kWChunkFloats];              // pre-split weights (hi, lo), cp.async ring
-  float raw[kRing][kRows * kRawStride];          // gathered im2col rows, cp.async ring
-  uint64_t mma_done[kStages];
-  uint32_t tmem_base;
-};
+constexpr int kTW = 8, kTH = 16;            // conv pixels per MMA tile (M = 128)
+constexpr int kST = 2;                      // tiles per super-tile (side by side)
+constexpr int kPH = kTH + 4;                // patch rows
+constexpr int kEpiWarps = 4, kCvtWarps = 4;
+constexpr int kMmaWarp = kEpiWarps;
+constexpr int kConvThreads = (kEpiWarps + 1 + kCvtWarps) * 32;
+constexpr int kCvtThreads = kCvtWarps * 32;
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kAccCols = 64;                // [xh*wh + xl*wh | xh*wl]
+constexpr int kTmemCols = 2 * kST * kAccCols;
+constexpr int kStepBytes = 64 * 16 * 2;     // one K-step of [wh; wl]: 64 rows x 16 bf16
+constexpr int kMaxSteps = 64;
+constexpr int kCout = 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ uint64_t sdesc(const void* p) {
-  uint64_t d = 0;
-  d |= (uint64_t)((smem_u32(p) & 0x3FFFF) >> 4);
-  d |= (uint64_t)(128 >> 4) << 16;                      // LBO: next core matrix along K
-  d |= (uint64_t)(((kKC / 4) * 128) >> 4) << 32;        // SBO: next core matrix along rows
-  d |= (uint64_t)1 << 46;                                // sm100 descriptor version
-  return d;                                              // SWIZZLE_NONE, base offset 0
+// Shared-memory matrix descriptor, K-major, no swizzle (sm100 version 1).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr & 0x3FFFF) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
 }
 
-__device__ __forceinline__ uint32_t idesc_tf32() {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kCout >> 3) << 17) |
-         ((uint32_t)(kRows >> 4) << 24);
+// kind::f16 instruction descriptor: bf16 A/B, fp32 D, K-major, M = 128.
+__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t acc) {
+__device__ __forceinline__ void mma_bf16(uint32_t tmem, uint64_t a, uint64_t b, uint32_t id,
+                                         uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-      "l"(a), "l"(b), "r"(idesc_tf32()), "r"(acc));
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\nW_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t@!p bra W_%=;\n\t}" ::"r"(
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(
           smem_u32(bar)),
-      "r"(parity), "r"(1000000u)
+      "r"(parity)
       : "memory");
 }
 
-// cp.async with zero fill: copies src_bytes (0 or size) and zero-fills the rest
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(valid ? 16 : 0)
-               : "memory");
+// x = hi + lo, each bf16 round-to-nearest; packs 8 values per 16 bytes.
+__device__ __forceinline__ uint32_t pack_hi(float a, float b, float& ra, float& rb) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  ra = a - __low2float(h);
+  rb = b - __high2float(h);
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
-__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(valid ? 4 : 0)
-               : "memory");
+__device__ __forceinline__ uint32_t pack_lo(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-__device__ __forceinline__ int core_off(int row, int k) {  // float offset in a plane
-  return ((row >> 3) * (kKC / 4) + (k >> 2)) * 32 + (row & 7) * 4 + (k & 3);
-}
-
-__device__ __forceinline__ void split(float x, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-  lo = __fsub_rn(x, hi);
+__device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
+  float r[8];
+  hi.x = pack_hi(v[0], v[1], r[0], r[1]);
+  hi.y = pack_hi(v[2], v[3], r[2], r[3]);
+  hi.z = pack_hi(v[4], v[5], r[4], r[5]);
+  hi.w = pack_hi(v[6], v[7], r[6], r[7]);
+  lo.x = pack_lo(r[0], r[1]);
+  lo.y = pack_lo(r[2], r[3]);
+  lo.z = pack_lo(r[4], r[5]);
+  lo.w = pack_lo(r[6], r[7]);
 }
 
-// Geometry of one conv layer launch.
+// Geometry of one conv launch (identical in every thread).
 struct ConvGeom {
-  int H, W, Cin, pad, Ho, Wo, Hp, Wp, K, n_chunks;
-  int64_t per_frame, per_unit, tiles_per_unit, total, in_frame, out_frame;
+  int H, W, Cin, pad, Ho, Wo, Hp, Wp;
+  int mode, np, pw, ps, steps, patch_bytes, w_bytes;
+  int sx_n, per_frame;
+  int64_t per_unit, total, in_frame, out_frame;
 };
 
-__device__ __forceinline__ ConvGeom geom(const pb_conv_actor& a, const pb_resolved& res) {
-  ConvGeom g;
+__host__ __device__ inline ConvGeom conv_geom(const pb_conv_actor& a, int n_streams, int n_iter) {
+  ConvGeom g{};
   g.H = a.h; g.W = a.w; g.Cin = a.cin; g.pad = a.pad;
   g.Ho = g.H + 2 * g.pad - 4; g.Wo = g.W + 2 * g.pad - 4;
   g.Hp = g.Ho / 2; g.Wp = g.Wo / 2;
-  g.K = 25 * g.Cin;
-  g.n_chunks = (g.K + kKC - 1) / kKC;
-  g.per_frame = (int64_t)g.Hp * g.Wp;
+  g.mode = (g.Cin % 16 == 0) ? 1 : 0;
+  g.np = g.mode ? g.Cin / 8 : 2;
+  g.pw = g.mode ? kST * kTW + 4 : kST * kTW;
+  g.ps = kPH * g.pw * 16;
+  g.steps = g.mode ? 25 * (g.Cin / 16) : 5;
+  g.patch_bytes = 2 * g.np * g.ps;
+  g.w_bytes = g.steps * kStepBytes;
+  g.sx_n = (g.Wo + kST * kTW - 1) / (kST * kTW);
+  g.per_frame = ((g.Ho + kTH - 1) / kTH) * g.sx_n;
   g.per_unit = (int64_t)a.frames * g.per_frame;
-  g.tiles_per_unit = (g.per_unit + kPool - 1) / kPool;
-  g.total = (int64_t)res.n_streams * res.n_iter * g.tiles_per_unit;
+  g.total = (int64_t)n_streams * n_iter * g.per_unit;
   g.in_frame = (int64_t)g.H * g.W * g.Cin;
-  g.out_frame = g.per_frame * kCout;
+  g.out_frame = (int64_t)g.Hp * g.Wp * kCout;
   return g;
 }
 
-// This thread's GEMM row of tile w: its input frame base and conv pixel.
-struct RowCtx {
-  const float* fin;   // input frame (nullptr: the tile is skipped)
-  float* out;         // output span of the firing
-  int64_t g;          // pooled pixel index within the firing
-  bool ok;
-  int oy, ox;
+inline size_t conv_smem_bytes(const ConvGeom& g) {
+  return 1024 + (size_t)g.w_bytes + 2 * (size_t)g.patch_bytes + 1024;
+}
+
+struct ConvBars {
+  uint64_t full[2], empty[2], acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+  uint16_t a_off[kMaxSteps];      // A start of each K-step, 16-byte units, tile 0
+  float bias[kCout];
 };
 
-__device__ __forceinline__ bool tile_live(const pb_conv_actor& a, const pb_resolved& res,
-                                          const ConvGeom& G, int64_t w) {
-  const int64_t unit = w / G.tiles_per_unit;
+// The super-tile a role is working on.
+struct SuperTile {
+  const float* fin;   // input frame
+  float* fout;        // output frame
+  int oy0, ox0;       // conv-output origin
+};
+
+__device__ __forceinline__ bool super_live(const pb_conv_actor& a, const pb_resolved& res,
+                                           const ConvGeom& G, int64_t w) {
+  const int64_t unit = w / G.per_unit;
   const int s = (int)(unit / res.n_iter), j = (int)(unit % res.n_iter);
   return j < pb::cond_count(res, a.cond, s);
 }
 
-__device__ __forceinline__ RowCtx row_ctx(const pb_conv_actor& a, const pb_resolved& res,
-                                          const ConvGeom& G, int64_t w, int tid) {
-  RowCtx r;
-  const int64_t unit = w / G.tiles_per_unit, tile = w % G.tiles_per_unit;
+__device__ __forceinline__ SuperTile super_tile(const pb_conv_actor& a, const pb_resolved& res,
+                                                const ConvGeom& G, int64_t w) {
+  const int64_t unit = w / G.per_unit, rem = w % G.per_unit;
   const int s = (int)(unit / res.n_iter), j = (int)(unit % res.n_iter);
   const int n = pb::firing_iter(res, a.cond, s, j);
-  const float* in = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n));
-  r.out = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
-  r.g = tile * kPool + (tid >> 2);
-  r.ok = r.g < G.per_unit;
-  int frame = 0;
-  r.oy = r.ox = 0;
-  if (r.ok) {
-    frame = (int)(r.g / G.per_frame);
-    const int p = (int)(r.g % G.per_frame);
-    r.oy = 2 * (p / G.Wp) + ((tid >> 1) & 1);
-    r.ox = 2 * (p % G.Wp) + (tid & 1);
-  }
-  r.fin = in + frame * G.in_frame;
-  return r;
+  const int f = (int)(rem / G.per_frame), st = (int)(rem % G.per_frame);
+  SuperTile t;
+  t.fin = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n)) + f * G.in_frame;
+  t.fout = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n)) + f * G.out_frame;
+  t.oy0 = (st / G.sx_n) * kTH;
+  t.ox0 = (st % G.sx_n) * (kST * kTW);
+  return t;
 }
 
-// Issue the asynchronous gather of chunk c of this thread's row (and its
-// share of the chunk's pre-split weights) into ring slot `slot`.
-__device__ __forceinline__ void prefetch(ConvSmem& sm, const pb_conv_actor& a, const ConvGeom& G,
-                                         const RowCtx& r, int c, int slot, int tid) {
-  float* dst = sm.raw[slot] + tid * kRawStride;
-  const int k0 = c * kKC;
-  if (G.Cin % kKC == 0) {
-    const int tap = k0 / G.Cin, ci0 = k0 % G.Cin;
-    const int iy = r.oy + tap / 5 - G.pad, ix = r.ox + tap % 5 - G.pad;
-    const bool ok = r.ok && iy >= 0 && iy < G.H && ix >= 0 && ix < G.W;
-    const float* src = ok ? r.fin + ((int64_t)iy * G.W + ix) * G.Cin + ci0 : r.fin;
+// Converter: stage the patch of super-tile `t` (bf16 hi planes then lo planes).
+__device__ __forceinline__ void fill_patch(uint8_t* patch, const ConvGeom& G, const SuperTile& t,
+                                           int ct) {
+  if (G.mode == 1) {
+    const int items = kPH * G.pw * G.np;
+    for (int i = ct; i < items; i += kCvtThreads) {
+      const int e = i / G.np, q = i % G.np;
+      const int iy = t.oy0 + e / G.pw - G.pad, ix = t.ox0 + e % G.pw - G.pad;
+      float v[8];
+      if (iy >= 0 && iy < G.H && ix >= 0 && ix < G.W) {
+        const float4* src = reinterpret_cast<const float4*>(
+            t.fin + ((int64_t)iy * G.W + ix) * G.Cin + 8 * q);
+        const float4 a = __ldg(src), b = __ldg(src + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+      } else {
 #pragma unroll
-    for (int q = 0; q < kKC / 4; ++q) cp_async16(dst + 4 * q, src + 4 * q, ok);
-  } else {
-#pragma unroll 8
-    for (int kk = 0; kk < kKC; ++kk) {
-      const int k = k0 + kk;
-      bool ok = r.ok && k < G.K;
-      const float* src = r.fin;
-      if (ok) {
-        const int tap = k / G.Cin, ci = k % G.Cin;
-        const int iy = r.oy + tap / 5 - G.pad, ix = r.ox + tap % 5 - G.pad;
-        ok = iy >= 0 && iy < G.H && ix >= 0 && ix < G.W;
-        if (ok) src = r.fin + ((int64_t)iy * G.W + ix) * G.Cin + ci;
+        for (int k = 0; k < 8; ++k) v[k] = 0.f;
       }
-      cp_async4(dst + kk, src, ok);
+      uint4 hi, lo;
+      split8(v, hi, lo);
+      *reinterpret_cast<uint4*>(patch + q * G.ps + e * 16) = hi;
+      *reinterpret_cast<uint4*>(patch + (G.np + q) * G.ps + e * 16) = lo;
+    }
+  } else {
+    const int items = kPH * G.pw;
+    for (int e = ct; e < items; e += kCvtThreads) {
+      const int iy = t.oy0 + e / G.pw - G.pad, ix0 = t.ox0 + e % G.pw - G.pad;
+      float v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = 0.f;
+      if (iy >= 0 && iy < G.H) {
+        const float* row = t.fin + (int64_t)iy * G.W * 3;
+#pragma unroll
+        for (int kx = 0; kx < 5; ++kx) {
+          const int ix = ix0 + kx;
+          if (ix >= 0 && ix < G.W) {
+#pragma unroll
+            for (int ci = 0; ci < 3; ++ci) v[kx * 3 + ci] = __ldg(row + ix * 3 + ci);
+          }
+        }
+      }
+      uint4 h0, l0, h1, l1;
+      split8(v, h0, l0);
+      split8(v + 8, h1, l1);
+      *reinterpret_cast<uint4*>(patch + 0 * G.ps + e * 16) = h0;
+      *reinterpret_cast<uint4*>(patch + 1 * G.ps + e * 16) = h1;
+      *reinterpret_cast<uint4*>(patch + 2 * G.ps + e * 16) = l0;
+      *reinterpret_cast<uint4*>(patch + 3 * G.ps + e * 16) = l1;
     }
   }
-  const float4* wsrc = reinterpret_cast<const float4*>(a.weights + (int64_t)c * 2 * kWChunkFloats);
-  float4* wdst = reinterpret_cast<float4*>(&sm.w[slot][0][0]);
-#pragma unroll
-  for (int e = tid; e < 2 * kWChunkFloats / 4; e += kThreadsConv) cp_async16(wdst + e, wsrc + e, true);
 }
 
-__global__ void __launch_bounds__(kThreadsConv, 1)
-conv_pool_kernel(pb_conv_actor a, pb_resolved res) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  ConvSmem& sm = *reinterpret_cast<ConvSmem*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const ConvGeom G = geom(a, res);
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
 
+__global__ void __launch_bounds__(kConvThreads, 1)
+conv_pool_kernel(pb_conv_actor a, pb_resolved res) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const ConvGeom G = conv_geom(a, res.n_streams, res.n_iter);
+  uint8_t* wsm = base;                                     // [steps][2 KB]
+  uint8_t* patch0 = base + G.w_bytes;                      // [2][patch_bytes]
+  ConvBars& B = *reinterpret_cast<ConvBars*>(base + G.w_bytes + 2 * G.patch_bytes);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---- prologue: weights, bias, step offsets, barriers, TMEM
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a.weights);
+    uint4* dst = reinterpret_cast<uint4*>(wsm);
+    for (int i = tid; i < G.w_bytes / 16; i += kConvThreads) dst[i] = __ldg(src + i);
+    if (tid < kCout) B.bias[tid] = __ldg(a.bias + tid);
+    for (int s = tid; s < G.steps; s += kConvThreads) {
+      int off;
+      if (G.mode == 1) {
+        const int kc_n = G.Cin / 16, tap = s / kc_n, kc = s % kc_n;
+        off = 2 * kc * G.ps + ((tap / 5) * G.pw + tap % 5) * 16;
+      } else {
+        off = s * G.pw * 16;
+      }
+      B.a_off[s] = (uint16_t)(off >> 4);
+    }
+  }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&sm.tmem_base)),
-                 "r"(32));
+                     smem_u32(&B.tmem_base)),
+                 "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.mma_done[s])));
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&B.full[b], kCvtThreads);
+      mbar_init(&B.empty[b], 1);
+      mbar_init(&B.acc_full[b], 1);
+      mbar_init(&B.acc_empty[b], kEpiThreads);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = sm.tmem_base;
+  const uint32_t tmem = B.tmem_base;
 
-  // The CTA's work is a linear sequence of (tile, chunk) steps over its live
-  // tiles; the prefetcher runs kAhead steps ahead of the consumer.
-  int64_t pf_tile = blockIdx.x - (int64_t)gridDim.x;   // prefetch cursor
-  int pf_chunk = G.n_chunks;
-  RowCtx pf_row{};
-  auto advance_pf = [&]() -> bool {   // move the prefetch cursor one step
-    if (++pf_chunk >= G.n_chunks) {
-      pf_chunk = 0;
-      do {
-        pf_tile += gridDim.x;
-      } while (pf_tile < G.total && !tile_live(a, res, G, pf_tile));
-      if (pf_tile >= G.total) return false;
-      pf_row = row_ctx(a, res, G, pf_tile, tid);
-    }
-    return true;
-  };
-  int64_t step_pf = 0;   // steps issued
-  bool pf_more = true;
-  for (int d = 0; d < kAhead; ++d) {
-    pf_more = pf_more && advance_pf();
-    if (pf_more) prefetch(sm, a, G, pf_row, pf_chunk, (int)(step_pf % kRing), tid);
-    cp_commit();
-    ++step_pf;
-  }
-
-  int64_t tile = blockIdx.x - (int64_t)gridDim.x;
-  int64_t step = 0;
-  uint32_t issued[kStages] = {0, 0};
-  for (;;) {
-    do {
-      tile += gridDim.x;
-    } while (tile < G.total && !tile_live(a, res, G, tile));
-    if (tile >= G.total) break;
-    const RowCtx r = row_ctx(a, res, G, tile, tid);
-    for (int c = 0; c < G.n_chunks; ++c, ++step) {
-      const int stage = (int)(step & 1);
-      const int slot = (int)(step % kRing);
-      // the MMAs of step-2 used A stage `stage` and ring slot (step-2)%kRing
-      if (issued[stage] > 0) mbar_wait(&sm.mma_done[stage], (issued[stage] - 1) & 1);
-      // refill the freed ring slot kAhead steps ahead
-      pf_more = pf_more && advance_pf();
-      if (pf_more) prefetch(sm, a, G, pf_row, pf_chunk, (int)(step_pf % kRing), tid);
-      cp_commit();
-      ++step_pf;
-      cp_wait<kAhead>();    // this step's group has landed (own row + own W share)
-      // split the own row into the MMA operand planes
-      const float* raw = sm.raw[slot] + tid * kRawStride;
-      float* ahi = sm.a_hi[stage];
-      float* alo = sm.a_lo[stage];
-#pragma unroll
-      for (int q = 0; q < kKC / 4; ++q) {
-        const float4 v = *reinterpret_cast<const float4*>(raw + 4 * q);
-        float4 h, l;
-        split(v.x, h.x, l.x);
-        split(v.y, h.y, l.y);
-        split(v.z, h.z, l.z);
-        split(v.w, h.w, l.w);
-        const int off = core_off(tid, 4 * q);
-        *reinterpret_cast<float4*>(ahi + off) = h;
-        *reinterpret_cast<float4*>(alo + off) = l;
-      }
+  if (warp >= kMmaWarp + 1) {
+    // ================================================ converters
+    const int ct = tid - (kMmaWarp + 1) * 32;
+    int it = 0;
+    for (int64_t w = blockIdx.x; w < G.total; w += gridDim.x) {
+      if (!super_live(a, res, G, w)) continue;
+      const int b = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      mbar_wait(&B.empty[b], (use & 1) ^ 1);
+      fill_patch(patch0 + b * G.patch_bytes, G, super_tile(a, res, G, w), ct);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();   // all rows split, all W shares landed
-      if (tid == 0) {
+      mbar_arrive(&B.full[b]);
+      ++it;
+    }
+  } else if (warp == kMmaWarp) {
+    // ================================================ MMA issue (one lane)
+    if (lane == 0) {
+      const uint32_t id64 = idesc_bf16(64), id32 = idesc_bf16(32);
+      const uint64_t db0 = sdesc(smem_u32(wsm), 128, 256);
+      int it = 0;
+      for (int64_t w = blockIdx.x; w < G.total; w += gridDim.x) {
+        if (!super_live(a, res, G, w)) continue;
+        const int b = it & 1;
+        const uint32_t use = (uint32_t)(it >> 1);
+        const int ox0 = (int)((w % G.per_unit) % G.per_frame % G.sx_n) * (kST * kTW);
+        mbar_wait(&B.full[b], use & 1);
+        mbar_wait(&B.acc_empty[b], (use & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const float* whi = sm.w[slot][0];
-        const float* wlo = sm.w[slot][1];
-#pragma unroll
-        for (int ks = 0; ks < kKC / 8; ++ks) {
-          const uint64_t dah = sdesc(ahi + ks * 64), dal = sdesc(alo + ks * 64);
-          const uint64_t dwh = sdesc(whi + ks * 64), dwl = sdesc(wlo + ks * 64);
-          mma_tf32(tmem, dah, dwh, (c | ks) ? 1u : 0u);
-          mma_tf32(tmem, dah, dwl, 1u);
-          mma_tf32(tmem, dal, dwh, 1u);
+        const uint64_t da0 = sdesc(smem_u32(patch0 + b * G.patch_bytes), G.ps, G.pw * 16);
+        const uint64_t lo_off = (uint64_t)((G.np * G.ps) >> 4);
+#pragma unroll 1
+        for (int t = 0; t < kST; ++t) {
+          if (ox0 + t * kTW >= G.Wo) break;
+          const uint32_t d = tmem + (uint32_t)((b * kST + t) * kAccCols);
+          const uint64_t dat = da0 + (uint64_t)(t * kTW);   // +8 entries = +128 B
+#pragma unroll 2
+          for (int s = 0; s < G.steps; ++s) {
+            const uint64_t dah = dat + B.a_off[s];
+            const uint64_t dbs = db0 + (uint64_t)(s * (kStepBytes >> 4));
+            mma_bf16(d, dah, dbs, id64, s > 0 ? 1u : 0u);
+            mma_bf16(d, dah + lo_off, dbs, id32, 1u);
+          }
         }
-        asm volatile(
-            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                smem_u32(&sm.mma_done[stage]))
-            : "memory");
+        mma_commit(&B.empty[b]);
+        mma_commit(&B.acc_full[b]);
+        ++it;
       }
-      issued[stage] += 1;
     }
-    // ---- epilogue: the tile's last commit covers all of its MMAs
-    const int last = (int)((step - 1) & 1);
-    mbar_wait(&sm.mma_done[last], (issued[last] - 1) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    uint32_t v32[32];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v32[0]), "=r"(v32[1]), "=r"(v32[2]), "=r"(v32[3]), "=r"(v32[4]), "=r"(v32[5]),
-          "=r"(v32[6]), "=r"(v32[7]), "=r"(v32[8]), "=r"(v32[9]), "=r"(v32[10]), "=r"(v32[11]),
-          "=r"(v32[12]), "=r"(v32[13]), "=r"(v32[14]), "=r"(v32[15]), "=r"(v32[16]),
-          "=r"(v32[17]), "=r"(v32[18]), "=r"(v32[19]), "=r"(v32[20]), "=r"(v32[21]),
-          "=r"(v32[22]), "=r"(v32[23]), "=r"(v32[24]), "=r"(v32[25]), "=r"(v32[26]),
-          "=r"(v32[27]), "=r"(v32[28]), "=r"(v32[29]), "=r"(v32[30]), "=r"(v32[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    float v[32];
+    __syncwarp();
+  } else {
+    // ================================================ epilogue (warps 0-3)
+    int it = 0;
+    const int gr = warp * 4 + (lane >> 3), x = lane & 7;   // tile row / column of this lane
+    for (int64_t w = blockIdx.x; w < G.total; w += gridDim.x) {
+      if (!super_live(a, res, G, w)) continue;
+      const int b = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      const SuperTile t = super_tile(a, res, G, w);
+      mbar_wait(&B.acc_full[b], use & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+      for (int tt = 0; tt < kST; ++tt) {
+        if (t.ox0 + tt * kTW >= G.Wo) break;
+        const uint32_t taddr =
+            tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((b * kST + tt) * kAccCols);
+        float v0[32], v1[32];
+        tmem_ld32(taddr, v0);
+        tmem_ld32(taddr + 32, v1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int ch = 0; ch < 32; ++ch) {
-      float x = fmaxf(__fadd_rn(__uint_as_float(v32[ch]), __ldg(a.bias + ch)), 0.0f);
-      x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 1));
-      x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 2));
-      v[ch] = x;
-    }
-    if ((tid & 3) == 0 && r.ok) {
-      const int frame = (int)(r.g / G.per_frame);
-      const int p = (int)(r.g % G.per_frame);
-      float4* dst = reinterpret_cast<float4*>(r.out + frame * G.out_frame + (int64_t)p * kCout);
+        for (int c = 0; c < 32; ++c) {
+          float y = fmaxf(__fadd_rn(__fadd_rn(v0[c], v1[c]), B.bias[c]), 0.0f);
+          y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 1));
+          y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 8));
+          v0[c] = y;
+        }
+        const int oy = t.oy0 + gr, ox = t.ox0 + tt * kTW + x;
+        if ((lane & 9) == 0 && oy < G.Ho && ox < G.Wo) {
+          float4* dst = reinterpret_cast<float4*>(
+              t.fout + ((int64_t)(oy >> 1) * G.Wp + (ox >> 1)) * kCout);
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          for (int q = 0; q < 8; ++q)
+            dst[q] = make_float4(v0[4 * q], v0[4 * q + 1], v0[4 * q + 2], v0[4 * q + 3]);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&B.acc_empty[b]);
+      ++it;
     }
-    // TMEM reads done before the next tile's first MMA overwrites D
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
   }
-  cp_wait<0>();
+
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(32));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
 }
 
 // ------------------------------------------------------------- dense (L3)
@@ -453,20 +511,23 @@ int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream) {
   const int Ho = actor.h + 2 * actor.pad - 4, Wo = actor.w + 2 * actor.pad - 4;
   if (Ho < 2 || Wo < 2 || Ho % 2 || Wo % 2)
     return pb::fail(PB_E_UNSUPPORTED, "conv: output must be even-sized for the 2x2 pool");
-  if (actor.cin % kKC != 0 && actor.cin > kKC)
-    return pb::fail(PB_E_UNSUPPORTED, "conv: Cin must be a multiple of 32 or < 32");
-  const size_t smem = sizeof(ConvSmem) + 1024;
-  static bool configured = false;
+  if (actor.cin != 3 && actor.cin % 16 != 0)
+    return pb::fail(PB_E_UNSUPPORTED, "conv: Cin must be 3 or a multiple of 16");
+  const ConvGeom G = conv_geom(actor, res.n_streams, res.n_iter);
+  const size_t smem = conv_smem_bytes(G) + sizeof(ConvBars);
+  if (G.steps > kMaxSteps || smem > 227 * 1024)
+    return pb::fail(PB_E_UNSUPPORTED, "conv: weights + patches exceed shared memory");
   static int sms = 0;
-  if (!configured) {
+  if (sms == 0) {
     PB_CUDA(cudaFuncSetAttribute(conv_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+                                 227 * 1024));
     int dev = 0;
     PB_CUDA(cudaGetDevice(&dev));
     PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    configured = true;
   }
-  conv_pool_kernel<<<sms, kThreadsConv, smem, pb::as_stream(stream)>>>(actor, res);
+  const int grid = (int)std::min<int64_t>(G.total, sms);
+  if (grid == 0) return PB_OK;
+  conv_pool_kernel<<<grid, kConvThreads, smem, pb::as_stream(stream)>>>(actor, res);
   PB_LAUNCHED("conv_pool_kernel");
   return PB_OK;
 }

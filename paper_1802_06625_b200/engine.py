@@ -474,7 +474,7 @@ class DeviceRuntime:
                 if fi.token_bytes != b.h * b.w * b.cin * 4:
                     raise UnsupportedGraph(f"{aid}: token is not one {b.h}x{b.w}x{b.cin} frame")
                 act = _lib.ConvActor(self._ref(in_f[0]), self._ref(out_f[0]),
-                                     self.mem.upload(conv_device_layout(b.weights)),
+                                     self.mem.upload(conv_device_layout(b.weights, b.cin)),
                                      self.mem.upload(b.bias), fi.rate, b.h, b.w, b.cin,
                                      b.cout, b.pad, plan.actor_cond[aid], 0)
                 self.launches.append(("conv", act))

@@ -6,38 +6,81 @@ from oracle import cnn as oc
 from paper_1802_06625_b200 import admit, as_graph
 from paper_1802_06625_b200.apps import vision
 from paper_1802_06625_b200.behaviors import resolve
-from paper_1802_06625_b200.cnn_weights import (KC, conv_device_layout, core_layout,
-                                               layer_params, tf32_split)
+from paper_1802_06625_b200.cnn_weights import (bf16_rn, bf16_split, conv_device_layout,
+                                               conv_steps, layer_params)
 
 
-def test_tf32_split_is_exact():
-    x = np.random.default_rng(0).standard_normal(10000).astype(np.float32)
-    hi, lo = tf32_split(x)
-    assert (hi + lo == x).all()
-    assert ((hi.view(np.uint32) & 0x1FFF) == 0).all()
+def test_bf16_rn_matches_torch():
+    import torch
+    x = np.random.default_rng(0).standard_normal(100000).astype(np.float32) * 37.0
+    want = torch.from_numpy(x).to(torch.bfloat16).to(torch.float32).numpy()
+    assert (bf16_rn(x) == want).all()
 
 
-def test_core_layout_matches_kernel_indexing():
-    rows = 32
-    t = np.arange(rows * KC, dtype=np.float32).reshape(rows, KC)
-    flat = core_layout(t)
-    for r in range(rows):
-        for k in range(KC):
-            off = ((r // 8) * (KC // 4) + k // 4) * 32 + (r % 8) * 4 + k % 4
-            assert flat[off] == t[r, k]
+def test_bf16_split_accuracy():
+    x = np.random.default_rng(1).standard_normal(100000).astype(np.float32)
+    hi, lo = bf16_split(x)
+    assert ((hi.view(np.uint32) & 0xFFFF) == 0).all() and ((lo.view(np.uint32) & 0xFFFF) == 0).all()
+    rel = np.abs((hi.astype(np.float64) + lo) - x) / np.abs(x)
+    assert rel.max() <= 2.0 ** -17
+
+
+def _unpack(dev, steps):
+    """Inverse of conv_device_layout: [S][64][16] fp32 from bf16 bits."""
+    bits = dev.reshape(steps, 8, 2, 8, 8).transpose(0, 1, 3, 2, 4).reshape(steps, 64, 16)
+    return (bits.astype(np.uint32) << 16).view(np.float32)
 
 
 def test_conv_device_layout_roundtrip():
-    w, _ = layer_params({"seed": 1}, 32, 75)
-    dev = conv_device_layout(w).reshape(-1, 2, 32 * KC)
-    assert dev.shape[0] == 3   # 75 -> 96 padded K
-    rec = np.zeros((32, 3 * KC), np.float32)
-    for c in range(3):
-        for r in range(32):
-            for k in range(KC):
-                off = ((r // 8) * (KC // 4) + k // 4) * 32 + (r % 8) * 4 + k % 4
-                rec[r, c * KC + k] = dev[c, 0, off] + dev[c, 1, off]
-    assert (rec[:, :75] == w).all() and (rec[:, 75:] == 0).all()
+    for cin, steps in ((3, 5), (32, 50)):
+        w, _ = layer_params({"seed": 1}, 32, 25 * cin)
+        dev = conv_device_layout(w, cin)
+        assert dev.dtype == np.uint16 and dev.size == steps * 64 * 16
+        m = _unpack(dev, steps)
+        hi, lo = bf16_split(conv_steps(w, cin))
+        assert (m[:, :32] == hi).all() and (m[:, 32:] == lo).all()
+        rec = conv_steps(w, cin)
+        if cin == 3:   # step ky, index kx*3+ci
+            assert (rec[:, :, 15] == 0).all()
+            assert (rec.transpose(1, 0, 2)[:, :, :15].reshape(32, 75) == w).all()
+        else:          # step (ky, kx, kc), channel 16kc+e
+            assert (rec.reshape(25, 2, 32, 16).transpose(2, 0, 1, 3).reshape(32, 800) == w).all()
+
+
+def emulate_conv(x, w, b, pad):
+    """The kernel's arithmetic on the CPU: operands split to bf16 hi/lo,
+    D = xh*wh + xl*wh + xh*wl (float64 accumulation ~ TMEM fp32), bias,
+    ReLU, 2x2 max pool."""
+    F, H, W, Cin = x.shape
+    xh, xl = bf16_split(x)
+    wh, wl = bf16_split(w)
+    xp = [np.pad(a.astype(np.float64), ((0, 0), (pad, pad), (pad, pad), (0, 0))) for a in (xh, xl)]
+    Ho, Wo = H + 2 * pad - 4, W + 2 * pad - 4
+    def im2col(a):
+        cols = np.empty((F, Ho, Wo, 25 * Cin))
+        for ky in range(5):
+            for kx in range(5):
+                t = ky * 5 + kx
+                cols[..., t * Cin:(t + 1) * Cin] = a[:, ky:ky + Ho, kx:kx + Wo, :]
+        return cols
+    ch, cl = im2col(xp[0]), im2col(xp[1])
+    y = ch @ wh.astype(np.float64).T + cl @ wh.astype(np.float64).T + ch @ wl.astype(np.float64).T
+    y = np.maximum(y + b, 0.0)
+    return y.reshape(F, Ho // 2, 2, Wo // 2, 2, -1).max(axis=(2, 4))
+
+
+def test_split_bf16_conv_within_tolerance():
+    """bf16x3 meets the stated activation tolerance (1e-4 of max(1,|y|)) on
+    the vision graph's own layer shapes."""
+    p = oc.graph_params(vision.build_description(1))
+    x = vision.make_frames(0, 1)
+    want1 = oc.conv_relu_pool(x, *p["l1"])
+    got1 = emulate_conv(x, *p["l1"])
+    assert (np.abs(got1 - want1) / np.maximum(1, np.abs(want1))).max() <= 2e-5
+    x2 = want1.astype(np.float32)
+    want2 = oc.conv_relu_pool(x2, *p["l2"])
+    got2 = emulate_conv(x2, *p["l2"])
+    assert (np.abs(got2 - want2) / np.maximum(1, np.abs(want2))).max() <= 2e-5
 
 
 def test_oracle_conv_against_direct_loops():
