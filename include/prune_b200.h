@@ -304,14 +304,15 @@ int pb_fire_path_merge(pb_path_merge_actor actor, pb_resolved res, void* stream)
  * Tokens are NHWC fp32 frames; `frames` = frames per firing (port rate). */
 
 /* conv2d_relu_pool: 5x5 conv (zero pad), bias, ReLU, 2x2 max pool, 32 output
- * channels, as a tcgen05 implicit GEMM (split-TF32, fp32 accumulate in TMEM).
- * weights: host-prepared per 32-wide K chunk (K = 25*cin ordered ky,kx,ci):
- * [hi 32x32][lo 32x32] in the UMMA K-major core-matrix layout (see
- * paper_1802_06625_b200/cnn_weights.py). */
+ * channels, as a warp-specialised tcgen05 implicit GEMM (bf16x3 split
+ * operands, fp32 accumulation in TMEM).  cin must be 3 or a multiple of 16.
+ * weights: the host-prepared device layout of W[32][25*cin] ((ky,kx,ci)
+ * order): per 16-wide K-step a 64-row [bf16 hi; bf16 lo] UMMA operand
+ * (paper_1802_06625_b200/cnn_weights.py conv_device_layout). */
 typedef struct {
   pb_span_ref in;
   pb_span_ref out;
-  const float* weights;
+  const void* weights;
   const float* bias;       /* [32] */
   int32_t frames;
   int32_t h, w, cin, cout, pad;
@@ -320,11 +321,14 @@ typedef struct {
 } pb_conv_actor;
 int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream);
 
-/* dense: out[f] = W x[f] + b, W row-major [nout][nin] (fp32 FMA). */
+/* dense: out[f] = W x[f] + b, W [nout][nin] (nout <= 112, nin % 64 == 0), as a
+ * tcgen05 GEMM over 128 frames gathered across firings (bf16x3 split, fp32
+ * accumulation; split-K with a deterministic last-CTA reduction when there
+ * are fewer frame tiles than SMs).  weights: cnn_weights.dense_device_layout. */
 typedef struct {
   pb_span_ref in;
   pb_span_ref out;
-  const float* weights;
+  const void* weights;
   const float* bias;
   int32_t frames, nin, nout, cond;
 } pb_dense_actor;

@@ -78,3 +78,24 @@ def conv_device_layout(w: np.ndarray, cin: int) -> np.ndarray:
     S = bits.shape[0]
     core = bits.reshape(S, 8, 8, 2, 8).transpose(0, 1, 3, 2, 4)   # [S][r/8][kb][r%8][8]
     return np.ascontiguousarray(core).reshape(-1)
+
+
+DENSE_N = 112   # padded outputs per precision half (csrc/pb_cnn.cu kDN)
+
+
+def dense_device_layout(w: np.ndarray) -> np.ndarray:
+    """W[nout][nin] -> per 16-wide K-step a UMMA B operand of 224 rows
+    [wh (nout, zero-padded to 112); wl (same)] x 16 bf16 in the K-major
+    no-swizzle core layout [row/8][kblock][row%8][8]; steps are contiguous, so
+    a 64-wide K chunk is one 28 KB block.  Returned as uint16 bf16 bits."""
+    nout, nin = w.shape
+    if nout > DENSE_N or nin % 64:
+        raise ValueError("dense: nout <= 112 and nin a multiple of 64")
+    hi, lo = bf16_split(w)
+    rows = np.zeros((2 * DENSE_N, nin), np.float32)
+    rows[:nout] = hi
+    rows[DENSE_N:DENSE_N + nout] = lo
+    bits = (rows.view(np.uint32) >> 16).astype(np.uint16)
+    S = nin // 16
+    core = bits.reshape(2 * DENSE_N // 8, 8, S, 2, 8).transpose(2, 0, 3, 1, 4)
+    return np.ascontiguousarray(core).reshape(-1)

@@ -410,60 +410,221 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res) {
 }
 
 // ------------------------------------------------------------- dense (L3)
-// out[f][o] = b[o] + sum_k x[f][k] * w[o][k], k ascending (fp32 FMA, one
-// accumulator per output: deterministic).  One CTA per firing: the firing's
-// frames and 32-wide K slices of all weight rows are staged in shared memory,
-// so each weight element is read once per firing.
-constexpr int kDenseThreads = 256;
-constexpr int kDenseKC = 32;
-constexpr int kDenseMaxF = 32;
-constexpr int kDenseMaxOut = 128;
+// out[f] = W x[f] + b, W [nout][nin], as a tcgen05 GEMM with the same bf16x3
+// split as the convolutions: M = 128 frames gathered across the launch's
+// live firings (rows of a tile may come from different firings and
+// streams), N = [wh; wl] padded to 2 x 112 rows so one MMA gives xh*wh and
+// xh*wl and a second (N = 112) adds xl*wh into the first half, K = nin in
+// 64-wide chunks through a 3-stage ring: the weight chunk arrives by one
+// cp.async.bulk (pre-split on the host, cnn_weights.dense_device_layout),
+// the frame chunk is split to bf16 hi/lo by the converter warps.  When there
+// are fewer M-tiles than SMs the K range is split across CTAs and the last
+// CTA of a tile sums the partials in split order (deterministic).
+constexpr int kDN = 112;                    // padded outputs per precision half
+constexpr int kDKC = 64;                    // K per pipeline chunk (4 K16 steps)
+constexpr int kDStages = 3;
+constexpr int kDStepBytes = 2 * kDN * 16 * 2;       // [wh; wl] 224 rows x 16 bf16
+constexpr int kDChunkBytes = 4 * kDStepBytes;       // 28 KB
+constexpr int kDAPiece = 128 * kDKC * 2;            // 16 KB (one precision piece)
+constexpr int kDTmemCols = 256;
 
-__global__ void __launch_bounds__(kDenseThreads)
-dense_kernel(pb_dense_actor a, pb_resolved res) {
-  const int s = blockIdx.y;
-  const int j = blockIdx.x;
-  if (j >= pb::cond_count(res, a.cond, s)) return;
-  const int n = pb::firing_iter(res, a.cond, s, j);
-  const float* x = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n));
-  float* out = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
-  __shared__ float xs[kDenseMaxF][kDenseKC + 1];
-  __shared__ float ws[kDenseMaxOut][kDenseKC + 1];
-  const int o = threadIdx.x % kDenseMaxOut;
-  const int fg = threadIdx.x / kDenseMaxOut;                 // 0 or 1
-  float acc[kDenseMaxF / 2];
-#pragma unroll
-  for (int i = 0; i < kDenseMaxF / 2; ++i) acc[i] = 0.f;
-  for (int k0 = 0; k0 < a.nin; k0 += kDenseKC) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < a.frames * kDenseKC; e += kDenseThreads) {
-      const int f = e / kDenseKC, k = e % kDenseKC;
-      xs[f][k] = k0 + k < a.nin ? __ldg(x + (int64_t)f * a.nin + k0 + k) : 0.f;
+struct DenseSmem {
+  uint8_t a[kDStages][2][kDAPiece];        // K-major core layout [row/8][kb][row%8][16 B]
+  uint8_t b[kDStages][kDChunkBytes];
+  uint64_t full[kDStages], empty[kDStages], acc_full;
+  uint32_t tmem_base;
+  int last;
+  const float* rowp[128];
+  float* outp[128];
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kConvThreads, 1)
+dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, int chunks_per_split) {
+  extern __shared__ uint8_t smem_raw[];
+  DenseSmem& S = *reinterpret_cast<DenseSmem*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int mt = blockIdx.x, split = blockIdx.y, splits = gridDim.y;
+  const int n_chunks = a.nin / kDKC;
+  const int c0 = split * chunks_per_split;
+  const int c1 = min(n_chunks, c0 + chunks_per_split);
+
+  // ---- rows of this tile: the m-th frame over the live firings, stream-major
+  if (tid < 128) {
+    const int64_t m = (int64_t)mt * 128 + tid;
+    const int64_t unit = m / a.frames;
+    const int f = (int)(m % a.frames);
+    const float* rp = nullptr;
+    float* op = nullptr;
+    int64_t acc = 0;
+    for (int s = 0; s < res.n_streams; ++s) {
+      const int cnt = pb::cond_count(res, a.cond, s);
+      if (unit < acc + cnt) {
+        const int n = pb::firing_iter(res, a.cond, s, (int)(unit - acc));
+        rp = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n)) + (int64_t)f * a.nin;
+        op = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n)) + (int64_t)f * a.nout;
+        break;
+      }
+      acc += cnt;
     }
-    for (int e = threadIdx.x; e < a.nout * kDenseKC; e += kDenseThreads) {
-      const int r = e / kDenseKC, k = e % kDenseKC;
-      ws[r][k] = k0 + k < a.nin ? __ldg(a.weights + (int64_t)r * a.nin + k0 + k) : 0.f;
+    S.rowp[tid] = rp;
+    S.outp[tid] = op;
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&S.tmem_base)), "r"(kDTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int st = 0; st < kDStages; ++st) {
+      mbar_init(&S.full[st], kCvtThreads);
+      mbar_init(&S.empty[st], 1);
     }
-    __syncthreads();
-    if (o < a.nout) {
-#pragma unroll 4
-      for (int k = 0; k < kDenseKC; ++k) {
-        const float wv = ws[o][k];
+    mbar_init(&S.acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = S.tmem_base;
+  bool any_row = false;
+  for (int r = 0; r < 128 && !any_row; ++r) any_row = S.rowp[r] != nullptr;
+  const uint8_t* wg = reinterpret_cast<const uint8_t*>(a.weights);
+
+  if (!any_row) {
+    // nothing to do (tile beyond the live frames)
+  } else if (warp >= kMmaWarp + 1) {
+    // ================================================ converters + weight copies
+    const int ct = tid - (kMmaWarp + 1) * 32;
+    for (int c = c0, it = 0; c < c1; ++c, ++it) {
+      const int st = it % kDStages;
+      const uint32_t use = (uint32_t)(it / kDStages);
+      mbar_wait(&S.empty[st], (use & 1) ^ 1);
+      if (ct == 0) {
+        mbar_arrive_tx(&S.full[st], kDChunkBytes);
+        bulk_g2s(S.b[st], wg + (int64_t)c * kDChunkBytes, kDChunkBytes, &S.full[st]);
+      }
+      // 128 rows x 4 quarters of 16 K: 4 items per thread, 4 threads per row
 #pragma unroll
-        for (int i = 0; i < kDenseMaxF / 2; ++i) {
-          const int f = fg + 2 * i;
-          if (f < a.frames) acc[i] = fmaf(xs[f][k], wv, acc[i]);
+      for (int k = 0; k < 4; ++k) {
+        const int i = ct + k * kCvtThreads;
+        const int r = i >> 2, q = i & 3;
+        const float* rp = S.rowp[r];
+        float v[16];
+        if (rp != nullptr) {
+          const float4* src = reinterpret_cast<const float4*>(rp + (int64_t)c * kDKC + 16 * q);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4 t = __ldg(src + u);
+            v[4 * u] = t.x; v[4 * u + 1] = t.y; v[4 * u + 2] = t.z; v[4 * u + 3] = t.w;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = 0.f;
         }
+        uint4 h0, l0, h1, l1;
+        split8(v, h0, l0);
+        split8(v + 8, h1, l1);
+        // K-blocks 2q and 2q+1 of row r
+        const int o0 = ((r >> 3) * 8 + 2 * q) * 128 + (r & 7) * 16;
+        *reinterpret_cast<uint4*>(S.a[st][0] + o0) = h0;
+        *reinterpret_cast<uint4*>(S.a[st][0] + o0 + 128) = h1;
+        *reinterpret_cast<uint4*>(S.a[st][1] + o0) = l0;
+        *reinterpret_cast<uint4*>(S.a[st][1] + o0 + 128) = l1;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (ct != 0) mbar_arrive(&S.full[st]);
+    }
+  } else if (warp == kMmaWarp) {
+    // ================================================ MMA issue
+    if (lane == 0) {
+      const uint32_t id224 = idesc_bf16(2 * kDN), id112 = idesc_bf16(kDN);
+      for (int c = c0, it = 0; c < c1; ++c, ++it) {
+        const int st = it % kDStages;
+        const uint32_t use = (uint32_t)(it / kDStages);
+        mbar_wait(&S.full[st], use & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint64_t dah = sdesc(smem_u32(S.a[st][0]), 128, 1024);
+        const uint64_t dal = sdesc(smem_u32(S.a[st][1]), 128, 1024);
+        const uint64_t db = sdesc(smem_u32(S.b[st]), 128, 256);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t ak = (uint64_t)(k * 256 >> 4), bk = (uint64_t)(k * kDStepBytes >> 4);
+          mma_bf16(tmem, dah + ak, db + bk, id224, (it | k) ? 1u : 0u);
+          mma_bf16(tmem, dal + ak, db + bk, id112, 1u);
+        }
+        mma_commit(&S.empty[st]);
+      }
+      mma_commit(&S.acc_full);
+    }
+    __syncwarp();
+  } else {
+    // ================================================ epilogue (warps 0-3)
+    const int r = warp * 32 + lane;
+    mbar_wait(&S.acc_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+    float y[kDN];
+#pragma unroll
+    for (int c = 0; c < kDN; c += 32) {
+      float t0[32], t1[32];
+      tmem_ld32(tl + c, t0);          // xh*wh + xl*wh, outputs c..c+31
+      tmem_ld32(tl + kDN + c, t1);    // xh*wl
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int u = 0; u < 32; ++u)
+        if (c + u < kDN) y[c + u] = __fadd_rn(t0[u], t1[u]);
+    }
+    const int64_t m = (int64_t)mt * 128 + r;
+    float* op = S.outp[r];
+    if (splits == 1) {
+      if (op != nullptr) {
+#pragma unroll
+        for (int o = 0; o < kDN; ++o)
+          if (o < a.nout) op[o] = __fadd_rn(y[o], __ldg(a.bias + o));
+      }
+    } else {
+      float* mine = partial + ((int64_t)split * gridDim.x * 128 + m) * kDN;
+#pragma unroll
+      for (int o = 0; o < kDN; o += 4)
+        *reinterpret_cast<float4*>(mine + o) = make_float4(y[o], y[o + 1], y[o + 2], y[o + 3]);
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
+      if (r == 0) S.last = (atomicAdd(counters + mt, 1) == splits - 1);
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
+      if (S.last) {
+        __threadfence();
+        if (op != nullptr) {
+          for (int o = 0; o < a.nout; ++o) {
+            float acc = 0.f;
+            for (int sp = 0; sp < splits; ++sp)
+              acc = __fadd_rn(acc, __ldcg(partial + ((int64_t)sp * gridDim.x * 128 + m) * kDN + o));
+            op[o] = __fadd_rn(acc, __ldg(a.bias + o));
+          }
+        }
+        if (r == 0) counters[mt] = 0;
       }
     }
   }
-  if (o < a.nout) {
-#pragma unroll
-    for (int i = 0; i < kDenseMaxF / 2; ++i) {
-      const int f = fg + 2 * i;
-      if (f < a.frames) out[(int64_t)f * a.nout + o] = __fadd_rn(acc[i], a.bias[o]);
-    }
-  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kDTmemCols));
 }
 
 // ------------------------------------------------- classify / bypass merge
@@ -534,10 +695,44 @@ int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream) {
 
 int pb_fire_dense(pb_dense_actor actor, pb_resolved res, void* stream) {
   if (res.n_iter == 0) return PB_OK;
-  if (actor.frames > kDenseMaxF || actor.nout > kDenseMaxOut)
-    return pb::fail(PB_E_UNSUPPORTED, "dense: at most 32 frames and 128 outputs per firing");
-  dim3 grid(res.n_iter, res.n_streams);
-  dense_kernel<<<grid, kDenseThreads, 0, pb::as_stream(stream)>>>(actor, res);
+  if (actor.nout > kDN || actor.nin % kDKC != 0)
+    return pb::fail(PB_E_UNSUPPORTED, "dense: nout <= 112 and nin a multiple of 64");
+  static int sms = 0;
+  static float* partial = nullptr;
+  static size_t partial_bytes = 0;
+  static int* counters = nullptr;
+  static int counters_n = 0;
+  if (sms == 0) {
+    PB_CUDA(cudaFuncSetAttribute(dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(DenseSmem) + 1024)));
+    int dev = 0;
+    PB_CUDA(cudaGetDevice(&dev));
+    PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int64_t rows = (int64_t)res.n_streams * res.n_iter * actor.frames;
+  const int m_tiles = (int)((rows + 127) / 128);
+  const int n_chunks = actor.nin / kDKC;
+  int splits = std::max(1, std::min({sms / std::max(1, m_tiles), 16, n_chunks}));
+  const int cps = (n_chunks + splits - 1) / splits;
+  splits = (n_chunks + cps - 1) / cps;
+  cudaStream_t st = pb::as_stream(stream);
+  if (splits > 1) {
+    const size_t need = (size_t)splits * m_tiles * 128 * kDN * sizeof(float);
+    if (need > partial_bytes) {
+      if (partial) PB_CUDA(cudaFree(partial));
+      PB_CUDA(cudaMalloc(&partial, need));
+      partial_bytes = need;
+    }
+    if (m_tiles > counters_n) {
+      if (counters) PB_CUDA(cudaFree(counters));
+      PB_CUDA(cudaMalloc(&counters, sizeof(int) * m_tiles));
+      PB_CUDA(cudaMemsetAsync(counters, 0, sizeof(int) * m_tiles, st));
+      counters_n = m_tiles;
+    }
+  }
+  dim3 grid(m_tiles, splits);
+  dense_kernel<<<grid, kConvThreads, sizeof(DenseSmem) + 1024, st>>>(actor, res, partial, counters,
+                                                                      cps);
   PB_LAUNCHED("dense_kernel");
   return PB_OK;
 }

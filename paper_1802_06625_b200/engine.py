@@ -481,8 +481,10 @@ class DeviceRuntime:
             elif kind == "dense":
                 b.init(aid, a.params, None)
                 fi = g.fifo(in_f[0])
+                from .cnn_weights import dense_device_layout
                 act = _lib.DenseActor(self._ref(in_f[0]), self._ref(out_f[0]),
-                                      self.mem.upload(b.weights), self.mem.upload(b.bias),
+                                      self.mem.upload(dense_device_layout(b.weights)),
+                                      self.mem.upload(b.bias),
                                       fi.rate, b.nin, b.nout, plan.actor_cond[aid])
                 self.launches.append(("dense", act))
             elif kind == "classify":

@@ -47,6 +47,18 @@ def test_conv_device_layout_roundtrip():
             assert (rec.reshape(25, 2, 32, 16).transpose(2, 0, 1, 3).reshape(32, 800) == w).all()
 
 
+def test_dense_device_layout_roundtrip():
+    from paper_1802_06625_b200.cnn_weights import dense_device_layout
+    w, _ = layer_params({"seed": 3}, 100, 256)
+    dev = dense_device_layout(w)
+    S = 256 // 16
+    bits = dev.reshape(S, 28, 2, 8, 8).transpose(1, 3, 0, 2, 4).reshape(224, 256)
+    m = (bits.astype(np.uint32) << 16).view(np.float32)
+    hi, lo = bf16_split(w)
+    assert (m[:100] == hi).all() and (m[112:212] == lo).all()
+    assert (m[100:112] == 0).all() and (m[212:] == 0).all()
+
+
 def emulate_conv(x, w, b, pad):
     """The kernel's arithmetic on the CPU: operands split to bf16 hi/lo,
     D = xh*wh + xl*wh + xh*wl (float64 accumulation ~ TMEM fp32), bias,

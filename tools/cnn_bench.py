@@ -36,10 +36,15 @@ def measure(S=4, firings=64, R=24, steps=20):
         return e.value
     marks = {}
 
+    seen = {}
+
     def hook(kind, phase):
         e = ev()
         lib.pb_event_record(e, rt.stream)
-        marks.setdefault(kind, []).append(e)
+        if phase == "pre":   # conv launches of one epoch are l1 then l2
+            seen[kind] = seen.get(kind, 0) + 1
+        k = kind if kind != "conv" else f"conv_l{(seen[kind] - 1) % 2 + 1}"
+        marks.setdefault(k, []).append(e)
     e0, e1 = ev(), ev()
     lib.pb_event_record(e0, rt.stream)
     for _ in range(steps):
