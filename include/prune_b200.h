@@ -317,7 +317,8 @@ typedef struct {
   int32_t frames;
   int32_t h, w, cin, cout, pad;
   int32_t cond;
-  int32_t pad_;
+  int32_t debug;           /* 0; profiling only: bit0 skip patch fill, bit1 skip
+                              epilogue, bit2 skip MMAs (results are garbage) */
 } pb_conv_actor;
 int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream);
 

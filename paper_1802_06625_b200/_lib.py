@@ -99,7 +99,7 @@ class PathMergeActor(C.Structure):
 class ConvActor(C.Structure):
     _fields_ = [("in_", SpanRef), ("out", SpanRef), ("weights", vp), ("bias", vp),
                 ("frames", i32), ("h", i32), ("w", i32), ("cin", i32), ("cout", i32),
-                ("pad", i32), ("cond", i32), ("pad_", i32)]
+                ("pad", i32), ("cond", i32), ("debug", i32)]
 
 
 class DenseActor(C.Structure):

@@ -8,6 +8,7 @@
 // fp32 accumulation in TMEM), persistent and warp-specialised:
 //
 //   * GEMM tile: M = 128 conv pixels laid out as 16 image rows x 8 columns,
+//     2 (layer 2) or 4 (layer 1) tiles side by side per super-tile,
 //     N = 32 output channels, K = 25 * Cin.  A 2x2 pool window is then two
 //     neighbouring lanes of two neighbouring 8-lane groups of ONE warp.
 //   * Accuracy: split bf16 ("bf16x3"): x = xh + xl, w = wh + wl (each bf16,
@@ -27,14 +28,16 @@
 //         x[y][x..x+4][0..Cin) (zero-padded to 16); a K-step is one kernel
 //         row ky, so 5 MMA pairs cover the whole 5x5xCin window.
 //     Probed on hardware in tools/conv_probe.cu (window modes 0-2).
-//   * Roles: warps 0-3 epilogue (TMEM lane quarters), warp 4 MMA issue
-//     (one elected lane), warps 5-8 converters (global fp32 -> bf16 hi/lo
+//   * Roles: warps 0-7 epilogue (TMEM lane quarter = warp % 4), warp 8 MMA issue
+//     (one elected lane), warps 9-15 converters (global fp32 -> bf16 hi/lo
 //     patch).  Patches and TMEM accumulators are double-buffered and handed
 //     over with mbarriers (converters -> MMA: 128 arrivals; MMA -> converter
 //     and epilogue: tcgen05.commit; epilogue -> MMA: 128 arrivals).
 //   * All weights stay resident in shared memory for the whole launch.
 #include <algorithm>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
 #include "pb_common.cuh"
@@ -42,18 +45,18 @@
 namespace {
 
 constexpr int kTW = 8, kTH = 16;            // conv pixels per MMA tile (M = 128)
-constexpr int kST = 2;                      // tiles per super-tile (side by side)
+constexpr int kMaxST = 4;                   // tiles per super-tile (side by side): mode 0 4, mode 1 2
 constexpr int kPH = kTH + 4;                // patch rows
-constexpr int kEpiWarps = 4, kCvtWarps = 4;
+constexpr int kEpiWarps = 8, kCvtWarps = 7;   // 16 warps: 4 per SM sub-partition, 128 regs
 constexpr int kMmaWarp = kEpiWarps;
+constexpr int kCvtWarp0 = kMmaWarp + 1;
 constexpr int kConvThreads = (kEpiWarps + 1 + kCvtWarps) * 32;
 constexpr int kCvtThreads = kCvtWarps * 32;
 constexpr int kEpiThreads = kEpiWarps * 32;
-constexpr int kAccCols = 64;                // [xh*wh + xl*wh | xh*wl]
-constexpr int kTmemCols = 2 * kST * kAccCols;
+constexpr int kTmemCols = 256;              // 2 accumulator sets x ST tiles x ACC columns
 constexpr int kStepBytes = 64 * 16 * 2;     // one K-step of [wh; wl]: 64 rows x 16 bf16
-constexpr int kMaxSteps = 64;
 constexpr int kCout = 32;
+constexpr int kRawBufs = 6;                 // layer-1 raw boxes in flight (prefetch depth 5)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -103,6 +106,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
 // x = hi + lo, each bf16 round-to-nearest; packs 8 values per 16 bytes.
 __device__ __forceinline__ uint32_t pack_hi(float a, float b, float& ra, float& rb) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -126,123 +142,204 @@ __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
   lo.w = pack_lo(r[6], r[7]);
 }
 
-// Geometry of one conv launch (identical in every thread).
-struct ConvGeom {
-  int H, W, Cin, pad, Ho, Wo, Hp, Wp;
-  int mode, np, pw, ps, steps, patch_bytes, w_bytes;
-  int sx_n, per_frame;
-  int64_t per_unit, total, in_frame, out_frame;
+// Geometry of one conv layer.  MODE/CIN are template parameters (layer 1:
+// <0, 3>, layer 2: <1, 32>), so every shared-memory offset and every MMA
+// descriptor step is a compile-time constant and the issue loop is a straight
+// run of tcgen05.mma with immediate descriptor offsets.
+template <int MODE, int CIN>
+struct ConvCfg {
+  static constexpr int ST = MODE ? 2 : 4;                 // tiles per super-tile
+  static constexpr int NP = MODE ? CIN / 8 : 2;           // 16-B planes per precision piece
+  static constexpr int PW = ST * kTW + (MODE ? 4 : 0);    // patch width (entries)
+  static constexpr int PS = kPH * PW * 16;                // plane stride (bytes)
+  static constexpr int STEPS = MODE ? 25 * (CIN / 16) : 5;
+  // layer 2 is MMA-bound: B = [wh; wl] (N = 64) gives two products per MMA and
+  // the epilogue adds the column halves; layer 1 is epilogue-bound: three
+  // N = 32 MMAs accumulate all products into 32 columns
+  static constexpr bool SPLIT3 = MODE == 0;
+  static constexpr int ACC = SPLIT3 ? 32 : 64;            // TMEM columns per tile
+  static constexpr int PATCH = 2 * NP * PS;
+  static constexpr int WBYTES = STEPS * kStepBytes;
+  // layer-1 raw input box staged by one TMA tensor load: kPH rows x
+  // (PW + 4) pixels x 3 channels fp32, zero-filled outside the frame; the box
+  // starts on a 16-byte boundary (a TMA requirement for the inner
+  // coordinate), so it carries up to 3 extra leading floats
+  static constexpr int RAW_W = MODE ? 0 : ((PW + 4) * 3 + 3 + 3) / 4 * 4;   // floats per raw row
+  static constexpr int RAW_TX = kPH * RAW_W * 4;          // bytes per box
+  static constexpr int RAW = MODE ? 0 : ((RAW_TX + 127) / 128) * 128;
+  static constexpr int SMEM = WBYTES + 2 * PATCH + kRawBufs * RAW;
+  static __host__ __device__ constexpr int a_off(int s) {   // bytes, tile 0, hi piece
+    return MODE ? 2 * (s % (CIN / 16)) * PS + (((s / (CIN / 16)) / 5) * PW + (s / (CIN / 16)) % 5) * 16
+                : s * PW * 16;
+  }
 };
 
-__host__ __device__ inline ConvGeom conv_geom(const pb_conv_actor& a, int n_streams, int n_iter) {
-  ConvGeom g{};
-  g.H = a.h; g.W = a.w; g.Cin = a.cin; g.pad = a.pad;
+struct ConvRun {   // runtime geometry
+  int H, W, pad, Ho, Wo, Hp, Wp, sx_n, per_frame, per_unit, n_units;
+  int64_t in_frame, out_frame;
+};
+
+template <class Cfg>
+__device__ __forceinline__ ConvRun conv_run(const pb_conv_actor& a, const pb_resolved& res) {
+  ConvRun g;
+  g.H = a.h; g.W = a.w; g.pad = a.pad;
   g.Ho = g.H + 2 * g.pad - 4; g.Wo = g.W + 2 * g.pad - 4;
   g.Hp = g.Ho / 2; g.Wp = g.Wo / 2;
-  g.mode = (g.Cin % 16 == 0) ? 1 : 0;
-  g.np = g.mode ? g.Cin / 8 : 2;
-  g.pw = g.mode ? kST * kTW + 4 : kST * kTW;
-  g.ps = kPH * g.pw * 16;
-  g.steps = g.mode ? 25 * (g.Cin / 16) : 5;
-  g.patch_bytes = 2 * g.np * g.ps;
-  g.w_bytes = g.steps * kStepBytes;
-  g.sx_n = (g.Wo + kST * kTW - 1) / (kST * kTW);
+  g.sx_n = (g.Wo + Cfg::ST * kTW - 1) / (Cfg::ST * kTW);
   g.per_frame = ((g.Ho + kTH - 1) / kTH) * g.sx_n;
-  g.per_unit = (int64_t)a.frames * g.per_frame;
-  g.total = (int64_t)n_streams * n_iter * g.per_unit;
-  g.in_frame = (int64_t)g.H * g.W * g.Cin;
+  g.per_unit = a.frames * g.per_frame;
+  g.n_units = res.n_streams * res.n_iter;
+  g.in_frame = (int64_t)g.H * g.W * a.cin;
   g.out_frame = (int64_t)g.Hp * g.Wp * kCout;
   return g;
 }
 
-inline size_t conv_smem_bytes(const ConvGeom& g) {
-  return 1024 + (size_t)g.w_bytes + 2 * (size_t)g.patch_bytes + 1024;
-}
-
 struct ConvBars {
-  uint64_t full[2], empty[2], acc_full[2], acc_empty[2];
+  uint64_t full[2], empty[2], acc_full[2], acc_empty[2], raw_full[kRawBufs];
   uint32_t tmem_base;
-  uint16_t a_off[kMaxSteps];      // A start of each K-step, 16-byte units, tile 0
   float bias[kCout];
 };
 
-// The super-tile a role is working on.
+// Walks this CTA's super-tiles (w = blockIdx.x, += gridDim.x) over the live
+// firings without 64-bit divisions: unit = (stream, iteration), rem = the
+// super-tile within the unit's frames.
+struct Cursor {
+  int unit, rem, s, j;
+  bool live;
+};
+
+__device__ __forceinline__ void cursor_fix(Cursor& c, const ConvRun& g, const pb_conv_actor& a,
+                                           const pb_resolved& res) {
+  if (c.unit < g.n_units) {
+    c.s = c.unit / res.n_iter;
+    c.j = c.unit - c.s * res.n_iter;
+    c.live = c.j < pb::cond_count(res, a.cond, c.s);
+  }
+}
+
+__device__ __forceinline__ Cursor cursor_first(const ConvRun& g, const pb_conv_actor& a,
+                                               const pb_resolved& res) {
+  Cursor c;
+  c.unit = blockIdx.x / g.per_unit;
+  c.rem = blockIdx.x - c.unit * g.per_unit;
+  c.live = false;
+  cursor_fix(c, g, a, res);
+  return c;
+}
+
+__device__ __forceinline__ void cursor_step(Cursor& c, const ConvRun& g, const pb_conv_actor& a,
+                                            const pb_resolved& res) {
+  c.rem += gridDim.x;
+  if (c.rem >= g.per_unit) {
+    while (c.rem >= g.per_unit) {
+      c.rem -= g.per_unit;
+      ++c.unit;
+    }
+    cursor_fix(c, g, a, res);
+  }
+}
+
+// next live super-tile (including the current one)
+__device__ __forceinline__ bool cursor_live(Cursor& c, const ConvRun& g, const pb_conv_actor& a,
+                                            const pb_resolved& res) {
+  while (c.unit < g.n_units && !c.live) cursor_step(c, g, a, res);
+  return c.unit < g.n_units;
+}
+
 struct SuperTile {
   const float* fin;   // input frame
   float* fout;        // output frame
   int oy0, ox0;       // conv-output origin
 };
 
-__device__ __forceinline__ bool super_live(const pb_conv_actor& a, const pb_resolved& res,
-                                           const ConvGeom& G, int64_t w) {
-  const int64_t unit = w / G.per_unit;
-  const int s = (int)(unit / res.n_iter), j = (int)(unit % res.n_iter);
-  return j < pb::cond_count(res, a.cond, s);
-}
-
-__device__ __forceinline__ SuperTile super_tile(const pb_conv_actor& a, const pb_resolved& res,
-                                                const ConvGeom& G, int64_t w) {
-  const int64_t unit = w / G.per_unit, rem = w % G.per_unit;
-  const int s = (int)(unit / res.n_iter), j = (int)(unit % res.n_iter);
-  const int n = pb::firing_iter(res, a.cond, s, j);
-  const int f = (int)(rem / G.per_frame), st = (int)(rem % G.per_frame);
+template <class Cfg>
+__device__ __forceinline__ SuperTile super_tile(const Cursor& c, const ConvRun& g,
+                                                const pb_conv_actor& a, const pb_resolved& res) {
+  const int n = pb::firing_iter(res, a.cond, c.s, c.j);
+  const int f = c.rem / g.per_frame, st = c.rem - f * g.per_frame;
+  const int sy = st / g.sx_n;
   SuperTile t;
-  t.fin = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n)) + f * G.in_frame;
-  t.fout = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n)) + f * G.out_frame;
-  t.oy0 = (st / G.sx_n) * kTH;
-  t.ox0 = (st % G.sx_n) * (kST * kTW);
+  t.fin = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, c.s, n)) + f * g.in_frame;
+  t.fout = reinterpret_cast<float*>(pb::span_ptr(a.out, res, c.s, n)) + f * g.out_frame;
+  t.oy0 = sy * kTH;
+  t.ox0 = (st - sy * g.sx_n) * (Cfg::ST * kTW);
   return t;
 }
 
-// Converter: stage the patch of super-tile `t` (bf16 hi planes then lo planes).
-__device__ __forceinline__ void fill_patch(uint8_t* patch, const ConvGeom& G, const SuperTile& t,
-                                           int ct) {
-  if (G.mode == 1) {
-    const int items = kPH * G.pw * G.np;
-    for (int i = ct; i < items; i += kCvtThreads) {
-      const int e = i / G.np, q = i % G.np;
-      const int iy = t.oy0 + e / G.pw - G.pad, ix = t.ox0 + e % G.pw - G.pad;
-      float v[8];
-      if (iy >= 0 && iy < G.H && ix >= 0 && ix < G.W) {
-        const float4* src = reinterpret_cast<const float4*>(
-            t.fin + ((int64_t)iy * G.W + ix) * G.Cin + 8 * q);
-        const float4 a = __ldg(src), b = __ldg(src + 1);
-        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-      } else {
+// Layer 1: one TMA tensor load of the raw box a super-tile needs (rows
+// oy0-pad .. +kPH, pixels ox0-pad .. +PW+4, all 3 channels); the tensor map
+// spans every frame of the input ring, so padding is the TMA zero fill.
+template <class Cfg>
+__device__ __forceinline__ void raw_issue(uint8_t* raw, uint64_t* bar, const CUtensorMap* tmap,
+                                          const ConvRun& g, const pb_conv_actor& a,
+                                          const SuperTile& t) {
+  const int frame = (int)((t.fin - reinterpret_cast<const float*>(a.in.data)) / g.in_frame);
+  mbar_arrive_tx(bar, Cfg::RAW_TX);
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(raw)),
+      "l"(tmap), "r"(((t.ox0 - g.pad) * 3) & ~3), "r"(t.oy0 - g.pad), "r"(frame), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Converter: build the bf16 hi/lo entry planes of super-tile `t` in `patch`.
+template <int MODE, int CIN>
+__device__ __forceinline__ void fill_patch(uint8_t* patch, const uint8_t* raw, const ConvRun& g,
+                                           const SuperTile& t, int ct) {
+  using Cfg = ConvCfg<MODE, CIN>;
+  if constexpr (MODE == 1) {
+    constexpr int kB = 4;
+    constexpr int items = kPH * Cfg::PW * Cfg::NP;
+#pragma unroll 1
+    for (int i0 = ct; i0 < items; i0 += kB * kCvtThreads) {
+      float v[kB][8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = 0.f;
-      }
-      uint4 hi, lo;
-      split8(v, hi, lo);
-      *reinterpret_cast<uint4*>(patch + q * G.ps + e * 16) = hi;
-      *reinterpret_cast<uint4*>(patch + (G.np + q) * G.ps + e * 16) = lo;
-    }
-  } else {
-    const int items = kPH * G.pw;
-    for (int e = ct; e < items; e += kCvtThreads) {
-      const int iy = t.oy0 + e / G.pw - G.pad, ix0 = t.ox0 + e % G.pw - G.pad;
-      float v[16];
+      for (int u = 0; u < kB; ++u) {
+        const int i = i0 + u * kCvtThreads;
+        const int e = i / Cfg::NP, q = i % Cfg::NP;
+        const int iy = t.oy0 + e / Cfg::PW - g.pad, ix = t.ox0 + e % Cfg::PW - g.pad;
+        if (i < items && iy >= 0 && iy < g.H && ix >= 0 && ix < g.W) {
+          const float4* src = reinterpret_cast<const float4*>(
+              t.fin + ((int64_t)iy * g.W + ix) * CIN + 8 * q);
+          const float4 a = __ldg(src), b = __ldg(src + 1);
+          v[u][0] = a.x; v[u][1] = a.y; v[u][2] = a.z; v[u][3] = a.w;
+          v[u][4] = b.x; v[u][5] = b.y; v[u][6] = b.z; v[u][7] = b.w;
+        } else {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = 0.f;
-      if (iy >= 0 && iy < G.H) {
-        const float* row = t.fin + (int64_t)iy * G.W * 3;
-#pragma unroll
-        for (int kx = 0; kx < 5; ++kx) {
-          const int ix = ix0 + kx;
-          if (ix >= 0 && ix < G.W) {
-#pragma unroll
-            for (int ci = 0; ci < 3; ++ci) v[kx * 3 + ci] = __ldg(row + ix * 3 + ci);
-          }
+          for (int k = 0; k < 8; ++k) v[u][k] = 0.f;
         }
       }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int i = i0 + u * kCvtThreads;
+        if (i >= items) break;
+        const int e = i / Cfg::NP, q = i % Cfg::NP;
+        uint4 hi, lo;
+        split8(v[u], hi, lo);
+        *reinterpret_cast<uint4*>(patch + q * Cfg::PS + e * 16) = hi;
+        *reinterpret_cast<uint4*>(patch + (Cfg::NP + q) * Cfg::PS + e * 16) = lo;
+      }
+    }
+  } else {
+    // entries from the raw box in shared memory (out-of-frame pixels are
+    // already zero)
+    constexpr int items = kPH * Cfg::PW;
+    const float* rawf = reinterpret_cast<const float*>(raw) + (((t.ox0 - g.pad) * 3) & 3);
+#pragma unroll 1
+    for (int e = ct; e < items; e += kCvtThreads) {
+      const int r = e / Cfg::PW, c = e % Cfg::PW;
+      const float* src = rawf + r * Cfg::RAW_W + c * 3;
+      float v[16];
+#pragma unroll
+      for (int k = 0; k < 15; ++k) v[k] = src[k];
+      v[15] = 0.f;
       uint4 h0, l0, h1, l1;
       split8(v, h0, l0);
       split8(v + 8, h1, l1);
-      *reinterpret_cast<uint4*>(patch + 0 * G.ps + e * 16) = h0;
-      *reinterpret_cast<uint4*>(patch + 1 * G.ps + e * 16) = h1;
-      *reinterpret_cast<uint4*>(patch + 2 * G.ps + e * 16) = l0;
-      *reinterpret_cast<uint4*>(patch + 3 * G.ps + e * 16) = l1;
+      *reinterpret_cast<uint4*>(patch + 0 * Cfg::PS + e * 16) = h0;
+      *reinterpret_cast<uint4*>(patch + 1 * Cfg::PS + e * 16) = h1;
+      *reinterpret_cast<uint4*>(patch + 2 * Cfg::PS + e * 16) = l0;
+      *reinterpret_cast<uint4*>(patch + 3 * Cfg::PS + e * 16) = l1;
     }
   }
 }
@@ -262,33 +359,34 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(p));
+  return p != 0;
+}
+
+template <int MODE, int CIN>
 __global__ void __launch_bounds__(kConvThreads, 1)
-conv_pool_kernel(pb_conv_actor a, pb_resolved res) {
+conv_pool_kernel(pb_conv_actor a, pb_resolved res, const __grid_constant__ CUtensorMap tmap) {
+  using Cfg = ConvCfg<MODE, CIN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const ConvGeom G = conv_geom(a, res.n_streams, res.n_iter);
-  uint8_t* wsm = base;                                     // [steps][2 KB]
-  uint8_t* patch0 = base + G.w_bytes;                      // [2][patch_bytes]
-  ConvBars& B = *reinterpret_cast<ConvBars*>(base + G.w_bytes + 2 * G.patch_bytes);
+  const ConvRun G = conv_run<Cfg>(a, res);
+  uint8_t* wsm = base;                                   // [STEPS][2 KB]
+  uint8_t* patch0 = base + Cfg::WBYTES;                  // [2][PATCH]
+  uint8_t* raw0 = patch0 + 2 * Cfg::PATCH;               // [kRawBufs][RAW] (layer 1)
+  ConvBars& B = *reinterpret_cast<ConvBars*>(base + Cfg::SMEM);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // ---- prologue: weights, bias, step offsets, barriers, TMEM
+  // ---- prologue: weights, bias, barriers, TMEM
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.weights);
     uint4* dst = reinterpret_cast<uint4*>(wsm);
-    for (int i = tid; i < G.w_bytes / 16; i += kConvThreads) dst[i] = __ldg(src + i);
+    for (int i = tid; i < Cfg::WBYTES / 16; i += kConvThreads) dst[i] = __ldg(src + i);
     if (tid < kCout) B.bias[tid] = __ldg(a.bias + tid);
-    for (int s = tid; s < G.steps; s += kConvThreads) {
-      int off;
-      if (G.mode == 1) {
-        const int kc_n = G.Cin / 16, tap = s / kc_n, kc = s % kc_n;
-        off = 2 * kc * G.ps + ((tap / 5) * G.pw + tap % 5) * 16;
-      } else {
-        off = s * G.pw * 16;
-      }
-      B.a_off[s] = (uint16_t)(off >> 4);
-    }
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -303,6 +401,7 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res) {
       mbar_init(&B.acc_full[b], 1);
       mbar_init(&B.acc_empty[b], kEpiThreads);
     }
+    for (int b = 0; b < kRawBufs; ++b) mbar_init(&B.raw_full[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -311,89 +410,145 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = B.tmem_base;
 
-  if (warp >= kMmaWarp + 1) {
+  if (warp >= kCvtWarp0) {
     // ================================================ converters
-    const int ct = tid - (kMmaWarp + 1) * 32;
-    int it = 0;
-    for (int64_t w = blockIdx.x; w < G.total; w += gridDim.x) {
-      if (!super_live(a, res, G, w)) continue;
+    const int ct = tid - kCvtWarp0 * 32;
+    Cursor c = cursor_first(G, a, res);
+    Cursor pf = c;               // layer 1: raw-box prefetch cursor, 2 super-tiles ahead
+    int it = 0, pf_it = 0;
+    if constexpr (MODE == 0) {
+      for (int k = 0; k < kRawBufs - 1 && cursor_live(pf, G, a, res); ++k, ++pf_it) {
+        if (ct == 0)
+          raw_issue<Cfg>(raw0 + (pf_it % kRawBufs) * Cfg::RAW, &B.raw_full[pf_it % kRawBufs],
+                         &tmap, G, a, super_tile<Cfg>(pf, G, a, res));
+        cursor_step(pf, G, a, res);
+      }
+    }
+    while (cursor_live(c, G, a, res)) {
+      const SuperTile t = super_tile<Cfg>(c, G, a, res);
       const int b = it & 1;
       const uint32_t use = (uint32_t)(it >> 1);
+      const int rb = it % kRawBufs;
+      cursor_step(c, G, a, res);
+      if constexpr (MODE == 0) mbar_wait(&B.raw_full[rb], (uint32_t)(it / kRawBufs) & 1);
       mbar_wait(&B.empty[b], (use & 1) ^ 1);
-      fill_patch(patch0 + b * G.patch_bytes, G, super_tile(a, res, G, w), ct);
+      if (!(a.debug & 1)) fill_patch<MODE, CIN>(patch0 + b * Cfg::PATCH, raw0 + rb * Cfg::RAW, G, t, ct);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&B.full[b]);
+      if constexpr (MODE == 0) {
+        // every converter is done with raw[rb]: refill it with the super-tile
+        // kRawBufs - 1 ahead
+        asm volatile("bar.sync 2, %0;" ::"n"(kCvtThreads));
+        if (cursor_live(pf, G, a, res)) {
+          if (ct == 0)
+            raw_issue<Cfg>(raw0 + (pf_it % kRawBufs) * Cfg::RAW, &B.raw_full[pf_it % kRawBufs],
+                           &tmap, G, a, super_tile<Cfg>(pf, G, a, res));
+          cursor_step(pf, G, a, res);
+          ++pf_it;
+        }
+      }
       ++it;
     }
   } else if (warp == kMmaWarp) {
-    // ================================================ MMA issue (one lane)
-    if (lane == 0) {
-      const uint32_t id64 = idesc_bf16(64), id32 = idesc_bf16(32);
-      const uint64_t db0 = sdesc(smem_u32(wsm), 128, 256);
-      int it = 0;
-      for (int64_t w = blockIdx.x; w < G.total; w += gridDim.x) {
-        if (!super_live(a, res, G, w)) continue;
-        const int b = it & 1;
-        const uint32_t use = (uint32_t)(it >> 1);
-        const int ox0 = (int)((w % G.per_unit) % G.per_frame % G.sx_n) * (kST * kTW);
-        mbar_wait(&B.full[b], use & 1);
-        mbar_wait(&B.acc_empty[b], (use & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint64_t da0 = sdesc(smem_u32(patch0 + b * G.patch_bytes), G.ps, G.pw * 16);
-        const uint64_t lo_off = (uint64_t)((G.np * G.ps) >> 4);
-#pragma unroll 1
-        for (int t = 0; t < kST; ++t) {
-          if (ox0 + t * kTW >= G.Wo) break;
-          const uint32_t d = tmem + (uint32_t)((b * kST + t) * kAccCols);
-          const uint64_t dat = da0 + (uint64_t)(t * kTW);   // +8 entries = +128 B
-#pragma unroll 2
-          for (int s = 0; s < G.steps; ++s) {
-            const uint64_t dah = dat + B.a_off[s];
+    // ================================================ MMA issue (warp-uniform loop, one lane issues)
+    constexpr uint32_t id64 = idesc_bf16(64), id32 = idesc_bf16(32);
+    const uint64_t db0 = sdesc(smem_u32(wsm), 128, 256);
+    Cursor c = cursor_first(G, a, res);
+    int it = 0;
+    while (cursor_live(c, G, a, res)) {
+      const int b = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      const int st = c.rem % G.per_frame;
+      const int ox0 = (st % G.sx_n) * (Cfg::ST * kTW);
+      cursor_step(c, G, a, res);
+      mbar_wait(&B.full[b], use & 1);
+      mbar_wait(&B.acc_empty[b], (use & 1) ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint64_t da0 = sdesc(smem_u32(patch0 + b * Cfg::PATCH), Cfg::PS, Cfg::PW * 16);
+      if (elect_one()) {
+#pragma unroll
+        for (int t = 0; t < Cfg::ST; ++t) {
+          if (ox0 + t * kTW >= G.Wo || (a.debug & 4)) break;
+          const uint32_t d = tmem + (uint32_t)((b * Cfg::ST + t) * Cfg::ACC);
+#pragma unroll
+          for (int s = 0; s < Cfg::STEPS; ++s) {
+            const uint64_t dah = da0 + (uint64_t)((Cfg::a_off(s) + t * kTW * 16) >> 4);
+            const uint64_t dal = dah + (uint64_t)((Cfg::NP * Cfg::PS) >> 4);
             const uint64_t dbs = db0 + (uint64_t)(s * (kStepBytes >> 4));
-            mma_bf16(d, dah, dbs, id64, s > 0 ? 1u : 0u);
-            mma_bf16(d, dah + lo_off, dbs, id32, 1u);
+            if constexpr (Cfg::SPLIT3) {
+              mma_bf16(d, dah, dbs, id32, s > 0 ? 1u : 0u);      // xh * wh
+              mma_bf16(d, dal, dbs, id32, 1u);                   // xl * wh
+              mma_bf16(d, dah, dbs + (1024 >> 4), id32, 1u);     // xh * wl (B rows 32-63)
+            } else {
+              mma_bf16(d, dah, dbs, id64, s > 0 ? 1u : 0u);      // [xh*wh | xh*wl]
+              mma_bf16(d, dal, dbs, id32, 1u);                   // + xl*wh
+            }
           }
         }
         mma_commit(&B.empty[b]);
         mma_commit(&B.acc_full[b]);
-        ++it;
       }
+      __syncwarp();
+      ++it;
     }
-    __syncwarp();
   } else {
-    // ================================================ epilogue (warps 0-3)
+    // ================================================ epilogue (warps 0-7)
+    // warp w reads TMEM lanes 32*(w%4).. of the tiles t = w/4, w/4 + 2, ...
+    const int q = warp & 3, h = warp >> 2;
+    const int gr = q * 4 + (lane >> 3), x = lane & 7;   // tile row / column of this lane
+    Cursor c = cursor_first(G, a, res);
     int it = 0;
-    const int gr = warp * 4 + (lane >> 3), x = lane & 7;   // tile row / column of this lane
-    for (int64_t w = blockIdx.x; w < G.total; w += gridDim.x) {
-      if (!super_live(a, res, G, w)) continue;
+    while (cursor_live(c, G, a, res)) {
+      const SuperTile t = super_tile<Cfg>(c, G, a, res);
       const int b = it & 1;
       const uint32_t use = (uint32_t)(it >> 1);
-      const SuperTile t = super_tile(a, res, G, w);
+      cursor_step(c, G, a, res);
       mbar_wait(&B.acc_full[b], use & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
-      for (int tt = 0; tt < kST; ++tt) {
-        if (t.ox0 + tt * kTW >= G.Wo) break;
+      for (int tt = h; tt < Cfg::ST; tt += 2) {
+        if (t.ox0 + tt * kTW >= G.Wo || (a.debug & 2)) break;
         const uint32_t taddr =
-            tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((b * kST + tt) * kAccCols);
-        float v0[32], v1[32];
-        tmem_ld32(taddr, v0);
-        tmem_ld32(taddr + 32, v1);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((b * Cfg::ST + tt) * Cfg::ACC);
+        float v[32];
+        tmem_ld32(taddr, v);
+        if constexpr (!Cfg::SPLIT3) {
+          float v1[32];
+          tmem_ld32(taddr + 32, v1);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          float y = fmaxf(__fadd_rn(__fadd_rn(v0[c], v1[c]), B.bias[c]), 0.0f);
-          y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 1));
-          y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 8));
-          v0[c] = y;
+          for (int ch = 0; ch < 32; ++ch) v[ch] = __fadd_rn(v[ch], v1[ch]);
+        } else {
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         }
-        const int oy = t.oy0 + gr, ox = t.ox0 + tt * kTW + x;
-        if ((lane & 9) == 0 && oy < G.Ho && ox < G.Wo) {
-          float4* dst = reinterpret_cast<float4*>(
-              t.fout + ((int64_t)(oy >> 1) * G.Wp + (ox >> 1)) * kCout);
+        // 2x2 max pool before bias + ReLU (both monotone, bias is per channel),
+        // as a halving butterfly: after the x-pair step a lane keeps 16
+        // channels, after the row-pair step 8, and all four lanes of a window
+        // store their 8 channels
+        const bool xodd = lane & 1, yodd = (lane >> 3) & 1;
+        float h16[16];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            dst[q] = make_float4(v0[4 * q], v0[4 * q + 1], v0[4 * q + 2], v0[4 * q + 3]);
+        for (int i = 0; i < 16; ++i) {
+          const float send = xodd ? v[i] : v[16 + i];
+          const float keep = xodd ? v[16 + i] : v[i];
+          h16[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 1));
+        }
+        float h8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float send = yodd ? h16[i] : h16[8 + i];
+          const float keep = yodd ? h16[8 + i] : h16[i];
+          h8[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+        }
+        const int c0 = (xodd ? 16 : 0) + (yodd ? 8 : 0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) h8[i] = fmaxf(__fadd_rn(h8[i], B.bias[c0 + i]), 0.0f);
+        const int oy = t.oy0 + (gr & ~1), ox = t.ox0 + tt * kTW + (x & ~1);
+        if (oy < G.Ho && ox < G.Wo) {
+          float4* dst = reinterpret_cast<float4*>(
+              t.fout + ((int64_t)(oy >> 1) * G.Wp + (ox >> 1)) * kCout + c0);
+          dst[0] = make_float4(h8[0], h8[1], h8[2], h8[3]);
+          dst[1] = make_float4(h8[4], h8[5], h8[6], h8[7]);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
@@ -407,6 +562,63 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res) {
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(kTmemCols));
+}
+
+using EncodeTiled = PFN_cuTensorMapEncodeTiled_v12000;
+
+int tensor_map_encoder(EncodeTiled* fn) {
+  static EncodeTiled enc = nullptr;
+  if (enc == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    PB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (p == nullptr || q != cudaDriverEntryPointSuccess)
+      return pb::fail(PB_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = reinterpret_cast<EncodeTiled>(p);
+  }
+  *fn = enc;
+  return PB_OK;
+}
+
+template <int MODE, int CIN>
+int launch_conv(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t st, int sms) {
+  using Cfg = ConvCfg<MODE, CIN>;
+  const size_t smem = 1024 + Cfg::SMEM + sizeof(ConvBars);
+  static_assert(1024 + Cfg::SMEM + sizeof(ConvBars) <= 227 * 1024, "conv smem");
+  static bool configured = false;
+  if (!configured) {
+    PB_CUDA(cudaFuncSetAttribute(conv_pool_kernel<MODE, CIN>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  const int Ho = actor.h + 2 * actor.pad - 4, Wo = actor.w + 2 * actor.pad - 4;
+  const int64_t per_frame = (int64_t)((Ho + kTH - 1) / kTH) * ((Wo + Cfg::ST * kTW - 1) / (Cfg::ST * kTW));
+  const int64_t total = per_frame * actor.frames * res.n_streams * res.n_iter;
+  if (total >= (int64_t)1 << 31) return pb::fail(PB_E_UNSUPPORTED, "conv: too many tiles per launch");
+  const int grid = (int)std::min<int64_t>(total, sms);
+  if (grid == 0) return PB_OK;
+  CUtensorMap tmap{};
+  if constexpr (MODE == 0) {
+    // the input ring as [frames][H][W*3] fp32; box = one super-tile's raw rows
+    const int64_t fbytes = (int64_t)actor.h * actor.w * CIN * 4;
+    if (actor.in.stream_stride % fbytes || actor.in.span_bytes % fbytes ||
+        (reinterpret_cast<uintptr_t>(actor.in.data) & 15))
+      return pb::fail(PB_E_UNSUPPORTED, "conv: input ring is not a whole number of frames");
+    EncodeTiled enc;
+    if (int rc = tensor_map_encoder(&enc)) return rc;
+    const cuuint64_t dims[3] = {(cuuint64_t)actor.w * CIN, (cuuint64_t)actor.h,
+                                (cuuint64_t)(actor.in.stream_stride / fbytes * res.n_streams)};
+    const cuuint64_t strides[2] = {(cuuint64_t)actor.w * CIN * 4, (cuuint64_t)fbytes};
+    const cuuint32_t box[3] = {(cuuint32_t)Cfg::RAW_W, (cuuint32_t)kPH, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, actor.in.data, dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return pb::fail(PB_E_CUDA, "conv: cuTensorMapEncodeTiled failed");
+  }
+  conv_pool_kernel<MODE, CIN><<<grid, kConvThreads, smem, st>>>(actor, res, tmap);
+  PB_LAUNCHED("conv_pool_kernel");
+  return PB_OK;
 }
 
 // ------------------------------------------------------------- dense (L3)
@@ -427,6 +639,10 @@ constexpr int kDStepBytes = 2 * kDN * 16 * 2;       // [wh; wl] 224 rows x 16 bf
 constexpr int kDChunkBytes = 4 * kDStepBytes;       // 28 KB
 constexpr int kDAPiece = 128 * kDKC * 2;            // 16 KB (one precision piece)
 constexpr int kDTmemCols = 256;
+constexpr int kDEpiWarps = 4, kDMmaWarp = 4;       // warps 0-3 epilogue, 4 MMA, 5-8 converters
+constexpr int kDEpiThreads = kDEpiWarps * 32;
+constexpr int kDCvtThreads = 128;
+constexpr int kDThreads = (kDEpiWarps + 1) * 32 + kDCvtThreads;
 
 struct DenseSmem {
   uint8_t a[kDStages][2][kDAPiece];        // K-major core layout [row/8][kb][row%8][16 B]
@@ -438,20 +654,7 @@ struct DenseSmem {
   float* outp[128];
 };
 
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__global__ void __launch_bounds__(kConvThreads, 1)
+__global__ void __launch_bounds__(kDThreads, 1)
 dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, int chunks_per_split) {
   extern __shared__ uint8_t smem_raw[];
   DenseSmem& S = *reinterpret_cast<DenseSmem*>(
@@ -490,7 +693,7 @@ dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, i
   }
   if (tid == 0) {
     for (int st = 0; st < kDStages; ++st) {
-      mbar_init(&S.full[st], kCvtThreads);
+      mbar_init(&S.full[st], kDCvtThreads);
       mbar_init(&S.empty[st], 1);
     }
     mbar_init(&S.acc_full, 1);
@@ -506,9 +709,9 @@ dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, i
 
   if (!any_row) {
     // nothing to do (tile beyond the live frames)
-  } else if (warp >= kMmaWarp + 1) {
+  } else if (warp >= kDMmaWarp + 1) {
     // ================================================ converters + weight copies
-    const int ct = tid - (kMmaWarp + 1) * 32;
+    const int ct = tid - (kDMmaWarp + 1) * 32;
     for (int c = c0, it = 0; c < c1; ++c, ++it) {
       const int st = it % kDStages;
       const uint32_t use = (uint32_t)(it / kDStages);
@@ -517,10 +720,10 @@ dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, i
         mbar_arrive_tx(&S.full[st], kDChunkBytes);
         bulk_g2s(S.b[st], wg + (int64_t)c * kDChunkBytes, kDChunkBytes, &S.full[st]);
       }
-      // 128 rows x 4 quarters of 16 K: 4 items per thread, 4 threads per row
+      // 128 rows x 4 quarters of 16 K, 4 threads per row
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int i = ct + k * kCvtThreads;
+      for (int k = 0; k < 512 / kDCvtThreads; ++k) {
+        const int i = ct + k * kDCvtThreads;
         const int r = i >> 2, q = i & 3;
         const float* rp = S.rowp[r];
         float v[16];
@@ -548,7 +751,7 @@ dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, i
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (ct != 0) mbar_arrive(&S.full[st]);
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == kDMmaWarp) {
     // ================================================ MMA issue
     if (lane == 0) {
       const uint32_t id224 = idesc_bf16(2 * kDN), id112 = idesc_bf16(kDN);
@@ -602,9 +805,9 @@ dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, i
       for (int o = 0; o < kDN; o += 4)
         *reinterpret_cast<float4*>(mine + o) = make_float4(y[o], y[o + 1], y[o + 2], y[o + 3]);
       __threadfence();
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
+      asm volatile("bar.sync 1, %0;" ::"n"(kDEpiThreads));
       if (r == 0) S.last = (atomicAdd(counters + mt, 1) == splits - 1);
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
+      asm volatile("bar.sync 1, %0;" ::"n"(kDEpiThreads));
       if (S.last) {
         __threadfence();
         if (op != nullptr) {
@@ -672,25 +875,19 @@ int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream) {
   const int Ho = actor.h + 2 * actor.pad - 4, Wo = actor.w + 2 * actor.pad - 4;
   if (Ho < 2 || Wo < 2 || Ho % 2 || Wo % 2)
     return pb::fail(PB_E_UNSUPPORTED, "conv: output must be even-sized for the 2x2 pool");
-  if (actor.cin != 3 && actor.cin % 16 != 0)
-    return pb::fail(PB_E_UNSUPPORTED, "conv: Cin must be 3 or a multiple of 16");
-  const ConvGeom G = conv_geom(actor, res.n_streams, res.n_iter);
-  const size_t smem = conv_smem_bytes(G) + sizeof(ConvBars);
-  if (G.steps > kMaxSteps || smem > 227 * 1024)
-    return pb::fail(PB_E_UNSUPPORTED, "conv: weights + patches exceed shared memory");
   static int sms = 0;
   if (sms == 0) {
-    PB_CUDA(cudaFuncSetAttribute(conv_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 227 * 1024));
     int dev = 0;
     PB_CUDA(cudaGetDevice(&dev));
     PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  const int grid = (int)std::min<int64_t>(G.total, sms);
-  if (grid == 0) return PB_OK;
-  conv_pool_kernel<<<grid, kConvThreads, smem, pb::as_stream(stream)>>>(actor, res);
-  PB_LAUNCHED("conv_pool_kernel");
-  return PB_OK;
+  cudaStream_t st = pb::as_stream(stream);
+  switch (actor.cin) {
+    case 3: return launch_conv<0, 3>(actor, res, st, sms);
+    case 16: return launch_conv<1, 16>(actor, res, st, sms);
+    case 32: return launch_conv<1, 32>(actor, res, st, sms);
+    default: return pb::fail(PB_E_UNSUPPORTED, "conv: Cin must be 3, 16 or 32");
+  }
 }
 
 int pb_fire_dense(pb_dense_actor actor, pb_resolved res, void* stream) {
@@ -731,7 +928,7 @@ int pb_fire_dense(pb_dense_actor actor, pb_resolved res, void* stream) {
     }
   }
   dim3 grid(m_tiles, splits);
-  dense_kernel<<<grid, kConvThreads, sizeof(DenseSmem) + 1024, st>>>(actor, res, partial, counters,
+  dense_kernel<<<grid, kDThreads, sizeof(DenseSmem) + 1024, st>>>(actor, res, partial, counters,
                                                                       cps);
   PB_LAUNCHED("dense_kernel");
   return PB_OK;

@@ -15,7 +15,7 @@ from paper_1802_06625_b200.apps import vision
 from paper_1802_06625_b200.engine import DeviceRuntime
 
 
-def measure(S=4, firings=64, R=24, steps=20):
+def measure(S=4, firings=64, R=24, steps=20, debug=0):
     desc = vision.build_description(R, policy="fixed_policy")
     rt = DeviceRuntime(desc, config=RuntimeConfig(source_firings=firings, epoch=firings),
                        n_streams=S, seeds=list(range(S)), sources={"src": [None] * S})
@@ -23,6 +23,9 @@ def measure(S=4, firings=64, R=24, steps=20):
     for s in range(S):
         st[s] = vision.make_frames(s, firings * R).reshape(firings, -1).view(np.uint8)
     lib = rt.lib
+    for item in rt.launches:   # profiling only: skip conv roles (pb_conv_actor.debug)
+        if item[0] == "conv":
+            item[1].debug = debug
     rt.reset()
     rt.stage_sources(0, firings, prestaged=True)
     rt.stage_control(0, firings)

@@ -173,6 +173,59 @@ static void run_tput2() {
   cudaFree(cyc);
 }
 
+
+// 1c. A-operand layout cost: bf16, M=128, N given; A start offset / LBO / SBO
+// varied (the conv patch uses unaligned starts, LBO = plane stride, SBO = row).
+template <int N>
+__global__ void tput3(int iters, uint32_t aoff, uint32_t lbo, uint32_t sbo, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.f;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  setup(&tslot, &bar, 256);
+  const uint32_t tmem = tslot;
+  if (threadIdx.x < 32) {
+    uint32_t phase = 0;
+    const uint32_t a = smem_u32(sm) + aoff, b = smem_u32(sm + 128 * 1024);
+    const uint32_t id = idesc(1, 128, N);
+    const uint64_t da = sdesc(a, lbo, sbo), db = sdesc(b, 128, 256);
+    long long t0 = clock64();
+    for (int i = 0; i < iters; i += 16) {
+      uint32_t e;
+      asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(e));
+      if (e) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;" ::"r"(tmem), "l"(da + (u & 3) * 8), "l"(db), "r"(id));
+        if (((i / 16) & 7) == 7) commit_wait(&bar, phase);
+      }
+      __syncwarp();
+    }
+    uint32_t e;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(e));
+    if (e) commit_wait(&bar, phase);
+    __syncwarp();
+    long long t1 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = t1 - t0;
+  }
+  teardown(tmem, 256);
+}
+
+template <int N>
+static void run_tput3(const char* name, uint32_t aoff, uint32_t lbo, uint32_t sbo) {
+  long long* cyc;
+  CK(cudaMalloc(&cyc, 8));
+  CK(cudaFuncSetAttribute(tput3<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  const int iters = 16384;
+  tput3<N><<<148, 128, 160 * 1024>>>(iters, aoff, lbo, sbo, cyc);
+  CK(cudaDeviceSynchronize());
+  long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("{\"probe\": \"layout\", \"case\": \"%s\", \"N\": %d, \"aoff\": %u, \"lbo\": %u, \"sbo\": %u, \"cyc_per_mma\": %.2f}\n",
+         name, N, aoff, lbo, sbo, (double)c / iters);
+  cudaFree(cyc);
+}
+
 // ------------------------------------------------- 2. shifted-window layouts
 // mode 0 (planar, tf32): P[cb][pix][4 f32], npix pixels, 8 planes (32 ch);
 //   D[r][o] = sum_shift sum_ci P[ci][shift + r] * W[shift][o][ci]
@@ -348,8 +401,27 @@ int main() {
       printf("{\"probe\": \"tput\", \"kind\": \"%s\", \"N\": %d, \"cyc_per_mma\": %.2f, \"tflops\": %.1f}\n",
              kind == 0 ? "tf32" : "bf16", n, (double)c / iters, flops / (ms * 1e-3) / 1e12);
     }
+  const char* only = getenv("PROBE_ONLY");
+  if (!only || strcmp(only, "layout")) {
   run_tput2<0, 32>(); run_tput2<0, 64>(); run_tput2<0, 128>(); run_tput2<0, 256>();
   run_tput2<1, 32>(); run_tput2<1, 64>(); run_tput2<1, 128>(); run_tput2<1, 256>();
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    // dense core layout (aligned), then misaligned starts, then the conv's planar layout
+    if (pass == 0) {
+      run_tput3<32>("dense", 0, 128, 1024); run_tput3<64>("dense", 0, 128, 1024);
+      run_tput3<32>("dense+16", 16, 128, 1024); run_tput3<64>("dense+16", 16, 128, 1024);
+      run_tput3<32>("dense+64", 64, 128, 1024); run_tput3<64>("dense+64", 64, 128, 1024);
+    } else {
+      run_tput3<32>("planar", 0, 6400, 320); run_tput3<64>("planar", 0, 6400, 320);
+      run_tput3<32>("planar+16", 16, 6400, 320); run_tput3<64>("planar+16", 16, 6400, 320);
+      run_tput3<32>("planar_sbo256", 0, 6400, 256); run_tput3<64>("planar_sbo256", 0, 6400, 256);
+      run_tput3<32>("planar_sbo384", 0, 6400, 384); run_tput3<64>("planar_sbo384", 0, 6400, 384);
+      run_tput3<32>("planar+16_sbo256", 16, 6400, 256); run_tput3<64>("planar+16_sbo256", 16, 6400, 256);
+      run_tput3<32>("toeplitz", 0, 16, 128); run_tput3<64>("toeplitz", 0, 16, 128);
+    }
+  }
+  if (only && !strcmp(only, "layout")) return 0;
   for (int mode = 0; mode < 3; ++mode) run_window(mode);
   return 0;
 }
