@@ -29,7 +29,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "DPD Msamples/s (stream input samples, whole job)"
+METRIC = "DPD Msamples/s & CNN frames/s per B200 (1\u20138 GPUs), % of HBM/tensor roofline"
 UNIT = "Msamples/s"
 
 
@@ -48,6 +48,12 @@ def parse():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-streams", type=int, default=64)
     ap.add_argument("--cpu-blocks", type=int, default=32)
+    ap.add_argument("--skip-cnn", action="store_true")
+    ap.add_argument("--cnn-streams", type=int, default=4, help="CNN streams per GPU")
+    ap.add_argument("--cnn-firings", type=int, default=64, help="24-frame firings per stream")
+    ap.add_argument("--cnn-steps", type=int, default=20)
+    ap.add_argument("--cnn-e2e-steps", type=int, default=2)
+    ap.add_argument("--cnn-cpu-frames", type=int, default=24)
     return ap.parse_args()
 
 
@@ -197,6 +203,153 @@ def run_reference(args, rank, world):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ CNN leg
+
+CNN_FRAMES_PER_FIRING = 24   # PAPER.md:680 (atr = 24 frames per token)
+
+
+def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
+    """BASELINE config 3: the vision graph (apps/vision.py) with every firing
+    processed (fixed_policy element 1: the worst case of the adaptive graph),
+    S streams x F firings x 24 frames of 96x96x3 fp32 per GPU and step.
+    value: device-resident frames/s (inputs already in the source rings);
+    e2e: DeviceRuntime.run_all from pinned host frames, logits D2H + SHA-256.
+    roofline: useful conv FLOPs (L1 + L2) over the conv kernels'
+    event-timed share, against the measured sustained bf16 peak."""
+    import ctypes as C
+
+    from paper_1802_06625_b200 import RuntimeConfig, _lib
+    from paper_1802_06625_b200.apps import vision
+    from paper_1802_06625_b200.engine import DeviceRuntime
+
+    S, F, R = args.cnn_streams, args.cnn_firings, CNN_FRAMES_PER_FIRING
+    desc = vision.build_description(R, policy="fixed_policy")
+    rt = DeviceRuntime(desc, config=RuntimeConfig(source_firings=F, epoch=F, device=local,
+                                                  capture_sinks=True),
+                       n_streams=S, seeds=[rank * S + s for s in range(S)],
+                       sources={"src": [None] * S})
+    stage = rt.source_staging("src")
+    for s in range(S):
+        stage[s] = vision.make_frames(rank * S + s, F * R).reshape(F, -1).view(np.uint8)
+    lib = rt.lib
+
+    def ev():
+        e = C.c_void_p()
+        _lib.check(lib.pb_event_create(C.byref(e)))
+        return e.value
+
+    rt.reset()
+    rt.stage_sources(0, F, prestaged=True)
+    rt.stage_control(0, F)
+    for _ in range(max(3, args.warmup)):
+        rt.fire_epoch(0, F)
+    _lib.check(lib.pb_stream_sync(rt.stream))
+    marks = {}
+    seen = {"conv": 0}
+
+    def hook(kind, phase):
+        e = ev()
+        lib.pb_event_record(e, rt.stream)
+        if kind == "conv" and phase == "pre":
+            seen["conv"] += 1
+        key = kind if kind != "conv" else f"conv_l{(seen['conv'] - 1) % 2 + 1}"
+        marks.setdefault(key, []).append(e)
+
+    barrier()
+    n0 = lib.pb_launch_count()
+    e0, e1 = ev(), ev()
+    lib.pb_event_record(e0, rt.stream)
+    for _ in range(args.cnn_steps):
+        rt.fire_epoch(0, F, hook=hook)
+    lib.pb_event_record(e1, rt.stream)
+    _lib.check(lib.pb_stream_sync(rt.stream))
+    launches = lib.pb_launch_count() - n0
+    ms = C.c_float()
+    _lib.check(lib.pb_event_elapsed_ms(e0, e1, C.byref(ms)))
+    step_ms = max_over_ranks(ms.value / args.cnn_steps)
+    kern = {}
+    for k, evs in marks.items():
+        ts = []
+        for i in range(0, len(evs) - 1, 2):
+            lib.pb_event_elapsed_ms(evs[i], evs[i + 1], C.byref(ms))
+            ts.append(ms.value)
+        kern[k] = statistics.mean(ts)
+    frames = S * F * R
+    value = frames * world / (step_ms / 1e3)
+
+    # end to end: pinned host frames -> logits on the host (+ digests)
+    e2e_t = []
+    for k in range(args.cnn_e2e_steps + 1 if args.cnn_e2e_steps > 0 else 0):
+        barrier()
+        t0 = time.perf_counter()
+        reps = rt.run_all(prestaged=True)
+        t1 = time.perf_counter()
+        if k:
+            e2e_t.append(max_over_ranks(t1 - t0))
+    e2e_s = statistics.median(e2e_t) if e2e_t else float("nan")
+    parity = None
+    if rank == 0 and e2e_t:
+        from oracle import cnn as oc
+        p = oc.graph_params(desc)
+        logits = np.frombuffer(reps[0].sink_data["sink"], np.float32) \
+            if reps[0].sink_data else None
+        if logits is not None:
+            want = oc.forward(vision.make_frames(0, R), p)["logits"]
+            got = logits[:R * vision.N_CLASSES].reshape(R, -1)
+            parity = {"max_abs_logit_err": float(np.abs(got - want).max()),
+                      "top1_equal": bool((got.argmax(-1) == want.argmax(-1)).all()),
+                      "checked": "stream 0, first firing vs oracle/cnn.py (tolerance 1e-3)"}
+    rt.close()
+
+    conv_flops = vision.flops_per_frame() - 18432 * 100 * 2
+    conv_ms = kern.get("conv_l1", 0.0) + kern.get("conv_l2", 0.0)
+    achieved = frames * conv_flops / (conv_ms / 1e3) / 1e12 if conv_ms else None
+    peak = float(peaks.get("bf16_tflops_sustained", 0) or 0)
+    peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained (measured)" if peak else \
+        "B200_PROFILING.md fallback 1.4 PFLOP/s sustained"
+    peak = peak or 1400.0
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu and args.cnn_cpu_frames > 0:
+        from oracle import cnn as oc
+        p = oc.graph_params(desc)
+        x = vision.make_frames(0, args.cnn_cpu_frames)
+        oc.forward(x[:1], p)
+        t0 = time.perf_counter()
+        oc.forward(x, p)
+        t = time.perf_counter() - t0
+        cpu = {"value": args.cnn_cpu_frames / t, "unit": "frames/s", "cores": os.cpu_count(),
+               "kind": "port",
+               "sample": f"{args.cnn_cpu_frames} frames through oracle/cnn.forward (the builder "
+                         "oracle; the reference ships no DNN): numpy float64 im2col GEMMs, BLAS "
+                         "threads = host cores"}
+    return {
+        "metric": "CNN frames/s (vision graph, every firing processed, whole job)",
+        "value": value, "unit": "frames/s", "ms_per_step": step_ms, "steps": args.cnn_steps,
+        "dtype": "f32 tokens; bf16x3 split operands on tcgen05, fp32 accumulate",
+        "config": {"workload": f"C3 CNN: {S} streams/GPU x {F} firings x {R} frames of "
+                               f"96x96x3 fp32 (conv5x5 3->32 + pool, conv5x5 32->32 + pool, "
+                               f"dense 18432->100, classifier), fixed_policy element 1",
+                   "frames_per_gpu_step": frames,
+                   "l2": f"inputs {frames * vision.FRAME_BYTES / 1e6:.0f} MB/GPU > L2; no flush"},
+        "kernel_ms": kern,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "kernel": "conv_pool_kernel (layers 1+2)", "kernel_ms": conv_ms,
+                     "algorithmic_flops_per_frame": conv_flops, "peak_source": peak_src,
+                     "note": "useful FLOPs; bf16x3 issues 3 MMA products per useful one, "
+                             "layer 2 at N=32/64 is shared-memory-read bound (tools/conv_probe)"},
+        "e2e": {"value": frames * world / e2e_s, "unit": "frames/s",
+                "h2d_bytes_per_step": frames * vision.FRAME_BYTES,
+                "d2h_bytes_per_step": frames * vision.N_CLASSES * 4,
+                "seconds_per_step": e2e_s,
+                "includes": "H2D pinned frames, native control actor, device firings, "
+                            "logits D2H, SHA-256 per stream"},
+        "gpu_launches": launches,
+        "parity_stream0": parity,
+        "cpu_baseline": cpu,
+    }
 
 
 # ------------------------------------------------------------------ our arm
@@ -396,6 +549,12 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {e!r}"}
 
+    cnn = None
+    if not args.skip_cnn:
+        rt.close()
+        rt = None
+        cnn = cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -427,9 +586,11 @@ def main():
             "tolerance_mode": tol,
             "parity_stream0": parity,
             "cpu_baseline": cpu,
+            "cnn": cnn,
         }
         print(json.dumps(line), flush=True)
-    rt.close()
+    if rt is not None:
+        rt.close()
     if dist is not None:
         dist.destroy_process_group()
 
