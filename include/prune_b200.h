@@ -225,6 +225,7 @@ typedef struct {
 #define PB_FIR_EXACT 0
 #define PB_FIR_EXACT_PAIRED 1
 #define PB_FIR_FMA 2
+#define PB_FIR_MERGED 3   /* bank only: one FMA FIR with the active branches' taps summed */
 
 /* All firings of n_actors fir_branch actors in one launch.  actors is a
  * DEVICE array. */

@@ -13,7 +13,10 @@ from pathlib import Path
 from .errors import (ActorPanic, DeviceUnavailable, EndOfStream, InvalidParams, Poisoned,
                      ProtocolError)
 
-LIB_PATH = Path(__file__).resolve().parent / "libprune_b200.so"
+# PB_LIB_PATH selects an alternative build of the same library (profiling
+# experiments with different compile-time tunings); default: the in-tree build
+LIB_PATH = Path(os.environ.get("PB_LIB_PATH") or
+                Path(__file__).resolve().parent / "libprune_b200.so")
 
 PB_OK = 0
 PB_E_INVALID = -1
@@ -29,6 +32,7 @@ PB_TAPS = 10
 PB_FIR_EXACT = 0
 PB_FIR_EXACT_PAIRED = 1
 PB_FIR_FMA = 2
+PB_FIR_MERGED = 3
 PB_MAX_BRANCHES = 32
 PB_MAX_PORTS = 16
 PB_POLICY_STATE_BYTES = 2560

@@ -45,7 +45,6 @@
 namespace {
 
 constexpr int kTW = 8, kTH = 16;            // conv pixels per MMA tile (M = 128)
-constexpr int kMaxST = 4;                   // tiles per super-tile (side by side): mode 0 4, mode 1 2
 constexpr int kPH = kTH + 4;                // patch rows
 constexpr int kEpiWarps = 8, kCvtWarps = 7;   // 16 warps: 4 per SM sub-partition, 128 regs
 constexpr int kMmaWarp = kEpiWarps;

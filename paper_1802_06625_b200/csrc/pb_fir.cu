@@ -36,14 +36,23 @@ typedef unsigned long long u64;
 
 constexpr int kTaps = PB_TAPS;
 constexpr int kHist = PB_TAPS - 1;
-constexpr int kConsumerWarps = 4;
+#ifndef PB_FIR_CWARPS
+#define PB_FIR_CWARPS 4
+#endif
+#ifndef PB_FIR_PER_THREAD
+#define PB_FIR_PER_THREAD 8
+#endif
+constexpr int kConsumerWarps = PB_FIR_CWARPS;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kThreads = kConsumers + 32;        // + producer warp
-constexpr int kPerThread = 8;                    // consecutive outputs per thread
+constexpr int kPerThread = PB_FIR_PER_THREAD;    // consecutive outputs per thread
 constexpr int kTile = kConsumers * kPerThread;   // outputs per work item
 constexpr int kPad = 12;                         // halo slots in front of the tile (>= 9, x4)
 constexpr int kWin = kPerThread + kPad;          // per-thread window (20 samples)
-constexpr int kStages = 4;
+#ifndef PB_FIR_STAGES
+#define PB_FIR_STAGES 4
+#endif
+constexpr int kStages = PB_FIR_STAGES;
 constexpr int kMaxBr = PB_MAX_BRANCHES;
 constexpr int kChunkSpans = 4;               // spans per dynamic work grab
 
@@ -60,11 +69,17 @@ struct __align__(16) Desc {
   int first;      // tile 0: window entries before the span come from hist
   int8_t br[kMaxBr];
   float hist[kMaxBr][2][kHist];
+  // PB_FIR_MERGED (bank): the active branches' taps summed per tap
+  // ({cr, ci, ci, cr}), and for the span's first kHist outputs the
+  // contribution of each branch's own history (pre-span samples)
+  float4 mtaps[kTaps];
+  float corr[kHist][2];
 };
 
 struct __align__(16) Smem {
   StageBuf buf[kStages];
   Desc desc[kStages];
+  float pf_hist[2][kMaxBr][2][kHist];   // bank: next span's branch histories (cp.async)
   float4 taps[kMaxBr][kTaps];   // {cr, ci, ci, cr}
   u64 full[kStages];
   u64 empty[kStages];
@@ -90,17 +105,30 @@ __device__ __forceinline__ void mbar_arrive_tx(u64* bar, uint32_t bytes) {
       "r"(bytes)
       : "memory");
 }
-// try_wait with a suspend-time hint: the warp sleeps in hardware until the
-// phase completes (or the hint elapses) instead of spinning on issue slots
-// the FP32 consumers need.
+// try_wait: kSuspendHint > 0 passes a suspend-time hint (the warp may sleep
+// in hardware until the phase completes instead of spinning on issue slots
+// the FP32 consumers need); PB_FIR_SUSPEND_NS at build time overrides it.
+#ifndef PB_FIR_SUSPEND_NS
+#define PB_FIR_SUSPEND_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(u64* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(1000000u)
-      : "memory");
+  if (PB_FIR_SUSPEND_NS > 0) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"((uint32_t)PB_FIR_SUSPEND_NS)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, u64* bar) {
   asm volatile(
@@ -127,6 +155,20 @@ __device__ __forceinline__ u64 fadd2(u64 a, u64 b) {
   u64 r;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
+}
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
+// span_ptr with the stream's ring base already loaded (pb_common.cuh)
+__device__ __forceinline__ const uint8_t* span_ptr_b(const pb_span_ref& r, int64_t base,
+                                                     const pb_resolved& res, int s, int n) {
+  int64_t idx = n;
+  if (r.index_cond >= 0)
+    idx = res.prefix[((int64_t)r.index_cond * res.n_streams + s) * res.cap + n];
+  return r.data + (int64_t)s * r.stream_stride + ((base + idx) % r.slots) * r.span_bytes;
 }
 
 // ------------------------------------------------------------- FIR math
@@ -226,6 +268,12 @@ __device__ __forceinline__ void store8(float* out, int64_t B, int n0, const u64 
 //                region; output = sum over active branches (combiner order)
 // kBank = false: items (actor, s, j, tile) of per-actor batched firings;
 //                output = the actor's own output span
+// PB_FIR_MERGED (bank launches only): every active branch sees the same
+// input inside a span, so sum_k FIR_k(x) = FIR_{sum_k c_k}(x) there; the
+// consumers run ONE fused-multiply-add FIR per output with the producer's
+// merged taps, and the first kHist outputs add the producer's correction for
+// the pre-span samples, which differ per branch (each branch's own history).
+// Reassociated sums: within ~1e-7 of the exact path (tolerance 1e-5).
 template <bool kBank, int kMath>
 __global__ void __launch_bounds__(kThreads, 4)
 fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actors, int n_actors,
@@ -262,7 +310,9 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
     // Bank launches with a scheduler pointer grab chunks of kChunkSpans spans
     // dynamically (the active-branch count per span varies 1..K, so static
     // ranges leave a tail); otherwise each CTA takes one contiguous range.
-    const bool dynamic = kBank && bank.sched != nullptr;
+    // (MERGED work per span is constant: static ranges balance, and keep the
+    // per-branch history source in registers across the CTA's spans)
+    const bool dynamic = kBank && bank.sched != nullptr && kMath != PB_FIR_MERGED;
     const int64_t chunk = dynamic ? (int64_t)kChunkSpans * tiles : 0;
     int64_t w0 = total * blockIdx.x / gridDim.x;
     int64_t w1 = total * (blockIdx.x + 1) / gridDim.x;
@@ -273,6 +323,17 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
     bool have = false;
     unsigned mask = 0;
     int prev_n = -2;   // lane b: iteration branch b last fired at (-1: none yet, -2: unknown)
+    float4 mtap = make_float4(0.f, 0.f, 0.f, 0.f);   // MERGED: lane t's merged tap
+    int64_t in_base = 0, out_base = 0;               // ring bases of the current stream
+    const float* span_in = nullptr;                  // current span's input / output
+    u64 span_out = 0;
+    // bank: the next span's activity and each branch's history candidate are
+    // loaded one span ahead (registers / cp.async into pf_hist), so resolving
+    // a span costs no dependent global-load round trips
+    int64_t pf_unit = -1;
+    int pf_n = -1;
+    bool pf_have = false, pf_act = false, pf_ok = false, cur_pf_ok = false;
+    constexpr bool kMerged = kBank && kMath == PB_FIR_MERGED;
     for (;;) {
     if (dynamic) {
       int64_t c = 0;
@@ -283,42 +344,113 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
       w1 = min(total, w0 + chunk);
       cur_unit = -1;   // chunks are not contiguous with the previous one
     }
-    for (int64_t w = w0; w < w1; ++w) {
-      int64_t r = w;
-      int a = 0;
+    // decode w0 once, then step (a, s, it, tile) incrementally
+    int a = 0, s = 0, it = 0, tile = 0;
+    {
+      int64_t r = w0;
       if (!kBank) {
         a = (int)(r / ((int64_t)res.n_streams * per_unit));
         r %= (int64_t)res.n_streams * per_unit;
       }
-      const int s = (int)(r / per_unit);
+      s = (int)(r / per_unit);
       r %= per_unit;
-      const int it = (int)(r / tiles);
-      const int tile = (int)(r % tiles);
+      it = (int)(r / tiles);
+      tile = (int)(r % tiles);
+    }
+    for (int64_t w = w0; w < w1; ++w) {
+      if (w > w0 && ++tile == tiles) {
+        tile = 0;
+        if (++it == res.n_iter) {
+          it = 0;
+          if (++s == res.n_streams) {
+            s = 0;
+            ++a;
+          }
+        }
+      }
       const int64_t unit = (int64_t)a * res.n_streams + s;
       if (unit != cur_unit || it != cur_it) {
         // ---- new span: resolve its firing
-        if (unit != cur_unit) prev_n = -2;
+        if (unit != cur_unit) {
+          prev_n = -2;
+          const pb_span_ref& ir = kBank ? bank.in : actors[a].in;
+          const pb_span_ref& orf = kBank ? bank.out : actors[a].out;
+          in_base = ir.base ? ir.base[s] : 0;
+          out_base = orf.base ? orf.base[s] : 0;
+        }
         cur_unit = unit;
         cur_it = it;
         bool act = false;
         if (kBank) {
           n = it;
-          have = pb::active(res, bank.actor_cond, s, n);
-          if (have && lane < nb) act = pb::active(res, br[lane].cond, s, n);
+          const bool use_pf = unit == pf_unit && it == pf_n;
+          if (use_pf) {
+            have = pf_have;
+            act = have && pf_act;
+          } else {
+            have = pb::active(res, bank.actor_cond, s, n);
+            if (have && lane < nb) act = pb::active(res, br[lane].cond, s, n);
+          }
+          cur_pf_ok = use_pf && pf_ok;
+          // prefetch span n + 1 of this stream
+          if (it + 1 < res.n_iter) {
+            pf_unit = unit;
+            pf_n = it + 1;
+            pf_have = pb::active(res, bank.actor_cond, s, it + 1);
+            pf_act = lane < nb && pb::active(res, br[lane].cond, s, it + 1);
+            const int src = act ? n : prev_n;   // branch's latest firing before n + 1
+            pf_ok = lane < nb && src != -2;
+            if (pf_ok) {
+              const float* hr;
+              const float* hi;
+              if (src < 0) {
+                hr = br[lane].state + (int64_t)s * 2 * kHist;
+                hi = hr + kHist;
+              } else {   // every branch fired on the bank's own input span
+                const float* prev = reinterpret_cast<const float*>(
+                    span_ptr_b(bank.in, in_base, res, s, src));
+                hr = prev + B - kHist;
+                hi = prev + 2 * B - kHist;
+              }
+              float* dst = sm.pf_hist[(it + 1) & 1][lane][0];
+#pragma unroll
+              for (int q = 0; q < kHist; ++q) {
+                cp_async4(dst + q, hr + q);
+                cp_async4(dst + kHist + q, hi + q);
+              }
+            }
+          }
+          // one group per span, possibly empty: "wait_group 1" at the next
+          // span's first tile then covers exactly the groups issued before it
+          asm volatile("cp.async.commit_group;" ::: "memory");
         } else {
           have = it < pb::cond_count(res, actors[a].cond, s);
           n = have ? pb::firing_iter(res, actors[a].cond, s, it) : 0;
           act = have && lane == 0;
         }
         mask = __ballot_sync(0xffffffffu, act);
+        if (have) {   // the span's input / output, once per span
+          span_in = reinterpret_cast<const float*>(
+              span_ptr_b(kBank ? bank.in : actors[a].in, in_base, res, s, n));
+          span_out = reinterpret_cast<u64>(
+              span_ptr_b(kBank ? bank.out : actors[a].out, out_base, res, s, n));
+        }
+        if (kMerged && have && lane < kTaps) {
+          float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int b = 0; b < nb; ++b)
+            if ((mask >> b) & 1u) {
+              const float4 c = sm.taps[b][lane];
+              m.x += c.x; m.y += c.y; m.z += c.z; m.w += c.w;
+            }
+          mtap = m;
+        }
       }
       if (!have) continue;
       const int stage = k % kStages;
       mbar_wait(&sm.empty[stage], ((k / kStages) & 1) ^ 1);
       Desc& d = sm.desc[stage];
       StageBuf& sb = sm.buf[stage];
-      const pb_span_ref& in_ref = kBank ? bank.in : actors[a].in;
-      const float* in = reinterpret_cast<const float*>(pb::span_ptr(in_ref, res, s, n));
+      const float* in = span_in;
       const int t0 = tile * kTile;
       const int64_t rem = B - t0;
       const int len = (int)(rem < kTile ? rem : kTile);
@@ -333,7 +465,16 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
       if (act) {
         const int rank = __popc(mask & ((1u << lane) - 1u));
         d.br[rank] = (int8_t)(kBank ? lane : a);
-        if (t0 == 0) {
+        if (kBank && t0 == 0 && cur_pf_ok) {
+          // prefetched one span ago (this lane's own cp.async groups)
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+          const float* ph = sm.pf_hist[it & 1][lane][0];
+#pragma unroll
+          for (int q = 0; q < kHist; ++q) {
+            d.hist[rank][0][q] = ph[q];
+            d.hist[rank][1][q] = ph[kHist + q];
+          }
+        } else if (t0 == 0) {
           const pb_fir_actor& fa = br[kBank ? lane : a];
           int src = prev_n;  // iteration of the branch's previous firing
           if (src == -2) {
@@ -364,10 +505,31 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
           }
         }
       }
+      if (kMerged) {
+        if (lane < kTaps) d.mtaps[lane] = mtap;
+        if (t0 == 0) {
+          __syncwarp();   // d.br / d.hist of the active lanes are written
+          if (lane < kHist) {
+            // output `lane` reads pre-span sample lane - t (< 0) for taps t > lane
+            float cr = 0.f, ci = 0.f;
+            const int na = __popc(mask);
+            for (int r = 0; r < na; ++r) {
+              const float4* tp = sm.taps[d.br[r]];
+              for (int t = lane + 1; t < kTaps; ++t) {
+                const int q = lane - t + kHist;
+                const float hr = d.hist[r][0][q], hi = d.hist[r][1][q];
+                const float4 c = tp[t];
+                cr = __fmaf_rn(-c.y, hi, __fmaf_rn(c.x, hr, cr));
+                ci = __fmaf_rn(c.y, hr, __fmaf_rn(c.x, hi, ci));
+              }
+            }
+            d.corr[lane][0] = cr;
+            d.corr[lane][1] = ci;
+          }
+        }
+      }
       if (lane == 0) {
-        const pb_span_ref& out_ref = kBank ? bank.out : actors[a].out;
-        float* out = reinterpret_cast<float*>(pb::span_ptr(out_ref, res, s, n));
-        d.out = reinterpret_cast<u64>(out);
+        d.out = span_out;
         d.valid = 1;
         d.t0 = t0;
         d.n_act = __popc(mask);
@@ -420,6 +582,30 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
       float wr[kWin], wi[kWin];
       load_window(sm.buf[stage], ct, wr, wi);
       const bool patch = d.first && ct * kPerThread < kPad;
+      if constexpr (kBank && kMath == PB_FIR_MERGED) {
+        if (patch) {   // pre-span samples: zero here, per-branch history in d.corr
+#pragma unroll
+          for (int i = 0; i < kPad; ++i)
+            if (kPerThread * ct - kPad + i < 0) wr[i] = wi[i] = 0.0f;
+        }
+        u64 y[kPerThread];
+        fir8_fma(wr, wi, d.mtaps, y);
+        if (patch) {
+#pragma unroll
+          for (int v = 0; v < kPerThread; ++v) {
+            const int m = kPerThread * ct + v;
+            if (m < kHist) {
+              float yr, yi;
+              unpack2(y[v], yr, yi);
+              y[v] = pack2(yr + d.corr[m][0], yi + d.corr[m][1]);
+            }
+          }
+        }
+        store8(out, B, n0, y);
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.empty[stage]);
+        continue;
+      }
       u64 acc[kPerThread];
 #pragma unroll
       for (int v = 0; v < kPerThread; ++v) acc[v] = pack2(0.0f, 0.0f);
@@ -465,6 +651,186 @@ __global__ void fir_carry_kernel(const pb_fir_actor* __restrict__ actors, pb_res
   const float* in = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, nl));
   const int plane = threadIdx.x / kHist, k = threadIdx.x % kHist;
   a.state[(int64_t)s * 2 * kHist + plane * kHist + k] = in[plane * B + B - kHist + k];
+}
+
+
+// ------------------------------------------------- PB_FIR_MERGED filter bank
+// Tolerance mode of the fused bank as two plain data-parallel kernels: the
+// bank is then an HBM-bound stencil (8 B read + 8 B written per sample, one
+// 10-tap complex FMA FIR), with no producer warp on the critical path.
+//   bank_plan_kernel: one warp per span (s, n): the active branches' taps
+//     summed per tap, and the correction of outputs 0..8 for the pre-span
+//     samples (each branch's own 9-sample history).
+//   bank_merged_kernel: 8 consecutive outputs per thread, window straight
+//     from global memory (neighbouring threads share it through L1).
+struct __align__(16) BankPlan {
+  float4 taps[kTaps];   // merged {cr, ci, ci, cr}
+  float2 corr[kHist];   // added to outputs 0..8
+  int have;             // the bank fires at (s, n)
+  int pad_[3];
+};
+
+constexpr int kPlanWarps = 4;   // spans per block (one warp each)
+
+__global__ void __launch_bounds__(32 * kPlanWarps)
+bank_plan_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan) {
+  const int n = blockIdx.x * kPlanWarps + threadIdx.y, s = blockIdx.y, lane = threadIdx.x;
+  if (n >= res.n_iter) return;
+  BankPlan& p = plan[(int64_t)s * res.n_iter + n];
+  if (!pb::active(res, bank.actor_cond, s, n)) {
+    if (lane == 0) p.have = 0;
+    return;
+  }
+  const pb_fir_actor* br = bank.branches;
+  const int nb = bank.n_branches;
+  __shared__ float4 taps_all[kPlanWarps][kMaxBr][kTaps];
+  __shared__ float hist_all[kPlanWarps][kMaxBr][2][kHist];
+  float4 (*taps)[kTaps] = taps_all[threadIdx.y];
+  float (*hist)[2][kHist] = hist_all[threadIdx.y];
+  for (int e = lane; e < nb * kTaps; e += 32) {
+    const int b = e / kTaps, t = e % kTaps;
+    const float cr = br[b].taps[t], ci = br[b].taps[kTaps + t];
+    taps[b][t] = make_float4(cr, ci, ci, cr);
+  }
+  const bool act = lane < nb && pb::active(res, br[lane].cond, s, n);
+  const unsigned mask = __ballot_sync(0xffffffffu, act);
+  if (act) {
+    const pb_fir_actor& fa = br[lane];
+    const int j = fa.cond < 0 ? n : res.prefix[((int64_t)fa.cond * res.n_streams + s) * res.cap + n];
+    const int src = j == 0 ? -1 : pb::firing_iter(res, fa.cond, s, j - 1);
+    const float *hr, *hi;
+    if (src < 0) {
+      hr = fa.state + (int64_t)s * 2 * kHist;
+      hi = hr + kHist;
+    } else {
+      const float* prev = reinterpret_cast<const float*>(pb::span_ptr(fa.in, res, s, src));
+      hr = prev + B - kHist;
+      hi = prev + 2 * B - kHist;
+    }
+#pragma unroll
+    for (int q = 0; q < kHist; ++q) {
+      hist[lane][0][q] = hr[q];
+      hist[lane][1][q] = hi[q];
+    }
+  }
+  __syncwarp();
+  if (lane < kTaps) {
+    float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int b = 0; b < nb; ++b)
+      if ((mask >> b) & 1u) {
+        const float4 c = taps[b][lane];
+        m.x += c.x; m.y += c.y; m.z += c.z; m.w += c.w;
+      }
+    p.taps[lane] = m;
+  }
+  if (lane < kHist) {   // output `lane` reads pre-span sample lane - t for taps t > lane
+    float cr = 0.f, ci = 0.f;
+    for (int b = 0; b < nb; ++b) {
+      if (!((mask >> b) & 1u)) continue;
+      for (int t = lane + 1; t < kTaps; ++t) {
+        const int q = lane - t + kHist;
+        const float hr = hist[b][0][q], hi = hist[b][1][q];
+        const float4 c = taps[b][t];
+        cr = __fmaf_rn(-c.y, hi, __fmaf_rn(c.x, hr, cr));
+        ci = __fmaf_rn(c.y, hr, __fmaf_rn(c.x, hi, ci));
+      }
+    }
+    p.corr[lane] = make_float2(cr, ci);
+  }
+  if (lane == 0) p.have = 1;
+}
+
+#ifndef PB_MERGED_PT
+#define PB_MERGED_PT 8
+#endif
+#ifndef PB_MERGED_MINB
+#define PB_MERGED_MINB 4
+#endif
+constexpr int kMergedThreads = 256;
+constexpr int kMPT = PB_MERGED_PT;             // outputs per thread
+constexpr int kMWin = kMPT + kPad;             // window (samples)
+
+__global__ void __launch_bounds__(kMergedThreads, PB_MERGED_MINB)
+bank_merged_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPlan* plan,
+                   int blocks_per_span) {
+  const int64_t span = blockIdx.x / blocks_per_span;
+  const int part = (int)(blockIdx.x % blocks_per_span);
+  const int s = (int)(span / res.n_iter), n = (int)(span % res.n_iter);
+  __shared__ BankPlan sp;
+  __shared__ const float* in;
+  __shared__ float* out;
+  if (threadIdx.x < (int)(sizeof(BankPlan) / 16))
+    reinterpret_cast<uint4*>(&sp)[threadIdx.x] =
+        __ldg(reinterpret_cast<const uint4*>(plan + span) + threadIdx.x);
+  if (threadIdx.x == 32) {
+    in = reinterpret_cast<const float*>(pb::span_ptr(bank.in, res, s, n));
+    out = reinterpret_cast<float*>(pb::span_ptr(bank.out, res, s, n));
+  }
+  __syncthreads();
+  if (!sp.have) return;
+  const int64_t n0 = ((int64_t)part * kMergedThreads + threadIdx.x) * kMPT;
+  if (n0 >= B) return;
+  float wr[kMWin], wi[kMWin];
+#pragma unroll
+  for (int k = 0; k < kMWin / 4; ++k) {
+    const int64_t idx = n0 - kPad + 4 * k;   // multiple of 4: all-or-nothing pre-span
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (idx >= 0) {
+      a = __ldg(reinterpret_cast<const float4*>(in + idx));
+      b = __ldg(reinterpret_cast<const float4*>(in + B + idx));
+    }
+    wr[4 * k] = a.x; wr[4 * k + 1] = a.y; wr[4 * k + 2] = a.z; wr[4 * k + 3] = a.w;
+    wi[4 * k] = b.x; wi[4 * k + 1] = b.y; wi[4 * k + 2] = b.z; wi[4 * k + 3] = b.w;
+  }
+  float yr[kMPT], yi[kMPT];
+#pragma unroll
+  for (int v = 0; v < kMPT; ++v) yr[v] = yi[v] = 0.0f;
+#pragma unroll
+  for (int t = 0; t < kTaps; ++t) {
+    const float4 c = sp.taps[t];
+#pragma unroll
+    for (int v = 0; v < kMPT; ++v) {
+      const float xr = wr[kPad + v - t], xi = wi[kPad + v - t];
+      yr[v] = __fmaf_rn(-c.y, xi, __fmaf_rn(c.x, xr, yr[v]));
+      yi[v] = __fmaf_rn(c.y, xr, __fmaf_rn(c.x, xi, yi[v]));
+    }
+  }
+  if (n0 < kHist) {
+#pragma unroll
+    for (int v = 0; v < kMPT; ++v)
+      if (n0 + v < kHist) {
+        yr[v] += sp.corr[n0 + v].x;
+        yi[v] += sp.corr[n0 + v].y;
+      }
+  }
+  float4* orr = reinterpret_cast<float4*>(out + n0);
+  float4* oi = reinterpret_cast<float4*>(out + B + n0);
+#pragma unroll
+  for (int k = 0; k < kMPT / 4; ++k) {
+    orr[k] = make_float4(yr[4 * k], yr[4 * k + 1], yr[4 * k + 2], yr[4 * k + 3]);
+    oi[k] = make_float4(yi[4 * k], yi[4 * k + 1], yi[4 * k + 2], yi[4 * k + 3]);
+  }
+}
+
+int launch_merged_bank(const pb_filter_bank& bank, const pb_resolved& res, int64_t B,
+                       cudaStream_t st) {
+  static BankPlan* plan = nullptr;
+  static int64_t plan_n = 0;
+  const int64_t spans = (int64_t)res.n_streams * res.n_iter;
+  if (spans > plan_n) {
+    if (plan) PB_CUDA(cudaFree(plan));
+    PB_CUDA(cudaMalloc(&plan, sizeof(BankPlan) * spans));
+    plan_n = spans;
+  }
+  dim3 pgrid((res.n_iter + kPlanWarps - 1) / kPlanWarps, res.n_streams);
+  bank_plan_kernel<<<pgrid, dim3(32, kPlanWarps), 0, st>>>(bank, res, B, plan);
+  PB_LAUNCHED("bank_plan_kernel");
+  const int bps = (int)((B / kMPT + kMergedThreads - 1) / kMergedThreads);
+  const int64_t blocks = spans * bps;
+  if (blocks >= ((int64_t)1 << 31)) return pb::fail(PB_E_UNSUPPORTED, "filter bank: too many spans");
+  bank_merged_kernel<<<(unsigned)blocks, kMergedThreads, 0, st>>>(bank, res, B, plan, bps);
+  PB_LAUNCHED("bank_merged_kernel");
+  return PB_OK;
 }
 
 int check_block(int64_t B) {
@@ -515,6 +881,9 @@ int launch(const pb_filter_bank& bank, const pb_fir_actor* actors, int n_actors,
       return launch_variant<kBank, PB_FIR_EXACT_PAIRED>(bank, actors, n_actors, res, B, st);
     case PB_FIR_FMA:
       return launch_variant<kBank, PB_FIR_FMA>(bank, actors, n_actors, res, B, st);
+    case PB_FIR_MERGED:   // per-actor launches have nothing to merge: FMA
+      return kBank ? launch_merged_bank(bank, res, B, st)
+                   : launch_variant<kBank, PB_FIR_FMA>(bank, actors, n_actors, res, B, st);
     default:
       return pb::fail(PB_E_INVALID, "unknown FIR math mode " + std::to_string(math));
   }

@@ -213,7 +213,7 @@ class DeviceRuntime:
             if role in ("source", "config", "sink") and is_device(b):
                 raise UnsupportedGraph(f"actor {a.id} ({role}) needs a host behaviour")
 
-        self.fir_math = _lib.PB_FIR_EXACT if config.exact else _lib.PB_FIR_FMA
+        self.fir_math = _lib.PB_FIR_EXACT if config.exact else _lib.PB_FIR_MERGED
         if config.exact and os.environ.get("PB_FIR_MATH") == "paired":
             self.fir_math = _lib.PB_FIR_EXACT_PAIRED
         self.banks = find_filter_banks(plan, self.behaviors[0]) if config.fuse else []

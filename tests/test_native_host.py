@@ -178,8 +178,9 @@ def test_no_fma_in_fir_kernels():
         if "Function :" in line:
             fn = line.split("Function :")[1].strip()
             continue
-        # fir_persistent<bank, 2> is the opt-in FMA tolerance mode (PB_FIR_FMA)
-        exact = not ("fir_persistent" in fn and "Li2E" in fn) if fn else False
+        # fir_persistent<*, 2> / <bank, 3> are the opt-in tolerance modes
+        # (PB_FIR_FMA, PB_FIR_MERGED)
+        exact = not ("fir_persistent" in fn and ("Li2E" in fn or "Li3E" in fn)) if fn else False
         if fn and exact and any(k in fn for k in ("fir_persistent", "branch_sum", "matmul")):
             seen.add(fn)
             if "FFMA" in line or "HFMA2.MMA" in line:
