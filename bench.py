@@ -1,14 +1,19 @@
-"""Benchmark: PRUNE DPD filter bank on B200 (BASELINE.json config 2).
+"""Benchmark: PRUNE DPD filter bank (BASELINE.json config 2) and the CNN
+vision graph (config 3) on B200.
 
-Workload (one "step"): S=64 independent complex-baseband streams per GPU x
-256 blocks x 4096 samples (67.1 Msamples, 537 MB in + 537 MB out per GPU),
+DPD workload (one "step"): S=64 independent complex-baseband streams per GPU
+x 256 blocks x 4096 samples (67.1 Msamples, 537 MB in + 537 MB out per GPU),
 K=4 branches, a control token (subset_policy, CPython-exact RNG, seed
 1000+stream) every 4096 samples.  Metric: stream input Msamples/s, whole job.
+The headline FIR arithmetic is the north star's <= 1e-5 tolerance mode
+(PB_FIR_MERGED); the bit-exact mode is measured in the same run
+(`fir_modes.exact`, or the headline with --exact).
 
   value  device-resident: inputs and control tokens already in HBM; times
-         resolve + fused filter-bank + carry + ring advance per step
+         resolve + fused filter bank + carry + ring advance per step
   e2e    through DeviceRuntime.run_all: pinned-host inputs H2D, native
          control actors, device firings, sink D2H, SHA-256 digests per stream
+  cnn    the same three views for the vision graph (cnn_leg)
 
 python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -44,6 +49,9 @@ def parse():
     ap.add_argument("--block", type=int, default=4096)
     ap.add_argument("--branches", type=int, default=4)
     ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--exact", action="store_true",
+                    help="headline in the bit-exact FIR mode (default: the <= 1e-5 tolerance "
+                         "mode the north star states; both modes are always reported)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-streams", type=int, default=64)
@@ -403,100 +411,70 @@ def main():
     rt.stage_sources(0, blocks, prestaged=True)
     rt.stage_control(0, blocks)
     _lib.check(lib.pb_stream_sync(rt.stream))
-    for _ in range(max(3, args.warmup)):
-        rt.fire_epoch(0, blocks)
-    _lib.check(lib.pb_stream_sync(rt.stream))
-
-    ev = []
+    ms = C.c_float()
 
     def new_event():
         e = C.c_void_p()
         _lib.check(lib.pb_event_create(C.byref(e)))
         return e.value
 
-    bank_ev = []
-
-    def hook(kind, phase):
-        if kind in ("bank", "fir"):
-            e = new_event()
-            lib.pb_event_record(e, rt.stream)
-            bank_ev.append(e)
-
-    clocks = Clocks(local)
-    time.sleep(0.3)
-    barrier()
-    _lib.check(lib.pb_stream_sync(rt.stream))
-    e0, e1 = new_event(), new_event()
-    n_launch0 = lib.pb_launch_count()
-    t_wall0 = time.time()
-    lib.pb_event_record(e0, rt.stream)
-    for _ in range(args.steps):
-        rt.fire_epoch(0, blocks, hook=hook)
-    lib.pb_event_record(e1, rt.stream)
-    _lib.check(lib.pb_stream_sync(rt.stream))
-    t_wall1 = time.time()
-    clocks.mark(t_wall0, t_wall1)
-    launches = lib.pb_launch_count() - n_launch0
-    barrier()
-    ms = C.c_float()
-    _lib.check(lib.pb_event_elapsed_ms(e0, e1, C.byref(ms)))
-    ms_step = max_over_ranks(ms.value / args.steps)
-    kern = []
-    for i in range(0, len(bank_ev) - 1, 2):
-        lib.pb_event_elapsed_ms(bank_ev[i], bank_ev[i + 1], C.byref(ms))
-        kern.append(ms.value)
-    kern_ms = statistics.mean(kern) if kern else float("nan")
-    samples = S * blocks * B * world
-    value = samples / (ms_step / 1e3) / 1e6
-    clk = clocks.summary()
-
-    # tolerance mode (FMA taps, <= 1e-5): same workload, fused kernel only
-    tol = None
-    if not args.no_fuse:
-        rt.set_fir_math(_lib.PB_FIR_MERGED)
-        for _ in range(3):
+    def timed(math_mode, n_steps, clocks=None):
+        """n_steps device-resident steps in one FIR mode: (ms/step max over
+        ranks, mean bank/FIR launch ms on the launching stream, launches)."""
+        rt.set_fir_math(math_mode)
+        for _ in range(max(3, args.warmup)):
             rt.fire_epoch(0, blocks)
         _lib.check(lib.pb_stream_sync(rt.stream))
-        tol_ev = []
+        kev = []
 
-        def tol_hook(kind, phase):
-            if kind == "bank":
+        def hook(kind, phase):
+            if kind in ("bank", "fir"):
                 e = new_event()
                 lib.pb_event_record(e, rt.stream)
-                tol_ev.append(e)
-        n_tol = max(10, args.steps // 4)
-        t0e, t1e = new_event(), new_event()
-        lib.pb_event_record(t0e, rt.stream)
-        for _ in range(n_tol):
-            rt.fire_epoch(0, blocks, hook=tol_hook)
-        lib.pb_event_record(t1e, rt.stream)
+                kev.append(e)
+        if clocks is not None:
+            time.sleep(0.3)
+        barrier()
         _lib.check(lib.pb_stream_sync(rt.stream))
-        _lib.check(lib.pb_event_elapsed_ms(t0e, t1e, C.byref(ms)))
-        tol_ms = max_over_ranks(ms.value / n_tol)
-        tk = []
-        for i in range(0, len(tol_ev) - 1, 2):
-            lib.pb_event_elapsed_ms(tol_ev[i], tol_ev[i + 1], C.byref(ms))
-            tk.append(ms.value)
-        tol_kern_ms = statistics.mean(tk) if tk else float("nan")
-        tol_bytes = 16 * S * blocks * B
-        tol = {"value": samples / (tol_ms / 1e3) / 1e6, "unit": UNIT, "ms_per_step": tol_ms,
-               "mode": "PB_FIR_MERGED: one FMA FIR per sample with the active branches' taps "
-                       "summed (bank_plan_kernel + bank_merged_kernel)",
-               "roofline": {"bound": "hbm", "achieved": tol_bytes / (tol_kern_ms / 1e3) / 1e9,
-                            "peak": None, "unit": "GB/s", "frac": None,
-                            "kernel": "bank_plan_kernel + bank_merged_kernel",
-                            "kernel_ms": tol_kern_ms, "algorithmic_bytes_per_launch": tol_bytes},
-               "hbm_gbs_of_step": tol_bytes / (tol_ms / 1e3) / 1e9,
-               "tolerance": "max |y - y_exact| / max(1, |y_exact|) <= 1e-5 "
-                            "(tests/test_dpd_gpu.py::test_tolerance_mode_within_1e5)"}
-        rt.set_fir_math(_lib.PB_FIR_EXACT)
+        e0, e1 = new_event(), new_event()
+        n0 = lib.pb_launch_count()
+        t_wall0 = time.time()
+        lib.pb_event_record(e0, rt.stream)
+        for _ in range(n_steps):
+            rt.fire_epoch(0, blocks, hook=hook)
+        lib.pb_event_record(e1, rt.stream)
+        _lib.check(lib.pb_stream_sync(rt.stream))
+        if clocks is not None:
+            clocks.mark(t_wall0, time.time())
+        n_l = lib.pb_launch_count() - n0
+        barrier()
+        _lib.check(lib.pb_event_elapsed_ms(e0, e1, C.byref(ms)))
+        step = max_over_ranks(ms.value / n_steps)
+        kt = []
+        for i in range(0, len(kev) - 1, 2):
+            lib.pb_event_elapsed_ms(kev[i], kev[i + 1], C.byref(ms))
+            kt.append(ms.value)
+        return step, (statistics.mean(kt) if kt else float("nan")), n_l
+
+    fused = not args.no_fuse
+    exact_math = _lib.PB_FIR_EXACT
+    tol_math = _lib.PB_FIR_MERGED if fused else _lib.PB_FIR_FMA
+    head_math = exact_math if args.exact else tol_math
+    clocks = Clocks(local)
+    ms_step, kern_ms, launches = timed(head_math, args.steps, clocks)
+    clk = clocks.summary()
+    other_math = tol_math if args.exact else exact_math
+    o_step, o_kern, _ = timed(other_math, max(10, args.steps // 4))
+    samples = S * blocks * B * world
+    value = samples / (ms_step / 1e3) / 1e6
 
     # active firings of this workload (resolved on the device by the timed steps)
     counts = np.zeros((len(rt.plan.conds), S), dtype=np.int32)
     lib.pb_memcpy_d2h(counts.ctypes.data, rt.res_count, counts.nbytes, rt.stream)
     lib.pb_stream_sync(rt.stream)
 
-    # ---- end to end through the public runtime API
+    # ---- end to end through the public runtime API (headline FIR mode)
+    rt.set_fir_math(head_math)
     e2e_times = []
     reps = None
     for k in range(args.e2e_steps + 1 if args.e2e_steps > 0 else 0):
@@ -511,15 +489,31 @@ def main():
     h2d = S * blocks * span + S * blocks * rt.ctl_stride[next(iter(rt.ctl_ports))]
     d2h = S * blocks * span + 4 * len(rt.plan.conds) * S
 
-    # parity spot check of the e2e result on stream 0 against the oracle
+    # parity of stream 0 against the oracle, through the same public API in the
+    # headline FIR mode (a separate one-stream run that keeps the sink bytes):
+    # bit-exact in the exact mode, <= 1e-5 (relative to max(1, |y|)) in the
+    # tolerance mode; the timed e2e runs above digest without keeping them
     parity = None
-    if rank == 0:
+    if rank == 0 and reps:
         from oracle import dpd as od
-        import hashlib
+        from paper_1802_06625_b200 import run_streams
         x0 = pd.stream_input(streams[0], blocks, B)
+        (rep0,) = run_streams(pd.build_description(B, K), 1,
+                              RuntimeConfig(source_firings=blocks, epoch=blocks, fuse=fused,
+                                            device=local, capture_sinks=True,
+                                            exact=bool(args.exact)),
+                              seeds=[pd.stream_seed(streams[0])], sources={"src": [x0.tobytes()]})
         sets = od.subset_schedule(pd.stream_seed(streams[0]), blocks, length=K)
-        want = hashlib.sha256(od.dpd_stream(x0, sets, K).tobytes()).hexdigest()
-        parity = reps[0].sink_digests["sink"] == want if reps else None
+        want = od.dpd_stream(x0, sets, K)
+        got = np.frombuffer(rep0.sink_data["sink"], np.float32).reshape(want.shape)
+        err = float((np.abs(got.astype(np.float64) - want) /
+                     np.maximum(1.0, np.abs(want.astype(np.float64)))).max())
+        exact_eq = bool(got.tobytes() == want.tobytes())
+        parity = {"bit_exact": exact_eq, "max_rel_err": err,
+                  "ok": exact_eq if args.exact else err <= 1e-5,
+                  "firing_counts_exact": rep0.firing_counts == od.firing_counts(sets, K),
+                  "digest_matches_timed_run": rep0.sink_digests["sink"] ==
+                  reps[0].sink_digests["sink"]}
 
     peaks = {}
     try:
@@ -527,31 +521,22 @@ def main():
         hbm_peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
     except Exception:  # noqa: BLE001
         hbm_peak, peak_src = 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
-    if tol is not None:
-        tol["roofline"]["peak"] = hbm_peak
-        tol["roofline"]["frac"] = tol["roofline"]["achieved"] / hbm_peak
-        tol["hbm_frac_of_step"] = tol.pop("hbm_gbs_of_step") / hbm_peak
-    achieved = None
-    traffic = None
-    prof = ROOT / "profiles" / "ncu_summary.json"
-    if prof.exists():
-        try:
-            traffic = json.loads(prof.read_text()).get("filter_bank_kernel", {}).get(
-                "dram_bytes_per_launch")
-        except Exception:  # noqa: BLE001
-            traffic = None
-    # FP32 view: the bit-exact FIR forbids FMA, so each active branch-sample
-    # costs 80 rounded FP32 ops (10 taps x 4 mul + 2 add/sub + 2 accumulate)
-    # plus 2 for the branch sum; the active branch count comes from the
-    # device-resolved control tokens of this workload.
+    ncu = {}
+    try:   # per-launch DRAM bytes of the same kernels from the committed ncu capture
+        ncu = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+    except Exception:  # noqa: BLE001
+        ncu = {}
+    # FP32 view of the exact mode: FMA is forbidden, so each active
+    # branch-sample costs 80 rounded FP32 ops (10 taps x (4 mul + 2 add/sub +
+    # 2 accumulate)) plus 2 for the branch sum; the active branch count comes
+    # from the device-resolved control tokens of this workload.
     branch_samples = int(counts.sum()) * B
-    if args.no_fuse:
-        alg_bytes = 16 * branch_samples      # per fir_branch firing: 8 B read + 8 B written
-        fp32_ops = 80 * branch_samples
-    else:
+    if fused:
         alg_bytes = 16 * S * blocks * B      # fused bank: 8 B read + 8 B written per sample
         fp32_ops = 82 * branch_samples
-    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    else:
+        alg_bytes = 16 * branch_samples      # per fir_branch firing: 8 B read + 8 B written
+        fp32_ops = 80 * branch_samples
     probe = {}
     try:
         probe = json.loads((ROOT / "profiles" / "r1_fp32_probe.json").read_text())
@@ -559,6 +544,48 @@ def main():
         pass
     fp32_peak = 1e12 * max(probe.get("fmul_tops", 0), probe.get("fadd_tops", 0)) or \
         148 * 128 * 1.965e9
+    names = {exact_math: "fir_persistent<bank, EXACT>" if fused else "fir_persistent<actors>",
+             tol_math: "bank_plan_kernel + bank_merged_kernel" if fused else
+             "fir_persistent<actors, FMA>"}
+
+    def roofline(math_mode, k_ms):
+        a = alg_bytes / (k_ms / 1e3) / 1e9
+        tr = ncu.get(names[math_mode])
+        return {"bound": "hbm", "achieved": a, "peak": hbm_peak, "unit": "GB/s",
+                "frac": a / hbm_peak, "traffic": tr, "kernel": names[math_mode],
+                "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg_bytes,
+                "bytes_per_unit": "16 B per stream sample (8 B read + 8 B written)",
+                "peak_source": peak_src}
+
+    exact_ms, exact_kern = (ms_step, kern_ms) if args.exact else (o_step, o_kern)
+    modes = {
+        "headline": "exact" if args.exact else "tolerance",
+        "tolerance": {
+            "math": "PB_FIR_MERGED" if fused else "PB_FIR_FMA",
+            "what": "one FMA FIR per sample with the active branches' taps summed per span, "
+                    "each branch's 9-sample history as a correction of outputs 0..8",
+            "tolerance": "max |y - y_exact| / max(1, |y_exact|) <= 1e-5 "
+                         "(tests/test_dpd_gpu.py::test_tolerance_mode_within_1e5)"},
+        "exact": {
+            "math": "PB_FIR_EXACT",
+            "what": "bit-exact FirBranch.fire per active branch (every product and sum "
+                    "rounded, no FMA), summed in combiner port order",
+            "value": S * blocks * B * world / (exact_ms / 1e3) / 1e6, "unit": UNIT,
+            "ms_per_step": exact_ms, "roofline": roofline(exact_math, exact_kern),
+            "fp32": {"achieved": fp32_ops / (exact_kern / 1e3) / 1e12, "unit": "TFLOP/s",
+                     "peak": fp32_peak / 1e12,
+                     "frac": fp32_ops / (exact_kern / 1e3) / fp32_peak,
+                     "ops_per_launch": fp32_ops,
+                     "mean_active_branches": int(counts.sum()) / (S * blocks),
+                     "note": "the binding roof of the exact mode: non-FMA FP32 lane ops; peak = "
+                             "profiles/r1_fp32_probe.json (measured FMUL/FADD throughput)"}},
+    }
+    if not args.exact:
+        modes["exact"]["value"] = S * blocks * B * world / (o_step / 1e3) / 1e6
+    else:
+        modes["tolerance"].update({
+            "value": S * blocks * B * world / (o_step / 1e3) / 1e6, "unit": UNIT,
+            "ms_per_step": o_step, "roofline": roofline(tol_math, o_kern)})
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
@@ -588,26 +615,18 @@ def main():
             "config": {"workload": f"C2 DPD: {S} streams/GPU x {blocks} blocks x {B} samples, "
                                    f"K={K} branches, subset_policy control per block",
                        "fused": not args.no_fuse, "streams_per_gpu": S,
+                       "fir_math": "exact (bit-exact)" if args.exact else
+                       "tolerance (PB_FIR_MERGED, <= 1e-5; the exact mode is in fir_modes)",
                        "l2": "inputs (537 MB/GPU) larger than L2; no flush needed",
                        "parallelism": f"{world} GPU(s), streams sharded, no collectives"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": "filter_bank_kernel" if not args.no_fuse else "fir_kernel",
-                         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": alg_bytes,
-                         "peak_source": peak_src},
-            "fp32": {"achieved": fp32_ops / (kern_ms / 1e3) / 1e12, "unit": "TFLOP/s",
-                     "peak": fp32_peak / 1e12, "frac": fp32_ops / (kern_ms / 1e3) / fp32_peak,
-                     "ops_per_launch": fp32_ops, "mean_active_branches":
-                     int(counts.sum()) / (S * blocks),
-                     "note": "non-FMA FP32 lane ops; peak = profiles/r1_fp32_probe.json "
-                             "(measured FMUL/FADD throughput)"},
+            "roofline": roofline(head_math, kern_ms),
+            "fir_modes": modes,
             "clocks": clk,
             "e2e": {"value": samples / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s,
                     "includes": "H2D pinned inputs, native control actors, device firings, "
                                 "sink D2H, SHA-256 per stream"},
             "gpu_launches": launches,
-            "tolerance_mode": tol,
             "parity_stream0": parity,
             "cpu_baseline": cpu,
             "cnn": cnn,

@@ -757,34 +757,38 @@ bank_merged_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
   const int part = (int)(blockIdx.x % blocks_per_span);
   const int s = (int)(span / res.n_iter), n = (int)(span % res.n_iter);
   __shared__ BankPlan sp;
-  __shared__ const float* in;
-  __shared__ float* out;
+  // the window loads go out before the plan is known (an inactive span's
+  // input is still valid ring memory), so the block's start-up costs one
+  // memory round trip, not two
+  const float* in = reinterpret_cast<const float*>(pb::span_ptr(bank.in, res, s, n));
   if (threadIdx.x < (int)(sizeof(BankPlan) / 16))
     reinterpret_cast<uint4*>(&sp)[threadIdx.x] =
         __ldg(reinterpret_cast<const uint4*>(plan + span) + threadIdx.x);
-  if (threadIdx.x == 32) {
-    in = reinterpret_cast<const float*>(pb::span_ptr(bank.in, res, s, n));
-    out = reinterpret_cast<float*>(pb::span_ptr(bank.out, res, s, n));
-  }
-  __syncthreads();
-  if (!sp.have) return;
   const int64_t n0 = ((int64_t)part * kMergedThreads + threadIdx.x) * kMPT;
-  if (n0 >= B) return;
+  const bool live = n0 < B;
   float wr[kMWin], wi[kMWin];
 #pragma unroll
   for (int k = 0; k < kMWin / 4; ++k) {
     const int64_t idx = n0 - kPad + 4 * k;   // multiple of 4: all-or-nothing pre-span
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-    if (idx >= 0) {
+    if (live && idx >= 0) {
       a = __ldg(reinterpret_cast<const float4*>(in + idx));
       b = __ldg(reinterpret_cast<const float4*>(in + B + idx));
     }
     wr[4 * k] = a.x; wr[4 * k + 1] = a.y; wr[4 * k + 2] = a.z; wr[4 * k + 3] = a.w;
     wi[4 * k] = b.x; wi[4 * k + 1] = b.y; wi[4 * k + 2] = b.z; wi[4 * k + 3] = b.w;
   }
+  __syncthreads();
+  if (!sp.have || !live) return;
+  float* out = reinterpret_cast<float*>(pb::span_ptr(bank.out, res, s, n));
   float yr[kMPT], yi[kMPT];
 #pragma unroll
   for (int v = 0; v < kMPT; ++v) yr[v] = yi[v] = 0.0f;
+#ifdef PB_MERGED_COPYONLY   // profiling variant: memory traffic without the FIR
+#pragma unroll
+  for (int v = 0; v < kMPT; ++v) { yr[v] = wr[kPad + v]; yi[v] = wi[kPad + v]; }
+  if (0)
+#endif
 #pragma unroll
   for (int t = 0; t < kTaps; ++t) {
     const float4 c = sp.taps[t];

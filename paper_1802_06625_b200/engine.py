@@ -776,7 +776,7 @@ class DeviceRuntime:
                 data = bufs[0][2][s].reshape(-1)
                 h.update(data)
                 if cap is not None:
-                    cap.extend(data.tobytes())
+                    cap += memoryview(np.ascontiguousarray(data)).cast("B")
                 return
             for n in range(E):
                 if active is not None and not active[n]:
@@ -921,7 +921,7 @@ class DeviceRuntime:
                 data = arr[s, w:w + n].reshape(-1)
                 self.digests[a.id][s].update(data)
                 if self.captured is not None:
-                    self.captured[a.id][s].extend(data.tobytes())
+                    self.captured[a.id][s] += memoryview(np.ascontiguousarray(data)).cast("B")
             list(hash_pool.map(one, [(a, f, s) for a, f in sinks for s in range(S)]))
 
         try:

@@ -79,3 +79,36 @@ def test_vision_graph_logits(epoch):
         assert fc["l1"] == fc["l2"] == fc["l3"] == firings // 2
         assert fc["join"] == fc["sink"] == firings
         assert reps[s].eq1_checks == 4 * firings and reps[s].eq1_failures == 0
+
+
+@pytest.mark.parametrize("h,w,cin,pad", [(28, 28, 3, 2), (20, 36, 16, 0), (36, 44, 32, 2),
+                                         (12, 8, 32, 0), (96, 96, 3, 6)])
+def test_conv_shapes(h, w, cin, pad):
+    """Ragged super-tiles: output sizes that are not multiples of the 16x16 /
+    32x16 super-tile, every supported Cin, zero padding on all sides."""
+    R, firings = 2, 2
+    rng = np.random.default_rng(h * 100 + w)
+    x = rng.standard_normal((R * firings, h, w, cin)).astype(np.float32)
+    desc = {"name": "conv1", "control": {},
+            "actors": [
+                {"id": "src", "kind": "static", "behavior": "file_source",
+                 "params": {"path": "x.bin"},
+                 "ports": [{"id": "out", "dir": "out", "kind": "srp", "rate": R}]},
+                {"id": "c", "kind": "static", "behavior": "conv2d_relu_pool",
+                 "params": {"h": h, "w": w, "cin": cin, "cout": 32, "pad": pad, "seed": 9},
+                 "ports": [{"id": "in", "dir": "in", "kind": "srp", "rate": R},
+                           {"id": "out", "dir": "out", "kind": "srp", "rate": R}]},
+                {"id": "sink", "kind": "static", "behavior": "null_sink",
+                 "ports": [{"id": "in", "dir": "in", "kind": "srp", "rate": R}]}],
+            "fifos": [
+                {"id": "a", "src": "src.out", "dst": "c.in", "rate": R,
+                 "token_bytes": h * w * cin * 4},
+                {"id": "b", "src": "c.out", "dst": "sink.in", "rate": R,
+                 "token_bytes": ((h + 2 * pad - 4) // 2) * ((w + 2 * pad - 4) // 2) * 32 * 4}]}
+    (rep,) = run_streams(desc, 1, RuntimeConfig(source_firings=firings, capture_sinks=True),
+                         sources={"src": [x.tobytes()]})
+    from paper_1802_06625_b200.cnn_weights import layer_params
+    wt, b = layer_params({"seed": 9}, 32, 25 * cin)
+    want = oc.conv_relu_pool(x, wt, b, pad)
+    got = np.frombuffer(rep.sink_data["sink"], np.float32).reshape(want.shape)
+    assert rel_err(got, want) <= ACT_TOL

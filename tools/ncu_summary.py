@@ -5,7 +5,8 @@ import json
 import subprocess
 import sys
 
-WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+WANT = ['gpu__time_duration.sum', 'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active',
+        'sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
         'sm__throughput.avg.pct_of_peak_sustained_elapsed',
         'gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed',
         'dram__throughput.avg.pct_of_peak_sustained_elapsed',
@@ -41,7 +42,10 @@ def summarise(path):
                 st[s] = float(vals[hdr.index(key)] or 0)
         d["stalls_per_issue"] = {k: round(v, 3) for k, v in sorted(st.items(), key=lambda x: -x[1])
                                  if v > 0.01}
-        res[name.split("(")[0]] = d
+        key = name.split("(")[0]
+        if key in res:
+            key = f"{key} #{sum(k.startswith(key) for k in res) + 1}"
+        res[key] = d
     return res
 
 

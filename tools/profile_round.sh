@@ -1,16 +1,20 @@
 #!/usr/bin/env bash
-# Round profiling pass (run under gpurun): launch list of one bench step,
-# ncu --set full of the dominant kernel (fused filter bank) and of the
-# per-actor FIR kernel; summaries land in gpurun_out/ and are copied to
-# profiles/ by hand.
-set -x
+# Round profiling pass (run under gpurun, one GPU): launch list of one bench
+# step (DPD + CNN) and ncu --set full captures of the dominant kernels; the
+# summaries land in gpurun_out/ and are copied to profiles/ by hand.
 mkdir -p gpurun_out
 R=${ROUND:-r1}
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv \
-  --log-file gpurun_out/${R}_launches.csv python bench.py --steps 3 --warmup 3 --skip-cpu --e2e-steps 0 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fir_persistent -s 2 -c 1 \
-  -o gpurun_out/${R}_bank python bench.py --steps 2 --warmup 3 --skip-cpu --e2e-steps 0 > gpurun_out/${R}_ncu_bank.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fir_persistent -s 1 -c 1 \
-  -o gpurun_out/${R}_fir python bench.py --steps 2 --warmup 3 --skip-cpu --e2e-steps 0 --no-fuse > gpurun_out/${R}_ncu_fir.log 2>&1
-python tools/ncu_summary.py gpurun_out/${R}_bank.ncu-rep > gpurun_out/${R}_ncu_bank.json
-python tools/ncu_summary.py gpurun_out/${R}_fir.ncu-rep > gpurun_out/${R}_ncu_fir.json
+B="python bench.py --steps 2 --warmup 3 --skip-cpu --e2e-steps 0 --cnn-steps 1 --cnn-e2e-steps 0"
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 80 --csv \
+  --log-file gpurun_out/${R}_launches.csv $B > /dev/null 2>&1
+echo "launches: $?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:bank_ -c 2 \
+  -o gpurun_out/${R}_merged $B --skip-cnn > /dev/null 2>&1; echo "merged: $?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:fir_persistent -c 1 \
+  -o gpurun_out/${R}_exact python bench.py --steps 2 --warmup 3 --skip-cpu --e2e-steps 0 --skip-cnn --exact > /dev/null 2>&1; echo "exact: $?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"conv_pool|dense_kernel" -c 3 \
+  -o gpurun_out/${R}_cnn python tools/cnn_bench.py 2 32 24 1 > /dev/null 2>&1; echo "cnn: $?"
+for r in merged exact cnn; do
+  python tools/ncu_summary.py gpurun_out/${R}_$r.ncu-rep > gpurun_out/${R}_ncu_$r.json 2>/dev/null
+done
+ls -la gpurun_out/
