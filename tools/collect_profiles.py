@@ -1,0 +1,65 @@
+"""Copy the round's GPU evidence from gpurun_out/ into profiles/ (tracked):
+launch list (per-launch time + DRAM bytes, cold-cache and serialised under
+ncu: compare shares, not absolutes), ncu --set full summaries, the DRAM
+traffic per launch of the headline kernels (read by bench.py as
+roofline.traffic) and the bench line."""
+import csv
+import json
+import shutil
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+R = sys.argv[1] if len(sys.argv) > 1 else "r1"
+out = ROOT / "gpurun_out"
+prof = ROOT / "profiles"
+
+
+def launches():
+    rows = [r for r in csv.reader(open(out / f"{R}_launches.csv")) if len(r) > 10]
+    h = rows[0]
+    iK, iM, iV, iI = (h.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
+    d = {}
+    for r in rows[1:]:
+        e = d.setdefault(int(r[iI]), {"id": int(r[iI]), "kernel": r[iK].split("(")[0]})
+        v = float(r[iV].replace(",", ""))
+        e[{"gpu__time_duration.sum": "ns", "dram__bytes_read.sum": "dram_read",
+           "dram__bytes_write.sum": "dram_write"}.get(r[iM], r[iM])] = v
+    return [d[k] for k in sorted(d)]
+
+
+L = launches()
+(prof / f"{R}_launches.json").write_text(json.dumps({
+    "command": "tools/profile_round.sh: ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+               "dram__bytes_write.sum --clock-control none -c 80 python bench.py --steps 2 "
+               "--warmup 3 --skip-cpu --e2e-steps 0 --cnn-steps 1 --cnn-e2e-steps 0",
+    "note": "per-launch device times, cold-cache and serialised under ncu: compare shares, "
+            "not absolutes; units ns and bytes",
+    "launches": L}, indent=1))
+traffic = {}
+
+
+def last(kname):
+    xs = [x for x in L if kname in x["kernel"]]
+    return xs[-1] if xs else None
+
+
+m, p = last("bank_merged_kernel"), last("bank_plan_kernel")
+if m and p:
+    traffic["bank_plan_kernel + bank_merged_kernel"] = \
+        m["dram_read"] + m["dram_write"] + p["dram_read"] + p["dram_write"]
+e = last("fir_persistent<1, 0>")
+if e:
+    traffic["fir_persistent<bank, EXACT>"] = e["dram_read"] + e["dram_write"]
+for nm in ("conv_pool_kernel<0, 3>", "conv_pool_kernel<1, 32>", "dense_kernel"):
+    x = last(nm)
+    if x:
+        traffic[nm] = x["dram_read"] + x["dram_write"]
+(prof / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1))
+for r in ("merged", "exact", "cnn"):
+    src = out / f"{R}_ncu_{r}.json"
+    if src.exists():
+        shutil.copy(src, prof / f"{R}_ncu_{r}.json")
+if (out / "bench.json").exists():
+    shutil.copy(out / "bench.json", prof / f"{R}_bench.json")
+print(json.dumps(traffic, indent=1))
