@@ -319,9 +319,14 @@ typedef struct {
   int32_t h, w, cin, cout, pad;
   int32_t cond;
   int32_t debug;           /* 0; profiling only: bit0 skip patch fill, bit1 skip
-                              epilogue, bit2 skip MMAs (results are garbage) */
+                              epilogue, bit2 skip MMAs, bit3 skip the layer-1 raw
+                              TMA loads (results are garbage) */
 } pb_conv_actor;
 int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream);
+/* Profiling builds (-DPB_CONV_PROF=1) only: per-CTA role timing counters of
+ * conv_pool_kernel, uint64 [160][16] clock cycles (slots in csrc/pb_cnn.cu);
+ * all zero in normal builds.  reset != 0 zeroes them after the copy. */
+int pb_conv_debug_counters(unsigned long long* out, int reset);
 
 /* dense: out[f] = W x[f] + b, W [nout][nin] (nout <= 112, nin % 64 == 0), as a
  * tcgen05 GEMM over 128 frames gathered across firings (bf16x3 split, fp32

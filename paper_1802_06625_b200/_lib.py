@@ -172,6 +172,7 @@ SIGNATURES = {
     "pb_fire_matmul": (C.c_int, [MatmulActor, Resolved, vp]),
     "pb_fire_path_merge": (C.c_int, [PathMergeActor, Resolved, vp]),
     "pb_fire_conv_pool": (C.c_int, [ConvActor, Resolved, vp]),
+    "pb_conv_debug_counters": (C.c_int, [vp, C.c_int]),
     "pb_fire_dense": (C.c_int, [DenseActor, Resolved, vp]),
     "pb_fire_classify": (C.c_int, [ClassifyActor, Resolved, vp]),
     "pb_policy_init": (C.c_int, [vp, i64]),

@@ -34,6 +34,7 @@
 //     over with mbarriers (converters -> MMA: 128 arrivals; MMA -> converter
 //     and epilogue: tcgen05.commit; epilogue -> MMA: 128 arrivals).
 //   * All weights stay resident in shared memory for the whole launch.
+//   * Patches and accumulators: NB buffers (layer 1: 3, layer 2: 2).
 #include <algorithm>
 
 #include <cuda.h>
@@ -46,13 +47,16 @@ namespace {
 
 constexpr int kTW = 8, kTH = 16;            // conv pixels per MMA tile (M = 128)
 constexpr int kPH = kTH + 4;                // patch rows
-constexpr int kEpiWarps = 8, kCvtWarps = 7;   // 16 warps: 4 per SM sub-partition, 128 regs
+constexpr int kEpiWarps = 8, kCvtWarps = 6;   // + MMA + scheduler = 16 warps: 4 per SMSP, 128 regs
 constexpr int kMmaWarp = kEpiWarps;
 constexpr int kCvtWarp0 = kMmaWarp + 1;
-constexpr int kConvThreads = (kEpiWarps + 1 + kCvtWarps) * 32;
+constexpr int kSchedWarp = kCvtWarp0 + kCvtWarps;   // walks the work list
+constexpr int kSchedRing = 16;
+constexpr int kConvThreads = (kEpiWarps + 1 + kCvtWarps + 1) * 32;
 constexpr int kCvtThreads = kCvtWarps * 32;
 constexpr int kEpiThreads = kEpiWarps * 32;
-constexpr int kTmemCols = 256;              // 2 accumulator sets x ST tiles x ACC columns
+constexpr int kTmemCols = 512;              // NB accumulator sets x ST tiles x ACC columns
+constexpr int kMaxNB = 4;
 constexpr int kStepBytes = 64 * 16 * 2;     // one K-step of [wh; wl]: 64 rows x 16 bf16
 constexpr int kCout = 32;
 constexpr int kRawBufs = 6;                 // layer-1 raw boxes in flight (prefetch depth 5)
@@ -147,7 +151,13 @@ __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
 // run of tcgen05.mma with immediate descriptor offsets.
 template <int MODE, int CIN>
 struct ConvCfg {
-  static constexpr int ST = MODE ? 2 : 4;                 // tiles per super-tile
+#ifndef PB_CONV_ST0
+#define PB_CONV_ST0 4
+#endif
+#ifndef PB_CONV_SPLIT3_0
+#define PB_CONV_SPLIT3_0 1
+#endif
+  static constexpr int ST = MODE ? 2 : PB_CONV_ST0;       // tiles per super-tile
   static constexpr int NP = MODE ? CIN / 8 : 2;           // 16-B planes per precision piece
   static constexpr int PW = ST * kTW + (MODE ? 4 : 0);    // patch width (entries)
   static constexpr int PS = kPH * PW * 16;                // plane stride (bytes)
@@ -155,7 +165,7 @@ struct ConvCfg {
   // layer 2 is MMA-bound: B = [wh; wl] (N = 64) gives two products per MMA and
   // the epilogue adds the column halves; layer 1 is epilogue-bound: three
   // N = 32 MMAs accumulate all products into 32 columns
-  static constexpr bool SPLIT3 = MODE == 0;
+  static constexpr bool SPLIT3 = MODE == 0 && PB_CONV_SPLIT3_0;
   static constexpr int ACC = SPLIT3 ? 32 : 64;            // TMEM columns per tile
   static constexpr int PATCH = 2 * NP * PS;
   static constexpr int WBYTES = STEPS * kStepBytes;
@@ -166,16 +176,38 @@ struct ConvCfg {
   static constexpr int RAW_W = MODE ? 0 : ((PW + 4) * 3 + 3 + 3) / 4 * 4;   // floats per raw row
   static constexpr int RAW_TX = kPH * RAW_W * 4;          // bytes per box
   static constexpr int RAW = MODE ? 0 : ((RAW_TX + 127) / 128) * 128;
-  static constexpr int SMEM = WBYTES + 2 * PATCH + kRawBufs * RAW;
+#ifndef PB_CONV_NB0
+#define PB_CONV_NB0 3
+#endif
+  // patch / accumulator buffers in flight (layer 2 is shared-memory-limited)
+  static constexpr int NB = MODE ? 2 : PB_CONV_NB0;
+  static constexpr int SMEM = WBYTES + NB * PATCH + kRawBufs * RAW;
+  static_assert(NB <= kMaxNB && NB * ST * ACC <= kTmemCols, "conv buffers");
   static __host__ __device__ constexpr int a_off(int s) {   // bytes, tile 0, hi piece
     return MODE ? 2 * (s % (CIN / 16)) * PS + (((s / (CIN / 16)) / 5) * PW + (s / (CIN / 16)) % 5) * 16
                 : s * PW * 16;
   }
 };
 
+// n / d for 0 <= n < 2^24 without an integer divide: float reciprocal, then
+// an exact one-step correction.
+struct FastDiv {
+  int d;
+  float inv;
+};
+__device__ __forceinline__ FastDiv fast_div(int d) { return FastDiv{d, 1.0f / (float)d}; }
+__device__ __forceinline__ int fdiv(int n, FastDiv f) {
+  int q = __float2int_rz(__int2float_rn(n) * f.inv);
+  const int r = n - q * f.d;
+  if (r < 0) --q;
+  else if (r >= f.d) ++q;
+  return q;
+}
+
 struct ConvRun {   // runtime geometry
   int H, W, pad, Ho, Wo, Hp, Wp, sx_n, per_frame, per_unit, n_units;
   int64_t in_frame, out_frame;
+  FastDiv d_iter, d_frame, d_sx;   // n_iter, per_frame, sx_n
 };
 
 template <class Cfg>
@@ -190,11 +222,53 @@ __device__ __forceinline__ ConvRun conv_run(const pb_conv_actor& a, const pb_res
   g.n_units = res.n_streams * res.n_iter;
   g.in_frame = (int64_t)g.H * g.W * a.cin;
   g.out_frame = (int64_t)g.Hp * g.Wp * kCout;
+  g.d_iter = fast_div(res.n_iter);
+  g.d_frame = fast_div(g.per_frame);
+  g.d_sx = fast_div(g.sx_n);
   return g;
 }
 
+constexpr int kMaxStreams = 1024;          // per-stream firing counts cached in smem
+
+// Role timing (profiling builds only: -DPB_CONV_PROF=1, tools/build_variant.sh):
+// one thread per role accumulates clock64 deltas per phase into g_conv_prof
+// [CTA][slot]; read with pb_conv_debug_counters.
+#ifndef PB_CONV_PROF
+#define PB_CONV_PROF 0
+#endif
+constexpr int kProfCtas = 160, kProfSlots = 16;
+__device__ unsigned long long g_conv_prof[kProfCtas][kProfSlots];
+#define PROF_START() long long prof_t_ = PB_CONV_PROF ? clock64() : 0
+#define PROF(on, slot)                                                              \
+  do {                                                                              \
+    if (PB_CONV_PROF && (on)) {                                                     \
+      const long long n_ = clock64();                                               \
+      atomicAdd(&g_conv_prof[blockIdx.x % kProfCtas][slot], (unsigned long long)(n_ - prof_t_)); \
+      prof_t_ = n_;                                                                 \
+    }                                                                               \
+  } while (0)
+
+struct SuperTile {
+  const float* fin;   // input frame
+  float* fout;        // output frame
+  int oy0, ox0;       // conv-output origin
+  int frame;          // global input frame index (layer-1 TMA coordinate)
+  int pad_;
+};
+
+// Super-tile descriptors the converters publish with each patch (the MMA warp
+// and the epilogue never walk the work list or touch global memory for it).
+// A slot is rewritten 8 super-tiles later; the converters run at most NB
+// super-tiles ahead of the MMA warp and it at most NB ahead of the epilogue.
+constexpr int kDescRing = 8;
+static_assert(2 * kMaxNB <= kDescRing, "descriptor ring");
+
 struct ConvBars {
-  uint64_t full[2], empty[2], acc_full[2], acc_empty[2], raw_full[kRawBufs];
+  uint64_t full[kMaxNB], empty[kMaxNB], acc_full[kMaxNB], acc_empty[kMaxNB], raw_full[kRawBufs];
+  SuperTile desc[kDescRing];                  // fin unused; fout == nullptr: end of work
+  SuperTile sched[kSchedRing];                // the scheduler warp's work list ring
+  uint64_t sched_full[kSchedRing], sched_empty[kSchedRing];
+  int cnt[kMaxStreams];                       // live firings per stream (cond_count)
   uint32_t tmem_base;
   float bias[kCout];
 };
@@ -207,26 +281,28 @@ struct Cursor {
   bool live;
 };
 
-__device__ __forceinline__ void cursor_fix(Cursor& c, const ConvRun& g, const pb_conv_actor& a,
+// cnt: the per-stream live-firing counts, cached in shared memory, so walking
+// the cursor never waits on global memory
+__device__ __forceinline__ void cursor_fix(Cursor& c, const ConvRun& g, const int* cnt,
                                            const pb_resolved& res) {
   if (c.unit < g.n_units) {
-    c.s = c.unit / res.n_iter;
+    c.s = fdiv(c.unit, g.d_iter);
     c.j = c.unit - c.s * res.n_iter;
-    c.live = c.j < pb::cond_count(res, a.cond, c.s);
+    c.live = c.j < cnt[c.s];
   }
 }
 
-__device__ __forceinline__ Cursor cursor_first(const ConvRun& g, const pb_conv_actor& a,
+__device__ __forceinline__ Cursor cursor_first(const ConvRun& g, const int* cnt,
                                                const pb_resolved& res) {
   Cursor c;
   c.unit = blockIdx.x / g.per_unit;
   c.rem = blockIdx.x - c.unit * g.per_unit;
   c.live = false;
-  cursor_fix(c, g, a, res);
+  cursor_fix(c, g, cnt, res);
   return c;
 }
 
-__device__ __forceinline__ void cursor_step(Cursor& c, const ConvRun& g, const pb_conv_actor& a,
+__device__ __forceinline__ void cursor_step(Cursor& c, const ConvRun& g, const int* cnt,
                                             const pb_resolved& res) {
   c.rem += gridDim.x;
   if (c.rem >= g.per_unit) {
@@ -234,34 +310,71 @@ __device__ __forceinline__ void cursor_step(Cursor& c, const ConvRun& g, const p
       c.rem -= g.per_unit;
       ++c.unit;
     }
-    cursor_fix(c, g, a, res);
+    cursor_fix(c, g, cnt, res);
   }
 }
 
 // next live super-tile (including the current one)
-__device__ __forceinline__ bool cursor_live(Cursor& c, const ConvRun& g, const pb_conv_actor& a,
+__device__ __forceinline__ bool cursor_live(Cursor& c, const ConvRun& g, const int* cnt,
                                             const pb_resolved& res) {
-  while (c.unit < g.n_units && !c.live) cursor_step(c, g, a, res);
+  while (c.unit < g.n_units && !c.live) cursor_step(c, g, cnt, res);
   return c.unit < g.n_units;
 }
 
-struct SuperTile {
-  const float* fin;   // input frame
-  float* fout;        // output frame
-  int oy0, ox0;       // conv-output origin
+// Firing spans of every (stream, iteration) unit, resolved once per launch by
+// conv_units_kernel (nullptr: the actor does not fire there): a super-tile's
+// pointers are then one independent 16-byte load, not a chain of three.
+struct UnitSpans {
+  const float* in;
+  float* out;
+  int frame0;   // global frame index of the input span (layer-1 TMA coordinate)
+  int pad_;
+};
+
+__global__ void conv_units_kernel(pb_conv_actor a, pb_resolved res, UnitSpans* units) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= res.n_streams * res.n_iter) return;
+  const int s = u / res.n_iter, j = u - s * res.n_iter;
+  UnitSpans r{nullptr, nullptr, 0, 0};
+  if (j < pb::cond_count(res, a.cond, s)) {
+    const int n = pb::firing_iter(res, a.cond, s, j);
+    r.in = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n));
+    r.out = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
+    r.frame0 = (int)((r.in - reinterpret_cast<const float*>(a.in.data)) /
+                     ((int64_t)a.h * a.w * a.cin));
+  }
+  units[u] = r;
+}
+
+// A super-tile in two halves: the geometry and the (issued, not yet used)
+// load of its unit's spans, then the pointer arithmetic once the load is back
+// -- so the load latency overlaps a whole iteration of the caller.
+struct PendingTile {
+  UnitSpans u;
+  int f, oy0, ox0;
 };
 
 template <class Cfg>
-__device__ __forceinline__ SuperTile super_tile(const Cursor& c, const ConvRun& g,
-                                                const pb_conv_actor& a, const pb_resolved& res) {
-  const int n = pb::firing_iter(res, a.cond, c.s, c.j);
-  const int f = c.rem / g.per_frame, st = c.rem - f * g.per_frame;
-  const int sy = st / g.sx_n;
+__device__ __forceinline__ PendingTile pending_tile(const Cursor& c, const ConvRun& g,
+                                                    const UnitSpans* units) {
+  PendingTile p;
+  p.f = fdiv(c.rem, g.d_frame);
+  const int st = c.rem - p.f * g.per_frame;
+  const int sy = fdiv(st, g.d_sx);
+  p.oy0 = sy * kTH;
+  p.ox0 = (st - sy * g.sx_n) * (Cfg::ST * kTW);
+  p.u = units[c.unit];
+  return p;
+}
+
+__device__ __forceinline__ SuperTile finish_tile(const PendingTile& p, const ConvRun& g) {
   SuperTile t;
-  t.fin = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, c.s, n)) + f * g.in_frame;
-  t.fout = reinterpret_cast<float*>(pb::span_ptr(a.out, res, c.s, n)) + f * g.out_frame;
-  t.oy0 = sy * kTH;
-  t.ox0 = (st - sy * g.sx_n) * (Cfg::ST * kTW);
+  t.fin = p.u.in + p.f * g.in_frame;
+  t.fout = p.u.out + p.f * g.out_frame;
+  t.frame = p.u.frame0 + p.f;
+  t.oy0 = p.oy0;
+  t.ox0 = p.ox0;
+  t.pad_ = 0;
   return t;
 }
 
@@ -272,7 +385,7 @@ template <class Cfg>
 __device__ __forceinline__ void raw_issue(uint8_t* raw, uint64_t* bar, const CUtensorMap* tmap,
                                           const ConvRun& g, const pb_conv_actor& a,
                                           const SuperTile& t) {
-  const int frame = (int)((t.fin - reinterpret_cast<const float*>(a.in.data)) / g.in_frame);
+  const int frame = t.frame;
   mbar_arrive_tx(bar, Cfg::RAW_TX);
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
@@ -321,7 +434,8 @@ __device__ __forceinline__ void fill_patch(uint8_t* patch, const uint8_t* raw, c
     }
   } else {
     // entries from the raw box in shared memory (out-of-frame pixels are
-    // already zero)
+    // already zero); one entry per thread keeps the 16-byte stores of a warp
+    // on consecutive entries (conflict-free)
     constexpr int items = kPH * Cfg::PW;
     const float* rawf = reinterpret_cast<const float*>(raw) + (((t.ox0 - g.pad) * 3) & 3);
 #pragma unroll 1
@@ -368,7 +482,8 @@ __device__ __forceinline__ bool elect_one() {
 
 template <int MODE, int CIN>
 __global__ void __launch_bounds__(kConvThreads, 1)
-conv_pool_kernel(pb_conv_actor a, pb_resolved res, const __grid_constant__ CUtensorMap tmap) {
+conv_pool_kernel(pb_conv_actor a, pb_resolved res, const UnitSpans* __restrict__ units,
+                 const __grid_constant__ CUtensorMap tmap) {
   using Cfg = ConvCfg<MODE, CIN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>(
@@ -376,7 +491,7 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const __grid_constant__ CUten
   const ConvRun G = conv_run<Cfg>(a, res);
   uint8_t* wsm = base;                                   // [STEPS][2 KB]
   uint8_t* patch0 = base + Cfg::WBYTES;                  // [2][PATCH]
-  uint8_t* raw0 = patch0 + 2 * Cfg::PATCH;               // [kRawBufs][RAW] (layer 1)
+  uint8_t* raw0 = patch0 + Cfg::NB * Cfg::PATCH;         // [kRawBufs][RAW] (layer 1)
   ConvBars& B = *reinterpret_cast<ConvBars*>(base + Cfg::SMEM);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -386,6 +501,7 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const __grid_constant__ CUten
     uint4* dst = reinterpret_cast<uint4*>(wsm);
     for (int i = tid; i < Cfg::WBYTES / 16; i += kConvThreads) dst[i] = __ldg(src + i);
     if (tid < kCout) B.bias[tid] = __ldg(a.bias + tid);
+    for (int st = tid; st < res.n_streams; st += kConvThreads) B.cnt[st] = pb::cond_count(res, a.cond, st);
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -394,13 +510,19 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const __grid_constant__ CUten
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < Cfg::NB; ++b) {
       mbar_init(&B.full[b], kCvtThreads);
       mbar_init(&B.empty[b], 1);
-      mbar_init(&B.acc_full[b], 1);
+      // acc_full: the MMA completion (tcgen05.commit) and a plain release
+      // arrive of the MMA thread, which orders the descriptor it read
+      mbar_init(&B.acc_full[b], 2);
       mbar_init(&B.acc_empty[b], kEpiThreads);
     }
     for (int b = 0; b < kRawBufs; ++b) mbar_init(&B.raw_full[b], 1);
+    for (int k = 0; k < kSchedRing; ++k) {
+      mbar_init(&B.sched_full[k], 1);
+      mbar_init(&B.sched_empty[k], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -409,59 +531,114 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const __grid_constant__ CUten
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = B.tmem_base;
 
-  if (warp >= kCvtWarp0) {
+  if (warp == kSchedWarp) {
+    // ================================================ scheduler
+    // Walks this CTA's work list (the latency-bound cursor arithmetic and the
+    // unit-table loads, one super-tile ahead) and publishes one SuperTile per
+    // slot of a ring the converters consume; fout == nullptr ends the list.
+    const bool pon = lane == 0;
+    PROF_START();
+    Cursor c = cursor_first(G, B.cnt, res);
+    bool live = cursor_live(c, G, B.cnt, res);
+    PendingTile p_next{};
+    if (live) p_next = pending_tile<Cfg>(c, G, units);
+    for (int k = 0;; ++k) {
+      const int slot = k % kSchedRing;
+      mbar_wait(&B.sched_empty[slot], ((uint32_t)(k / kSchedRing) & 1) ^ 1);
+      SuperTile t{};
+      const bool more = live;
+      if (more) {
+        const PendingTile p = p_next;
+        cursor_step(c, G, B.cnt, res);
+        live = cursor_live(c, G, B.cnt, res);
+        if (live) p_next = pending_tile<Cfg>(c, G, units);
+        t = finish_tile(p, G);
+      }
+      if (lane == 0) {
+        B.sched[slot] = t;   // zero-initialised: fout == nullptr when !more
+        mbar_arrive(&B.sched_full[slot]);
+      }
+      __syncwarp();
+      PROF(pon, 15);
+      if (!more) break;
+    }
+  } else if (warp >= kCvtWarp0) {
     // ================================================ converters
     const int ct = tid - kCvtWarp0 * 32;
-    Cursor c = cursor_first(G, a, res);
-    Cursor pf = c;               // layer 1: raw-box prefetch cursor, 2 super-tiles ahead
-    int it = 0, pf_it = 0;
-    if constexpr (MODE == 0) {
-      for (int k = 0; k < kRawBufs - 1 && cursor_live(pf, G, a, res); ++k, ++pf_it) {
-        if (ct == 0)
-          raw_issue<Cfg>(raw0 + (pf_it % kRawBufs) * Cfg::RAW, &B.raw_full[pf_it % kRawBufs],
-                         &tmap, G, a, super_tile<Cfg>(pf, G, a, res));
-        cursor_step(pf, G, a, res);
+    constexpr int kRawIssuer = kCvtThreads - 32;   // layer 1: issues the raw-box TMA loads
+    const bool pon = ct == 0;
+    PROF_START();
+    bool raw_more = true;                          // (issuer) the list has not ended yet
+    auto issue_raw = [&](int k) {                  // raw box of super-tile k
+      if (ct != kRawIssuer || !raw_more) return;
+      mbar_wait(&B.sched_full[k % kSchedRing], (uint32_t)(k / kSchedRing) & 1);
+      const SuperTile tk = B.sched[k % kSchedRing];
+      if (tk.fout == nullptr) {
+        raw_more = false;
+        return;
       }
-    }
-    while (cursor_live(c, G, a, res)) {
-      const SuperTile t = super_tile<Cfg>(c, G, a, res);
-      const int b = it & 1;
-      const uint32_t use = (uint32_t)(it >> 1);
+      if (!(a.debug & 8))
+        raw_issue<Cfg>(raw0 + (k % kRawBufs) * Cfg::RAW, &B.raw_full[k % kRawBufs], &tmap, G, a, tk);
+    };
+    if constexpr (MODE == 0)
+      for (int k = 0; k < kRawBufs - 1; ++k) issue_raw(k);
+    for (int it = 0;; ++it) {
+      const int slot = it % kSchedRing;
+      const int b = it % Cfg::NB;
+      const uint32_t use = (uint32_t)(it / Cfg::NB);
+      mbar_wait(&B.sched_full[slot], (uint32_t)(it / kSchedRing) & 1);
+      const SuperTile t = B.sched[slot];
+      PROF(pon, 0);
+      if (t.fout == nullptr) {   // end of work: an empty descriptor through the normal handoff
+        mbar_wait(&B.empty[b], (use & 1) ^ 1);
+        if (ct == 0) B.desc[it % kDescRing].fout = nullptr;
+        mbar_arrive(&B.full[b]);
+        break;
+      }
       const int rb = it % kRawBufs;
-      cursor_step(c, G, a, res);
-      if constexpr (MODE == 0) mbar_wait(&B.raw_full[rb], (uint32_t)(it / kRawBufs) & 1);
+      if constexpr (MODE == 0)
+        if (!(a.debug & 8)) mbar_wait(&B.raw_full[rb], (uint32_t)(it / kRawBufs) & 1);
+      PROF(pon, 1);
       mbar_wait(&B.empty[b], (use & 1) ^ 1);
+      PROF(pon, 2);
       if (!(a.debug & 1)) fill_patch<MODE, CIN>(patch0 + b * Cfg::PATCH, raw0 + rb * Cfg::RAW, G, t, ct);
+      if (ct == 0) B.desc[it % kDescRing] = t;
+      PROF(pon, 3);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&B.full[b]);
-      if constexpr (MODE == 0) {
-        // every converter is done with raw[rb]: refill it with the super-tile
-        // kRawBufs - 1 ahead
-        asm volatile("bar.sync 2, %0;" ::"n"(kCvtThreads));
-        if (cursor_live(pf, G, a, res)) {
-          if (ct == 0)
-            raw_issue<Cfg>(raw0 + (pf_it % kRawBufs) * Cfg::RAW, &B.raw_full[pf_it % kRawBufs],
-                           &tmap, G, a, super_tile<Cfg>(pf, G, a, res));
-          cursor_step(pf, G, a, res);
-          ++pf_it;
-        }
-      }
-      ++it;
+      PROF(pon, 4);
+      // all converters are done with sched[slot] (and, layer 1, raw[rb])
+      asm volatile("bar.sync 2, %0;" ::"n"(kCvtThreads));
+      if (ct == 0) mbar_arrive(&B.sched_empty[slot]);
+      PROF(pon, 5);
+      if constexpr (MODE == 0) issue_raw(it + kRawBufs - 1);
+      PROF(pon, 6);
     }
   } else if (warp == kMmaWarp) {
     // ================================================ MMA issue (warp-uniform loop, one lane issues)
     constexpr uint32_t id64 = idesc_bf16(64), id32 = idesc_bf16(32);
     const uint64_t db0 = sdesc(smem_u32(wsm), 128, 256);
-    Cursor c = cursor_first(G, a, res);
-    int it = 0;
-    while (cursor_live(c, G, a, res)) {
-      const int b = it & 1;
-      const uint32_t use = (uint32_t)(it >> 1);
-      const int st = c.rem % G.per_frame;
-      const int ox0 = (st % G.sx_n) * (Cfg::ST * kTW);
-      cursor_step(c, G, a, res);
+    const bool pon = lane == 0;
+    PROF_START();
+    for (int it = 0;; ++it) {
+      const int b = it % Cfg::NB;
+      const uint32_t use = (uint32_t)(it / Cfg::NB);
       mbar_wait(&B.full[b], use & 1);
+      PROF(pon, 8);
+      const SuperTile& t = B.desc[it % kDescRing];
+      if (t.fout == nullptr) {   // end of work: let the epilogue see it too
+        mbar_wait(&B.acc_empty[b], (use & 1) ^ 1);
+        if (elect_one()) {
+          mma_commit(&B.acc_full[b]);
+          mbar_arrive(&B.acc_full[b]);
+        }
+        __syncwarp();
+        break;
+      }
+      const int ox0 = t.ox0;
+      PROF(pon, 7);
       mbar_wait(&B.acc_empty[b], (use & 1) ^ 1);
+      PROF(pon, 9);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint64_t da0 = sdesc(smem_u32(patch0 + b * Cfg::PATCH), Cfg::PS, Cfg::PW * 16);
       if (elect_one()) {
@@ -486,40 +663,57 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const __grid_constant__ CUten
         }
         mma_commit(&B.empty[b]);
         mma_commit(&B.acc_full[b]);
+        mbar_arrive(&B.acc_full[b]);
       }
       __syncwarp();
-      ++it;
+      PROF(pon, 10);
     }
   } else {
     // ================================================ epilogue (warps 0-7)
     // warp w reads TMEM lanes 32*(w%4).. of the tiles t = w/4, w/4 + 2, ...
     const int q = warp & 3, h = warp >> 2;
     const int gr = q * 4 + (lane >> 3), x = lane & 7;   // tile row / column of this lane
-    Cursor c = cursor_first(G, a, res);
-    int it = 0;
-    while (cursor_live(c, G, a, res)) {
-      const SuperTile t = super_tile<Cfg>(c, G, a, res);
-      const int b = it & 1;
-      const uint32_t use = (uint32_t)(it >> 1);
-      cursor_step(c, G, a, res);
+    const bool pon = tid == 0;
+    PROF_START();
+    for (int it = 0;; ++it) {
+      const int b = it % Cfg::NB;
+      const uint32_t use = (uint32_t)(it / Cfg::NB);
       mbar_wait(&B.acc_full[b], use & 1);
+      PROF(pon, 12);
+      const SuperTile t = B.desc[it % kDescRing];
+      if (t.fout == nullptr) break;
+      PROF(pon, 11);
       asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll 1
-      for (int tt = h; tt < Cfg::ST; tt += 2) {
-        if (t.ox0 + tt * kTW >= G.Wo || (a.debug & 2)) break;
-        const uint32_t taddr =
-            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((b * Cfg::ST + tt) * Cfg::ACC);
-        float v[32];
-        tmem_ld32(taddr, v);
-        if constexpr (!Cfg::SPLIT3) {
-          float v1[32];
-          tmem_ld32(taddr + 32, v1);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      // all of this warp's tiles leave TMEM first (one wait), so the
+      // accumulator set is released before the pooling math
+      constexpr int TPW = Cfg::ST / 2;        // tiles per warp
+      float v[TPW][32];
+      bool ok[TPW];
 #pragma unroll
-          for (int ch = 0; ch < 32; ++ch) v[ch] = __fadd_rn(v[ch], v1[ch]);
-        } else {
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int u = 0; u < TPW; ++u) {
+        const int tt = h + 2 * u;
+        ok[u] = t.ox0 + tt * kTW < G.Wo && !(a.debug & 2);
+        if (ok[u]) {
+          const uint32_t taddr =
+              tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((b * Cfg::ST + tt) * Cfg::ACC);
+          tmem_ld32(taddr, v[u]);
+          if constexpr (!Cfg::SPLIT3) {
+            float v1[32];
+            tmem_ld32(taddr + 32, v1);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int ch = 0; ch < 32; ++ch) v[u][ch] = __fadd_rn(v[u][ch], v1[ch]);
+          }
         }
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&B.acc_empty[b]);
+      PROF(pon, 13);
+#pragma unroll
+      for (int u = 0; u < TPW; ++u) {
+        if (!ok[u]) continue;
+        const int tt = h + 2 * u;
         // 2x2 max pool before bias + ReLU (both monotone, bias is per channel),
         // as a halving butterfly: after the x-pair step a lane keeps 16
         // channels, after the row-pair step 8, and all four lanes of a window
@@ -528,8 +722,8 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const __grid_constant__ CUten
         float h16[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float send = xodd ? v[i] : v[16 + i];
-          const float keep = xodd ? v[16 + i] : v[i];
+          const float send = xodd ? v[u][i] : v[u][16 + i];
+          const float keep = xodd ? v[u][16 + i] : v[u][i];
           h16[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 1));
         }
         float h8[8];
@@ -550,9 +744,7 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const __grid_constant__ CUten
           dst[1] = make_float4(h8[4], h8[5], h8[6], h8[7]);
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(&B.acc_empty[b]);
-      ++it;
+      PROF(pon, 14);
     }
   }
 
@@ -594,6 +786,8 @@ int launch_conv(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t
   const int64_t per_frame = (int64_t)((Ho + kTH - 1) / kTH) * ((Wo + Cfg::ST * kTW - 1) / (Cfg::ST * kTW));
   const int64_t total = per_frame * actor.frames * res.n_streams * res.n_iter;
   if (total >= (int64_t)1 << 31) return pb::fail(PB_E_UNSUPPORTED, "conv: too many tiles per launch");
+  if (res.n_streams > kMaxStreams)
+    return pb::fail(PB_E_UNSUPPORTED, "conv: more than 1024 streams per launch");
   const int grid = (int)std::min<int64_t>(total, sms);
   if (grid == 0) return PB_OK;
   CUtensorMap tmap{};
@@ -615,7 +809,17 @@ int launch_conv(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t
                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return pb::fail(PB_E_CUDA, "conv: cuTensorMapEncodeTiled failed");
   }
-  conv_pool_kernel<MODE, CIN><<<grid, kConvThreads, smem, st>>>(actor, res, tmap);
+  static UnitSpans* units = nullptr;
+  static int64_t units_n = 0;
+  const int64_t n_units = (int64_t)res.n_streams * res.n_iter;
+  if (n_units > units_n) {
+    if (units) PB_CUDA(cudaFree(units));
+    PB_CUDA(cudaMalloc(&units, sizeof(UnitSpans) * n_units));
+    units_n = n_units;
+  }
+  conv_units_kernel<<<(unsigned)((n_units + 255) / 256), 256, 0, st>>>(actor, res, units);
+  PB_LAUNCHED("conv_units_kernel");
+  conv_pool_kernel<MODE, CIN><<<grid, kConvThreads, smem, st>>>(actor, res, units, tmap);
   PB_LAUNCHED("conv_pool_kernel");
   return PB_OK;
 }
@@ -867,6 +1071,15 @@ __global__ void classify_kernel(pb_classify_actor a, pb_resolved res) {
 }  // namespace
 
 extern "C" {
+
+int pb_conv_debug_counters(unsigned long long* out, int reset) {
+  PB_CUDA(cudaMemcpyFromSymbol(out, g_conv_prof, sizeof(g_conv_prof)));
+  if (reset) {
+    static unsigned long long zero[kProfCtas][kProfSlots] = {};
+    PB_CUDA(cudaMemcpyToSymbol(g_conv_prof, zero, sizeof(zero)));
+  }
+  return PB_OK;
+}
 
 int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream) {
   if (res.n_iter == 0) return PB_OK;

@@ -226,6 +226,74 @@ static void run_tput3(const char* name, uint32_t aoff, uint32_t lbo, uint32_t sb
   cudaFree(cyc);
 }
 
+
+// 1d. the layer-1 conv MMA stream: per super-tile 4 tiles x 5 K-steps x 3
+// N=32 MMAs (xh*wh, xl*wh, xh*wl), A from the planar entry patch
+// (LBO = plane stride 10240 B, SBO = 512 B), B 2 KB per step; one commit per
+// super-tile, 3 accumulator sets in flight.  mode 1: every A at one address.
+__global__ void tput4(int supertiles, int mode, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar[3];
+  __shared__ uint32_t tslot;
+  for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.f;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if ((threadIdx.x >> 5) == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 3; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tslot;
+  if (threadIdx.x < 32) {
+    const uint32_t id = idesc(1, 128, 32);
+    const uint32_t wbase = smem_u32(sm), pbase = smem_u32(sm + 16384);
+    const uint64_t db0 = sdesc(wbase, 128, 256);
+    uint32_t ph[3] = {0, 0, 0};
+    long long t0 = clock64();
+    for (int it = 0; it < supertiles; ++it) {
+      const int b = it % 3;
+      if (it >= 3) {   // accumulator set b was committed 3 super-tiles ago
+        asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(smem_u32(&bar[b])), "r"(ph[b]) : "memory");
+        ph[b] ^= 1;
+      }
+      const uint64_t da0 = sdesc(pbase + (b % 2) * 40960, 10240, 512);
+      uint32_t e;
+      asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(e));
+      if (e) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const uint32_t d = tmem + (uint32_t)((b * 4 + t) * 32);
+#pragma unroll
+          for (int s = 0; s < 5; ++s) {
+            const uint64_t dah = mode ? da0 : da0 + (uint64_t)((s * 512 + t * 128) >> 4);
+            const uint64_t dal = mode ? da0 : dah + (uint64_t)((2 * 10240) >> 4);
+            const uint64_t dbs = db0 + (uint64_t)(s * 128);
+            asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, %4;" ::"r"(d), "l"(dah), "l"(dbs), "r"(id), "n"(0));
+            asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;" ::"r"(d), "l"(dal), "l"(dbs), "r"(id));
+            asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;" ::"r"(d), "l"(dah), "l"(dbs + 64), "r"(id));
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar[b])) : "memory");
+      }
+      __syncwarp();
+    }
+    for (int b = 0; b < 3 && b < supertiles; ++b) {
+      asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(smem_u32(&bar[b])), "r"(ph[b]) : "memory");
+    }
+    long long t1 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // ------------------------------------------------- 2. shifted-window layouts
 // mode 0 (planar, tf32): P[cb][pix][4 f32], npix pixels, 8 planes (32 ch);
 //   D[r][o] = sum_shift sum_ci P[ci][shift + r] * W[shift][o][ci]
@@ -402,7 +470,7 @@ int main() {
              kind == 0 ? "tf32" : "bf16", n, (double)c / iters, flops / (ms * 1e-3) / 1e12);
     }
   const char* only = getenv("PROBE_ONLY");
-  if (!only || strcmp(only, "layout")) {
+  if (!only || (strcmp(only, "layout") && strcmp(only, "conv1"))) {
   run_tput2<0, 32>(); run_tput2<0, 64>(); run_tput2<0, 128>(); run_tput2<0, 256>();
   run_tput2<1, 32>(); run_tput2<1, 64>(); run_tput2<1, 128>(); run_tput2<1, 256>();
   }
@@ -422,6 +490,19 @@ int main() {
     }
   }
   if (only && !strcmp(only, "layout")) return 0;
+  if (only && !strcmp(only, "conv1")) {
+    long long* cyc;
+    CK(cudaMalloc(&cyc, 8));
+    CK(cudaFuncSetAttribute(tput4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (int mode = 0; mode < 2; ++mode) {
+      tput4<<<148, 128, 200 * 1024>>>(2000, mode, cyc);
+      CK(cudaDeviceSynchronize());
+      long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+      printf("{\"probe\": \"conv1_stream\", \"mode\": %d, \"cyc_per_mma\": %.2f, \"cyc_per_supertile\": %.1f}\n",
+             mode, (double)c / (2000.0 * 60), (double)c / 2000.0);
+    }
+    return 0;
+  }
   for (int mode = 0; mode < 3; ++mode) run_window(mode);
   return 0;
 }
