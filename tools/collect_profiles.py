@@ -15,8 +15,8 @@ out = ROOT / "gpurun_out"
 prof = ROOT / "profiles"
 
 
-def launches():
-    rows = [r for r in csv.reader(open(out / f"{R}_launches.csv")) if len(r) > 10]
+def launches(name=f"{R}_launches.csv"):
+    rows = [r for r in csv.reader(open(out / name)) if len(r) > 10]
     h = rows[0]
     iK, iM, iV, iI = (h.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
     d = {}
@@ -29,6 +29,13 @@ def launches():
 
 
 L = launches()
+LC = launches(f"{R}_launches_cnn.csv") if (out / f"{R}_launches_cnn.csv").exists() else []
+(prof / f"{R}_launches_cnn.json").write_text(json.dumps({
+    "command": "tools/profile_round.sh: ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+               "dram__bytes_write.sum --clock-control none -c 60 python tools/cnn_bench.py 4 64 24 2",
+    "note": "CNN vision graph, 4 streams x 64 firings x 24 frames per launch; cold-cache and "
+            "serialised under ncu: compare shares, not absolutes; units ns and bytes",
+    "launches": LC}, indent=1))
 (prof / f"{R}_launches.json").write_text(json.dumps({
     "command": "tools/profile_round.sh: ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
                "dram__bytes_write.sum --clock-control none -c 80 python bench.py --steps 2 "
@@ -40,7 +47,7 @@ traffic = {}
 
 
 def last(kname):
-    xs = [x for x in L if kname in x["kernel"]]
+    xs = [x for x in L + LC if kname in x["kernel"]]
     return xs[-1] if xs else None
 
 

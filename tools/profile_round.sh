@@ -8,6 +8,9 @@ B="python bench.py --steps 2 --warmup 3 --skip-cpu --e2e-steps 0 --cnn-steps 1 -
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 80 --csv \
   --log-file gpurun_out/${R}_launches.csv $B > /dev/null 2>&1
 echo "launches: $?"
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv \
+  --log-file gpurun_out/${R}_launches_cnn.csv python tools/cnn_bench.py 4 64 24 2 > /dev/null 2>&1
+echo "launches cnn: $?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:bank_ -c 2 \
   -o gpurun_out/${R}_merged $B --skip-cnn > /dev/null 2>&1; echo "merged: $?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fir_persistent -c 1 \
