@@ -188,9 +188,12 @@ int pb_rings_advance(const pb_ring_advance_t* rings /* host array */, int n_ring
 /* --------------------------------------------------------- span addressing */
 /* Where the span of a port lives for firing at iteration n of stream s:
  *   idx   = index_cond < 0 ? n : prefix[index_cond][s][n]
- *   chunk = (base[s] + idx) % slots     (base NULL -> 0)
+ *   chunk = (base[s] + idx + offset) % slots     (base NULL -> 0)
  *   ptr   = data + s*stream_stride + chunk*span_bytes
- * act_cond is the condition gating the port (-1: always active). */
+ * act_cond is the condition gating the port (-1: always active).  offset is
+ * the producer side of a FIFO with initial delay tokens: delay / rate chunks
+ * (fifos.py:87-98 aligned plan; the consumer side uses 0 and first reads the
+ * delay payload). */
 typedef struct {
   uint8_t* data;
   int64_t stream_stride;
@@ -199,7 +202,7 @@ typedef struct {
   int32_t slots;
   int32_t index_cond;
   int32_t act_cond;
-  int32_t pad_;
+  int32_t offset;
 } pb_span_ref;
 
 /* ------------------------------------------------------------- actor kernels */
@@ -298,6 +301,29 @@ typedef struct {
   int32_t* error_flag;
 } pb_path_merge_actor;
 int pb_fire_path_merge(pb_path_merge_actor actor, pb_resolved res, void* stream);
+
+/* ------------------------------------------- image actors (motion detection) */
+/* apps/motion.py:29-71: 8-bit side x side frames, integer arithmetic, bit-exact.
+ *   PB_IMG_BLUR   gauss_blur: separable 5x5 binomial (1 4 6 4 1), >> 8, the
+ *                 2-pixel border passes through; in[0] -> every out[k]
+ *   PB_IMG_DIFF   frame_diff_threshold: |in[0] - in[1]| > threshold ? 255 : 0
+ *                 (in[0] = "cur", in[1] = "prev")
+ *   PB_IMG_MEDIAN plus_median: median of the pixel and its 4-neighbourhood, the
+ *                 1-pixel border passes through */
+#define PB_IMG_BLUR 0
+#define PB_IMG_DIFF 1
+#define PB_IMG_MEDIAN 2
+typedef struct {
+  pb_span_ref in[2];
+  pb_span_ref out[PB_MAX_PORTS];
+  int32_t n_out;
+  int32_t op;
+  int32_t side;
+  int32_t threshold;
+  int32_t cond;
+  int32_t pad_;
+} pb_image_actor;
+int pb_fire_image(pb_image_actor actor, pb_resolved res, void* stream);
 
 /* ------------------------------------------------ CNN actors (vision example) */
 /* The paper's adaptive DNN is not in the reference

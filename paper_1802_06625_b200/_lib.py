@@ -68,7 +68,7 @@ class RingAdvance(C.Structure):
 
 class SpanRef(C.Structure):
     _fields_ = [("data", vp), ("stream_stride", i64), ("span_bytes", i64), ("base", vp),
-                ("slots", i32), ("index_cond", i32), ("act_cond", i32), ("pad_", i32)]
+                ("slots", i32), ("index_cond", i32), ("act_cond", i32), ("offset", i32)]
 
 
 class FirActor(C.Structure):
@@ -98,6 +98,14 @@ class PathMergeActor(C.Structure):
     _fields_ = [("in_", SpanRef * PB_MAX_PORTS), ("out", SpanRef), ("n_in", i32),
                 ("bypass_index", i32), ("marker", C.c_float), ("cond", i32),
                 ("error_flag", vp)]
+
+
+class ImageActor(C.Structure):
+    _fields_ = [("in_", SpanRef * 2), ("out", SpanRef * PB_MAX_PORTS), ("n_out", i32),
+                ("op", i32), ("side", i32), ("threshold", i32), ("cond", i32), ("pad_", i32)]
+
+
+PB_IMG_BLUR, PB_IMG_DIFF, PB_IMG_MEDIAN = 0, 1, 2
 
 
 class ConvActor(C.Structure):
@@ -171,6 +179,7 @@ SIGNATURES = {
     "pb_fire_bytes": (C.c_int, [BytesActor, Resolved, vp]),
     "pb_fire_matmul": (C.c_int, [MatmulActor, Resolved, vp]),
     "pb_fire_path_merge": (C.c_int, [PathMergeActor, Resolved, vp]),
+    "pb_fire_image": (C.c_int, [ImageActor, Resolved, vp]),
     "pb_fire_conv_pool": (C.c_int, [ConvActor, Resolved, vp]),
     "pb_conv_debug_counters": (C.c_int, [vp, C.c_int]),
     "pb_fire_dense": (C.c_int, [DenseActor, Resolved, vp]),

@@ -45,7 +45,7 @@ __device__ __forceinline__ int64_t span_index(const pb_span_ref& r, const pb_res
   if (r.index_cond >= 0)
     idx = res.prefix[((int64_t)r.index_cond * res.n_streams + s) * res.cap + n];
   int64_t b = r.base ? r.base[s] : 0;
-  return (b + idx) % r.slots;
+  return (b + idx + r.offset) % r.slots;
 }
 
 __device__ __forceinline__ uint8_t* span_ptr(const pb_span_ref& r, const pb_resolved& res,

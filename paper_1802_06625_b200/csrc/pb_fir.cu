@@ -168,7 +168,7 @@ __device__ __forceinline__ const uint8_t* span_ptr_b(const pb_span_ref& r, int64
   int64_t idx = n;
   if (r.index_cond >= 0)
     idx = res.prefix[((int64_t)r.index_cond * res.n_streams + s) * res.cap + n];
-  return r.data + (int64_t)s * r.stream_stride + ((base + idx) % r.slots) * r.span_bytes;
+  return r.data + (int64_t)s * r.stream_stride + ((base + idx + r.offset) % r.slots) * r.span_bytes;
 }
 
 // ------------------------------------------------------------- FIR math

@@ -103,9 +103,13 @@ class _Dev:
         arr = np.ctypeslib.as_array((C.c_uint8 * max(16, int(nbytes))).from_address(p.value))
         return p.value, arr[:int(nbytes)]
 
-    def ring(self, rate: int, tb: int, factor: int, n_streams: int):
+    def ring(self, rate: int, tb: int, factor: int, n_streams: int, delay: int = 0,
+             payload: bytes | None = None):
         r = C.c_void_p()
-        _lib.check(self.lib.pb_ring_create(rate, tb, 0, factor, n_streams, None, C.byref(r)),
+        pay = None
+        if payload is not None:
+            pay = (C.c_uint8 * len(payload)).from_buffer_copy(payload)
+        _lib.check(self.lib.pb_ring_create(rate, tb, delay, factor, n_streams, pay, C.byref(r)),
                    "pb_ring_create")
         self.rings.append(r.value)
         data, stride, ctr = C.c_void_p(), C.c_int64(), C.c_void_p()
@@ -240,6 +244,7 @@ class DeviceRuntime:
 
         self.counters: dict[str, int] = {}
         self.storage: dict[str, _Storage] = {}
+        self.delay_chunks: dict[str, int] = {}   # FIFOs with initial delay tokens
         route_alias: dict[str, str] = {}
         for a in g.actors:
             b = self.behaviors[0][a.id]
@@ -261,6 +266,18 @@ class DeviceRuntime:
                 first = None
                 for f in fifos:
                     span = f.rate * f.token_bytes
+                    if f.delay:
+                        # own ring, delay/rate chunks longer; the producer writes
+                        # that many chunks ahead (pb_span_ref.offset) and the
+                        # consumer first reads the delay payload (fifos.py:155-161)
+                        d = f.delay // f.rate
+                        _, data, stride, ctr = m.ring(f.rate, f.token_bytes, C_ + d, S,
+                                                      delay=f.delay, payload=f.delay_payload)
+                        self.counters[f.id] = ctr
+                        self.storage[f.id] = _Storage(data, stride, span, C_ + d, ctr,
+                                                      plan.fifo_cond[f.id], f.id)
+                        self.delay_chunks[f.id] = d
+                        continue
                     if f.id in self.virtual:
                         self.counters[f.id] = m.malloc(8 * 4 * S)
                         continue
@@ -332,17 +349,34 @@ class DeviceRuntime:
 
     # ------------------------------------------------------------ span refs
 
-    def _ref(self, fid: str) -> _lib.SpanRef:
+    def _ref(self, fid: str, producer: bool = False) -> _lib.SpanRef:
+        """Span addressing of a FIFO; the producer side of a FIFO with initial
+        delay tokens writes delay/rate chunks ahead of its consumer."""
         st = self.storage[fid]
+        off = self.delay_chunks.get(fid, 0) if producer else 0
         return _lib.SpanRef(st.data, st.stream_stride, st.span, st.base, st.slots,
-                            st.index_cond, self.plan.fifo_cond[fid], 0)
+                            st.index_cond, self.plan.fifo_cond[fid], off)
+
+    def _port_targets(self, aid: str, port: str) -> list[str]:
+        """The FIFOs an output port must write: one per distinct storage (a
+        broadcast of equal spans aliases the first; delayed FIFOs have their
+        own ring)."""
+        fifos = sorted(self.graph.fifos_from(PortRef(aid, port)), key=lambda f: f.id)
+        seen, out = set(), []
+        for f in fifos:
+            o = self.storage[f.id].owner if f.id in self.storage else f.id
+            key = (o, self.delay_chunks.get(f.id, 0))
+            if key not in seen:
+                seen.add(key)
+                out.append(f.id)
+        return out
 
     def _resolved(self, n_iter: int) -> _lib.Resolved:
         return _lib.Resolved(self.res_act, self.res_prefix, self.res_count, self.res_wl,
                              len(self.plan.conds), self.n_streams, n_iter, self.cap)
 
     def _fir_actor(self, aid: str, in_fid: str, out_fid: str | None) -> _lib.FirActor:
-        out = self._ref(out_fid) if out_fid is not None else _lib.SpanRef()
+        out = self._ref(out_fid, producer=True) if out_fid is not None else _lib.SpanRef()
         return _lib.FirActor(self._ref(in_fid), out, self.fir_taps[aid], self.fir_state[aid],
                              self.plan.actor_cond[aid], 0)
 
@@ -421,6 +455,12 @@ class DeviceRuntime:
             in_f = [g.fifo_into(PortRef(aid, p.id)).id for p in ins]
             out_f = [sorted(g.fifos_from(PortRef(aid, p.id)), key=lambda f: f.id)[0].id
                      for p in outs]
+            targets = {p.id: self._port_targets(aid, p.id) for p in outs}
+            if kind not in ("image", "bytes", "route") and \
+                    any(len(t) > 1 for t in targets.values()):
+                raise UnsupportedGraph(f"{aid}: an output port broadcasts to a delayed and an "
+                                       f"undelayed channel; only image and byte actors write "
+                                       f"both")
             if kind == "route":
                 if all(self.storage[f].owner == self.storage[in_f[0]].owner for f in out_f):
                     done.add(aid)          # aliased: no bytes move
@@ -433,7 +473,7 @@ class DeviceRuntime:
                 for k, fid in enumerate(in_f):
                     act.in_[k] = self._ref(fid)
                 act.n_in = len(in_f)
-                act.out = self._ref(out_f[0])
+                act.out = self._ref(out_f[0], producer=True)
                 act.cond = plan.actor_cond[aid]
                 f0 = g.fifo(out_f[0])
                 self.launches.append(("sum", act, f0.rate * f0.token_bytes // 8))
@@ -441,9 +481,12 @@ class DeviceRuntime:
                 act = _lib.BytesActor()
                 for k, fid in enumerate(in_f):
                     act.in_[k] = self._ref(fid)
-                for k, fid in enumerate(out_f):
-                    act.out[k] = self._ref(fid)
-                act.n_in, act.n_out = len(in_f), len(out_f)
+                outs_all = [fid for p in outs for fid in targets[p.id]]
+                if len(outs_all) > _lib.PB_MAX_PORTS or len(in_f) > _lib.PB_MAX_PORTS:
+                    raise UnsupportedGraph(f"{aid}: more than {_lib.PB_MAX_PORTS} ports")
+                for k, fid in enumerate(outs_all):
+                    act.out[k] = self._ref(fid, producer=True)
+                act.n_in, act.n_out = len(in_f), len(outs_all)
                 act.offset = int(a.params.get("offset", 0)) if b.registered_name == "add_mod" \
                     else 0
                 act.cond = plan.actor_cond[aid]
@@ -451,7 +494,7 @@ class DeviceRuntime:
             elif kind == "matmul":
                 w = np.array(a.params["w"], dtype=np.float32)
                 n = int(round(len(w) ** 0.5))
-                act = _lib.MatmulActor(self._ref(in_f[0]), self._ref(out_f[0]),
+                act = _lib.MatmulActor(self._ref(in_f[0]), self._ref(out_f[0], producer=True),
                                        self.mem.upload(w), n, plan.actor_cond[aid])
                 self.launches.append(("matmul", act))
             elif kind == "path_merge":
@@ -465,15 +508,44 @@ class DeviceRuntime:
                 act.marker = float(np.float32(a.params.get("marker", 0.5)))
                 act.cond = plan.actor_cond[aid]
                 act.error_flag = self.err_flag
-                act.out = self._ref(out_f[0])
+                act.out = self._ref(out_f[0], producer=True)
                 self.launches.append(("path_merge", act, aid))
+            elif kind == "image":
+                act = _lib.ImageActor()
+                names = [p.id for p in ins]
+                if b.op == _lib.PB_IMG_DIFF:
+                    if set(names) != {"cur", "prev"}:
+                        raise UnsupportedGraph(f"{aid}: frame_diff_threshold needs ports cur/prev")
+                    order = [in_f[names.index("cur")], in_f[names.index("prev")]]
+                else:
+                    if len(in_f) != 1:
+                        raise UnsupportedGraph(f"{aid}: one data input expected")
+                    order = in_f
+                for k, fid in enumerate(order):
+                    act.in_[k] = self._ref(fid)
+                outs_all = [fid for p in outs for fid in targets[p.id]]
+                if len(outs_all) > _lib.PB_MAX_PORTS:
+                    raise UnsupportedGraph(f"{aid}: more than {_lib.PB_MAX_PORTS} outputs")
+                for k, fid in enumerate(outs_all):
+                    act.out[k] = self._ref(fid, producer=True)
+                act.n_out = len(outs_all)
+                tb = g.fifo(in_f[0]).token_bytes * g.fifo(in_f[0]).rate
+                side = int(round(tb ** 0.5))
+                if side * side != tb or any(g.fifo(f).rate * g.fifo(f).token_bytes != tb
+                                            for f in in_f + outs_all):
+                    raise UnsupportedGraph(f"{aid}: image actors take square 8-bit frames of "
+                                           "one size on every port")
+                act.op, act.side = b.op, side
+                act.threshold = int(a.params.get("threshold", 16))
+                act.cond = plan.actor_cond[aid]
+                self.launches.append(("image", act))
             elif kind == "conv":
                 from .cnn_weights import conv_device_layout
                 b.init(aid, a.params, None)
                 fi = g.fifo(in_f[0])
                 if fi.token_bytes != b.h * b.w * b.cin * 4:
                     raise UnsupportedGraph(f"{aid}: token is not one {b.h}x{b.w}x{b.cin} frame")
-                act = _lib.ConvActor(self._ref(in_f[0]), self._ref(out_f[0]),
+                act = _lib.ConvActor(self._ref(in_f[0]), self._ref(out_f[0], producer=True),
                                      self.mem.upload(conv_device_layout(b.weights, b.cin)),
                                      self.mem.upload(b.bias), fi.rate, b.h, b.w, b.cin,
                                      b.cout, b.pad, plan.actor_cond[aid], 0)
@@ -482,7 +554,7 @@ class DeviceRuntime:
                 b.init(aid, a.params, None)
                 fi = g.fifo(in_f[0])
                 from .cnn_weights import dense_device_layout
-                act = _lib.DenseActor(self._ref(in_f[0]), self._ref(out_f[0]),
+                act = _lib.DenseActor(self._ref(in_f[0]), self._ref(out_f[0], producer=True),
                                       self.mem.upload(dense_device_layout(b.weights)),
                                       self.mem.upload(b.bias),
                                       fi.rate, b.nin, b.nout, plan.actor_cond[aid])
@@ -496,7 +568,7 @@ class DeviceRuntime:
                 chain_f = in_f[1 - names.index(bypass)]
                 bypass_f = in_f[names.index(bypass)]
                 act = _lib.ClassifyActor(
-                    self._ref(chain_f), self._ref(bypass_f), self._ref(out_f[0]),
+                    self._ref(chain_f), self._ref(bypass_f), self._ref(out_f[0], producer=True),
                     self.mem.upload(b.w4), self.mem.upload(b.b4), self.mem.upload(b.w5),
                     self.mem.upload(b.b5), g.fifo(out_f[0]).rate, b.nin, b.nhid, b.nout,
                     float(np.float32(a.params.get("marker", -1.0))), plan.actor_cond[aid],
@@ -707,6 +779,8 @@ class DeviceRuntime:
                 _lib.check(lib.pb_fire_matmul(item[1], res, st), "matmul")
             elif kind == "path_merge":
                 _lib.check(lib.pb_fire_path_merge(item[1], res, st), "path_merge")
+            elif kind == "image":
+                _lib.check(lib.pb_fire_image(item[1], res, st), "image")
             elif kind == "conv":
                 _lib.check(lib.pb_fire_conv_pool(item[1], res, st), "conv2d_relu_pool")
             elif kind == "dense":

@@ -14,17 +14,18 @@ exactly one condition or by none ("always").  Propagation goes
 
 A FIFO whose two ends disagree is exactly a graph whose token counts cannot
 balance per iteration (analysis.py:264-319 rejects those too), so admission
-raises InconsistentGraph.  The executor covers acyclic, delay-free graphs
-whose dynamic regions are not nested, with configuration actors that have no
-data inputs (every shipped app except motion detection, whose one-frame delay
-FIFO is listed as next work in DESIGN.md); anything else raises
-UnsupportedGraph rather than running incorrectly.
+raises InconsistentGraph.  The executor covers acyclic graphs whose dynamic
+regions are not nested, with configuration actors that have no data inputs
+and initial delay tokens only on aligned, always-active channels between
+device actors (every shipped app: the motion app's one-frame delay is such a
+channel); anything else raises UnsupportedGraph rather than running
+incorrectly.
 
 Per iteration n every "always" actor fires once and every gated actor fires
 iff its condition is true at n, which is the firing sequence both reference
 engines produce (interp.py:126-148 is the oracle's version of the rule).
-Buffer bounds follow compute_bounds (analysis.py:398-411): for a delay-free
-rate-r FIFO the per-period bound is r, so beta = r + (C-1)*r.
+Buffer bounds follow compute_bounds (analysis.py:398-411): beta = delay + r +
+(C-1)*r for a rate-r FIFO.
 """
 from __future__ import annotations
 
@@ -157,9 +158,6 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
                              f"different delays {sorted(delays)}")
         elif delays != {0}:
             unsupported.append(f"control channels of {ctl} carry initial delay tokens")
-    for fid in data_fifos:
-        if g.fifo(fid).delay:
-            unsupported.append(f"fifo {fid} carries {g.fifo(fid).delay} initial delay tokens")
 
     # propagate conditions through static actors
     def pc(ref: PortRef) -> int | None:
@@ -203,6 +201,20 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
         fifo_cond[fid] = cs
     for fid in control_fifos:
         fifo_cond[fid] = ALWAYS
+    # initial delay tokens on data FIFOs: supported between two device actors
+    # on an always-active, aligned channel (fifos.py:87-92; the producer
+    # writes delay/rate chunks ahead of the consumer)
+    for fid in data_fifos:
+        f = g.fifo(fid)
+        if not f.delay:
+            continue
+        if f.delay % f.rate:
+            unsupported.append(f"fifo {fid}: {f.delay} delay tokens are not a multiple of its "
+                               f"rate {f.rate}")
+        elif fifo_cond[fid] != ALWAYS:
+            unsupported.append(f"fifo {fid}: delay tokens on a dynamically gated channel")
+        elif roles[f.src.actor] != "device" or roles[f.dst.actor] != "device":
+            unsupported.append(f"fifo {fid}: delay tokens between host actors")
 
     # topological order over data FIFOs (delay-free cycles deadlock)
     indeg = {a.id: 0 for a in g.actors}
@@ -228,6 +240,20 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
             unsupported.append(f"cycle through {stuck} (delay tokens)")
         else:
             _problem(report, f"DeadlockError: zero-delay cycle through {stuck}")
+
+    # every actor must fire exactly once per source firing: a consumer whose
+    # inputs all carry delay tokens would keep firing on them after the sources
+    # are exhausted (the reference drains them), which the batched iteration
+    # schedule does not model
+    if len(order) == len(g.actors):
+        extra: dict[str, int] = {}
+        for aid in order:
+            ins = [g.fifo(fid) for fid in data_fifos if g.fifo(fid).dst.actor == aid]
+            extra[aid] = min((extra[f.src.actor] + f.delay // f.rate for f in ins), default=0)
+            if extra[aid] > 0:
+                unsupported.append(f"actor {aid} would fire {extra[aid]} more times than the "
+                                   "sources on its inputs' delay tokens (drain phase)")
+                break
 
     if not report.consistent:
         raise InconsistentGraph(report)

@@ -37,8 +37,9 @@ def golden():
     import numpy as np
 
     out = {}
-    for name in ("dpd", "fixtures", "bypass", "policies"):
+    for name in ("dpd", "fixtures", "bypass", "policies", "motion"):
         out[name] = json.loads((GOLDEN / f"{name}.json").read_text())
     out["dpd_small"] = dict(np.load(GOLDEN / "dpd_small.npz"))
     out["bypass_small"] = dict(np.load(GOLDEN / "bypass_small.npz"))
+    out["motion_small"] = dict(np.load(GOLDEN / "motion_small.npz"))
     return out

@@ -13,6 +13,9 @@ Outputs (all small):
                    conformance fixtures (pkg/tests/fixtures.py)
   bypass.json      bypass app digests; bypass_small.npz sink bytes
   policies.json    control sequences of the four policies for several seeds
+  motion.json      motion app (one-frame delay FIFO): sink digests and firing
+                   counts; motion_small.npz the sink bytes of a short run;
+                   the static chain fixture with a 2-token delay
 """
 from __future__ import annotations
 
@@ -33,6 +36,7 @@ sys.path.insert(0, str(REF / "tests"))
 import fixtures as fx  # noqa: E402  (reference test fixtures)
 from tokenflow import behavior as tb  # noqa: E402
 from tokenflow.apps import bypass as rbp  # noqa: E402
+from tokenflow.apps import motion as rmo  # noqa: E402
 from tokenflow.apps import make_app  # noqa: E402
 from tokenflow.apps import predistortion as rpd  # noqa: E402
 from tokenflow.interp import interpret  # noqa: E402
@@ -185,6 +189,49 @@ def main():
                 vecs.append(bytes(span).hex())
             pol[f"{name}|{json.dumps(params, sort_keys=True)}|{seed}"] = vecs
     (OUT / "policies.json").write_text(json.dumps(pol, indent=1, sort_keys=True))
+
+    # motion detection (one-frame delay FIFO, apps/motion.py)
+    mo = {}
+    arrays = {}
+    for frames, seed in ((16, 7), (40, 3)):
+        data = rmo.make_input(seed, frames)
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "motion.bin")
+            Path(path).write_bytes(data)
+            g = build_graph(rmo.build_description(path))
+            res = interpret(g, source_firings=frames, seed=seed, capture_sinks=True)
+        key = f"{frames}|{seed}"
+        mo[key] = {"frames": frames, "seed": seed,
+                   "sink_digest": res.sink_digests["sink"],
+                   "firing_counts": dict(res.firing_counts)}
+        if frames == 16:
+            arrays["sink_16_7"] = np.frombuffer(res.sink_data["sink"], dtype=np.uint8)
+    # a byte diamond with 2 initial delay tokens on one branch: s1 broadcasts
+    # to an undelayed and a delayed channel, add_mod sums both
+    def port(pid, d):
+        return {"id": pid, "dir": d, "kind": "srp", "rate": 1}
+    desc = {"name": "diamond", "control": {}, "actors": [
+        {"id": "src", "kind": "static", "behavior": "counter_source", "ports": [port("out", "out")]},
+        {"id": "s1", "kind": "static", "behavior": "passthrough",
+         "ports": [port("in", "in"), port("out", "out")]},
+        {"id": "m", "kind": "static", "behavior": "add_mod", "params": {"offset": 3},
+         "ports": [port("a", "in"), port("b", "in"), port("out", "out")]},
+        {"id": "sink", "kind": "static", "behavior": "null_sink", "ports": [port("in", "in")]}],
+        "fifos": [
+            {"id": "f0", "src": "src.out", "dst": "s1.in", "rate": 1, "delay": 0, "token_bytes": 4},
+            {"id": "fa", "src": "s1.out", "dst": "m.a", "rate": 1, "delay": 0, "token_bytes": 4},
+            {"id": "fb", "src": "s1.out", "dst": "m.b", "rate": 1, "delay": 2, "token_bytes": 4,
+             "delay_payload_hex": bytes(range(8)).hex()},
+            {"id": "fo", "src": "m.out", "dst": "sink.in", "rate": 1, "delay": 0,
+             "token_bytes": 4}]}
+    g = build_graph(desc)
+    res = interpret(g, source_firings=12, seed=5, capture_sinks=True)
+    mo["diamond_delay2"] = {"description": desc, "iterations": 12, "seed": 5,
+                            "sink_digest": res.sink_digests["sink"],
+                            "firing_counts": dict(res.firing_counts),
+                            "sink_hex": res.sink_data["sink"].hex()}
+    (OUT / "motion.json").write_text(json.dumps(mo, indent=1, sort_keys=True))
+    np.savez_compressed(OUT / "motion_small.npz", **arrays)
     print("golden vectors written to", OUT)
 
 

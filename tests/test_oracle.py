@@ -75,3 +75,17 @@ def test_impulse_response(golden):
     x[0, 0, 0] = 1.0
     out = od.dpd_stream(x, [{1, 2, 3, 4}], 4)
     assert out.tobytes() == golden["dpd_small"]["impulse_sink"].tobytes()
+
+
+def test_motion_oracle_matches_reference(golden):
+    """oracle/motion.py against the reference motion app run through
+    tokenflow.interp.interpret (tests/golden/motion.json)."""
+    from oracle import motion as om
+    from paper_1802_06625_b200.apps import motion as am
+    want = golden["motion_small"]["sink_16_7"].tobytes()
+    assert om.motion_stream(am.make_input(7, 16), 16) == want
+    for key, case in golden["motion"].items():
+        if "|" not in key:
+            continue
+        got = om.motion_stream(am.make_input(case["seed"], case["frames"]), case["frames"])
+        assert hashlib.sha256(got).hexdigest() == case["sink_digest"]

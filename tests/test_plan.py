@@ -43,10 +43,39 @@ def test_eq1_mismatch_rejected():
 
 
 def test_data_delay_is_unsupported_not_wrong(golden):
+    """Delay tokens are admitted only on aligned channels between device
+    actors; others raise UnsupportedGraph instead of running wrong."""
     desc = golden["fixtures"]["static_chain"]["description"]
     desc = json.loads(json.dumps(desc))
-    desc["fifos"][1]["delay"] = 2
+    desc["fifos"][0]["delay"] = 2          # source -> s1: a host producer
     with pytest.raises(UnsupportedGraph, match="delay"):
+        admit(as_graph(desc))
+    desc = json.loads(json.dumps(golden["fixtures"]["rate_pair_atr3"]["description"]))
+    for f in desc["fifos"]:
+        if f["rate"] == 3 and f["src"] != "src.out" and not f["dst"].startswith("sink"):
+            f["delay"] = 2                 # not a multiple of the rate
+            break
+    else:
+        pytest.skip("no rate-3 device channel in the fixture")
+    with pytest.raises(UnsupportedGraph, match="delay"):
+        admit(as_graph(desc))
+
+
+def test_device_delay_admitted(golden):
+    desc = golden["motion"]["diamond_delay2"]["description"]
+    p = admit(as_graph(desc))
+    assert p.admission.beta["fb"] == 2 + 1 + (p.admission.c_factor - 1) * 1
+    from paper_1802_06625_b200.apps import motion
+    p = admit(as_graph(motion.build_description()))
+    assert p.roles["blur"] == p.roles["detect"] == p.roles["clean"] == "device"
+
+
+def test_delay_drain_phase_is_unsupported(golden):
+    """A consumer whose only input is delayed would fire on the delay tokens
+    after the sources stop (the reference drains them): not modelled."""
+    desc = json.loads(json.dumps(golden["fixtures"]["static_chain"]["description"]))
+    desc["fifos"][1]["delay"] = 2          # s1 -> s2, both device actors
+    with pytest.raises(UnsupportedGraph, match="drain"):
         admit(as_graph(desc))
 
 
