@@ -209,6 +209,9 @@ int pb_policy_tokens_streams(void* states, int n_streams, int kind, int length, 
   if (!states || (!out && n_firings > 0)) return pb::fail(PB_E_INVALID, "pb_policy_tokens_streams: null argument");
   if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
   threads = std::min(threads, n_streams);
+  // thread start-up costs ~10-20 us each: small batches run inline (the
+  // pipelined runtime calls this per sub-epoch while its hashers hold the cores)
+  if ((int64_t)n_streams * n_firings < 65536) threads = 1;
   std::vector<int> rcs(n_streams, PB_OK);
   auto work = [&](int t) {
     for (int s = t; s < n_streams; s += threads) {

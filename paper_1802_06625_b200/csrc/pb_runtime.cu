@@ -140,8 +140,10 @@ int pb_stream_sync(void* stream) {
 }
 
 int pb_event_create(void** event) {
+  // blocking sync: a host thread waiting on the event sleeps instead of
+  // spinning on a core the pipelined runtime's hashing threads need
   cudaEvent_t e;
-  PB_CUDA(cudaEventCreate(&e));
+  PB_CUDA(cudaEventCreateWithFlags(&e, cudaEventBlockingSync));
   *event = e;
   return PB_OK;
 }

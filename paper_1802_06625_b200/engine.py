@@ -27,6 +27,7 @@ from __future__ import annotations
 import ctypes as C
 import hashlib
 import os
+import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -974,30 +975,63 @@ class DeviceRuntime:
         comp_ev = [self._event() for _ in chunks]
         d2h_ev = [self._event() for _ in chunks]
         n_cond = len(self.plan.conds)
-        counts = np.zeros((len(chunks), max(1, n_cond), S), dtype=np.int32)
+        # per-chunk firing counts land in PINNED memory: a D2H into pageable
+        # memory would block the host until the chunk's kernels finished and
+        # serialise the copy-in of the next chunk behind them
+        ncnt = len(chunks) * max(1, n_cond) * S
+        if getattr(self, "_counts_pinned", None) is None or self._counts_pinned[1].size < 4 * ncnt:
+            self._counts_pinned = self.mem.pinned(4 * ncnt)
+        counts = self._counts_pinned[1][:4 * ncnt].view(np.int32).reshape(
+            len(chunks), max(1, n_cond), S)
         src = [(a, sorted(g.fifos_from(PortRef(a.id, a.output_ports[0].id)),
                           key=lambda f: f.id)[0])
                for a in g.actors if self.plan.roles[a.id] == "source"]
         sinks = [(a, g.fifo_into(PortRef(a.id, a.input_ports[0].id)))
                  for a in g.actors if self.plan.roles[a.id] == "sink"]
-        hash_pool = self.pool
-        coord = ThreadPoolExecutor(max_workers=1)
-        hash_done = []
+        # Hashing: each host thread owns a fixed set of (sink, stream) digests
+        # and walks the chunks in order (a digest's updates are sequential),
+        # waiting for "chunk c copied out" itself -- no per-chunk fan-out or
+        # join, so deep pipelines do not pay a barrier per chunk.
+        jobs = [(a, f, s) for a, f in sinks for s in range(S)]
+        n_thr = max(1, min(len(jobs), int(self.config.host_threads or 16)))
+        recorded = [threading.Event() for _ in chunks]     # d2h_ev[c] has been recorded
+        hashed = [0] * len(chunks)                          # hashers done with chunk c
+        hashed_cv = threading.Condition()
+        failure: list[BaseException] = []
 
-        def hash_chunk(c, it0, n):
-            _lib.check(lib.pb_event_sync(d2h_ev[c]))
-            w = it0 % E
+        def hasher(t):
+            mine = jobs[t::n_thr]
+            try:
+                for c, (it0, n) in enumerate(chunks):
+                    recorded[c].wait()
+                    if failure:
+                        return
+                    _lib.check(lib.pb_event_sync(d2h_ev[c]))
+                    w = it0 % E
+                    for a, f, s in mine:
+                        span = f.rate * f.token_bytes
+                        arr = self.sink_host[f.id][1][:S * E * span].reshape(S, E, span)
+                        data = arr[s, w:w + n].reshape(-1)
+                        self.digests[a.id][s].update(data)
+                        if self.captured is not None:
+                            self.captured[a.id][s] += memoryview(np.ascontiguousarray(data)).cast("B")
+                    with hashed_cv:
+                        hashed[c] += 1
+                        hashed_cv.notify_all()
+            except BaseException as e:  # noqa: BLE001
+                failure.append(e)
+                with hashed_cv:
+                    hashed_cv.notify_all()
 
-            def one(job):
-                a, f, s = job
-                span = f.rate * f.token_bytes
-                arr = self.sink_host[f.id][1][:S * E * span].reshape(S, E, span)
-                data = arr[s, w:w + n].reshape(-1)
-                self.digests[a.id][s].update(data)
-                if self.captured is not None:
-                    self.captured[a.id][s] += memoryview(np.ascontiguousarray(data)).cast("B")
-            list(hash_pool.map(one, [(a, f, s) for a, f in sinks for s in range(S)]))
+        def wait_hashed(c):
+            with hashed_cv:
+                hashed_cv.wait_for(lambda: hashed[c] == n_thr or failure)
+            if failure:
+                raise failure[0]
 
+        hashers = [threading.Thread(target=hasher, args=(t,), daemon=True) for t in range(n_thr)]
+        for th in hashers:
+            th.start()
         try:
             for c, (it0, n) in enumerate(chunks):
                 w = it0 % E
@@ -1061,7 +1095,7 @@ class DeviceRuntime:
                 _lib.check(lib.pb_event_record(comp_ev[c], self.stream))
                 # copy out (the host window slot must have been hashed)
                 if c >= R:
-                    hash_done[c - R].result()
+                    wait_hashed(c - R)
                 _lib.check(lib.pb_stream_wait(self.copy_out, comp_ev[c]))
                 for a, f in sinks:
                     st = self.storage[f.id]
@@ -1070,13 +1104,18 @@ class DeviceRuntime:
                     self._d2h_chunks(st.data, st.stream_stride, span, hptr + w * span, n, it0,
                                      host_pitch=E * span, stream=self.copy_out)
                 _lib.check(lib.pb_event_record(d2h_ev[c], self.copy_out))
-                hash_done.append(coord.submit(hash_chunk, c, it0, n))
+                recorded[c].set()
                 if deadline is not None and time.perf_counter() > deadline and c + 1 < len(chunks):
                     raise Timeout(self.config.timeout_ms, sorted(a.id for a in g.actors))
-            for fut in hash_done:
-                fut.result()
+            for c in range(len(chunks)):
+                wait_hashed(c)
         finally:
-            coord.shutdown(wait=True)
+            if len(failure) == 0 and not all(ev.is_set() for ev in recorded):
+                failure.append(RuntimeError("pipeline aborted"))
+            for ev in recorded:
+                ev.set()
+            for th in hashers:
+                th.join()
             lib.pb_stream_sync(self.copy_in)
             lib.pb_stream_sync(self.stream)
             lib.pb_stream_sync(self.copy_out)
