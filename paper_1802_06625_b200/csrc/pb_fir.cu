@@ -151,6 +151,11 @@ __device__ __forceinline__ u64 fmul2(u64 a, u64 b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
 __device__ __forceinline__ u64 fadd2(u64 a, u64 b) {
   u64 r;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -746,6 +751,7 @@ bank_plan_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan
 #ifndef PB_MERGED_MINB
 #define PB_MERGED_MINB 4
 #endif
+
 constexpr int kMergedThreads = 256;
 constexpr int kMPT = PB_MERGED_PT;             // outputs per thread
 constexpr int kMWin = kMPT + kPad;             // window (samples)
