@@ -675,7 +675,7 @@ struct __align__(16) BankPlan {
   int pad_[3];
 };
 
-constexpr int kPlanWarps = 4;   // spans per block (one warp each)
+constexpr int kPlanWarps = 8;   // spans per block (one warp each)
 
 __global__ void __launch_bounds__(32 * kPlanWarps)
 bank_plan_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan) {
@@ -688,10 +688,14 @@ bank_plan_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan
   }
   const pb_fir_actor* br = bank.branches;
   const int nb = bank.n_branches;
-  __shared__ float4 taps_all[kPlanWarps][kMaxBr][kTaps];
-  __shared__ float hist_all[kPlanWarps][kMaxBr][2][kHist];
-  float4 (*taps)[kTaps] = taps_all[threadIdx.y];
-  float (*hist)[2][kHist] = hist_all[threadIdx.y];
+  // dynamic shared memory sized for this bank's branch count (more resident
+  // warps than a kMaxBr-sized static array): per warp the taps and the
+  // histories of its span
+  extern __shared__ float4 plan_smem[];
+  float4 (*taps)[kTaps] =
+      reinterpret_cast<float4 (*)[kTaps]>(plan_smem + threadIdx.y * nb * (kTaps + 5));
+  float (*hist)[2][kHist] = reinterpret_cast<float (*)[2][kHist]>(
+      plan_smem + threadIdx.y * nb * (kTaps + 5) + nb * kTaps);
   for (int e = lane; e < nb * kTaps; e += 32) {
     const int b = e / kTaps, t = e % kTaps;
     const float cr = br[b].taps[t], ci = br[b].taps[kTaps + t];
@@ -833,7 +837,9 @@ int launch_merged_bank(const pb_filter_bank& bank, const pb_resolved& res, int64
     plan_n = spans;
   }
   dim3 pgrid((res.n_iter + kPlanWarps - 1) / kPlanWarps, res.n_streams);
-  bank_plan_kernel<<<pgrid, dim3(32, kPlanWarps), 0, st>>>(bank, res, B, plan);
+  // per warp: nb x kTaps float4 taps + nb x 2 x kHist histories (<= 5 float4 per branch)
+  const size_t psmem = sizeof(float4) * kPlanWarps * bank.n_branches * (kTaps + 5);
+  bank_plan_kernel<<<pgrid, dim3(32, kPlanWarps), psmem, st>>>(bank, res, B, plan);
   PB_LAUNCHED("bank_plan_kernel");
   const int bps = (int)((B / kMPT + kMergedThreads - 1) / kMergedThreads);
   const int64_t blocks = spans * bps;
