@@ -438,21 +438,32 @@ __device__ __forceinline__ void fill_patch(uint8_t* patch, const uint8_t* raw, c
     // on consecutive entries (conflict-free)
     constexpr int items = kPH * Cfg::PW;
     const float* rawf = reinterpret_cast<const float*>(raw) + (((t.ox0 - g.pad) * 3) & 3);
+    // entries in pairs: both entries' 30 loads are issued before either is
+    // split (one shared-memory latency per pair)
 #pragma unroll 1
-    for (int e = ct; e < items; e += kCvtThreads) {
-      const int r = e / Cfg::PW, c = e % Cfg::PW;
-      const float* src = rawf + r * Cfg::RAW_W + c * 3;
-      float v[16];
+    for (int e0 = ct; e0 < items; e0 += 2 * kCvtThreads) {
+      float v[2][16];
 #pragma unroll
-      for (int k = 0; k < 15; ++k) v[k] = src[k];
-      v[15] = 0.f;
-      uint4 h0, l0, h1, l1;
-      split8(v, h0, l0);
-      split8(v + 8, h1, l1);
-      *reinterpret_cast<uint4*>(patch + 0 * Cfg::PS + e * 16) = h0;
-      *reinterpret_cast<uint4*>(patch + 1 * Cfg::PS + e * 16) = h1;
-      *reinterpret_cast<uint4*>(patch + 2 * Cfg::PS + e * 16) = l0;
-      *reinterpret_cast<uint4*>(patch + 3 * Cfg::PS + e * 16) = l1;
+      for (int u = 0; u < 2; ++u) {
+        const int e = min(e0 + u * kCvtThreads, items - 1);
+        const int r = e / Cfg::PW, c = e % Cfg::PW;
+        const float* src = rawf + r * Cfg::RAW_W + c * 3;
+#pragma unroll
+        for (int k = 0; k < 15; ++k) v[u][k] = src[k];
+        v[u][15] = 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e = e0 + u * kCvtThreads;
+        if (e >= items) break;
+        uint4 h0, l0, h1, l1;
+        split8(v[u], h0, l0);
+        split8(v[u] + 8, h1, l1);
+        *reinterpret_cast<uint4*>(patch + 0 * Cfg::PS + e * 16) = h0;
+        *reinterpret_cast<uint4*>(patch + 1 * Cfg::PS + e * 16) = h1;
+        *reinterpret_cast<uint4*>(patch + 2 * Cfg::PS + e * 16) = l0;
+        *reinterpret_cast<uint4*>(patch + 3 * Cfg::PS + e * 16) = l1;
+      }
     }
   }
 }
