@@ -853,9 +853,10 @@ constexpr int kDStepBytes = 2 * kDN * 16 * 2;       // [wh; wl] 224 rows x 16 bf
 constexpr int kDChunkBytes = 4 * kDStepBytes;       // 28 KB
 constexpr int kDAPiece = 128 * kDKC * 2;            // 16 KB (one precision piece)
 constexpr int kDTmemCols = 256;
-constexpr int kDEpiWarps = 4, kDMmaWarp = 4;       // warps 0-3 epilogue, 4 MMA, 5-8 converters
+constexpr int kDEpiWarps = 4, kDMmaWarp = 4;       // warps 0-3 epilogue, 4 MMA, 5-12 converters
 constexpr int kDEpiThreads = kDEpiWarps * 32;
-constexpr int kDCvtThreads = 128;
+constexpr int kDCvtThreads = 256;
+constexpr int kDItems = 512 / kDCvtThreads;        // (row, 16-K quarter) items per thread per chunk
 constexpr int kDThreads = (kDEpiWarps + 1) * 32 + kDCvtThreads;
 
 struct DenseSmem {
@@ -926,9 +927,32 @@ dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, i
   } else if (warp >= kDMmaWarp + 1) {
     // ================================================ converters + weight copies
     const int ct = tid - (kDMmaWarp + 1) * 32;
+    // the next chunk's frame values are loaded while the current one is split
+    // (registers double-buffered), so a chunk costs no global-load latency
+    float4 nxt[kDItems][4];
+    auto load_chunk = [&](int c) {
+#pragma unroll
+      for (int k = 0; k < kDItems; ++k) {
+        const int i = ct + k * kDCvtThreads;
+        const int r = i >> 2, q = i & 3;
+        const float* rp = S.rowp[r];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          nxt[k][u] = rp != nullptr
+                          ? __ldg(reinterpret_cast<const float4*>(rp + (int64_t)c * kDKC + 16 * q) + u)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    if (c0 < c1) load_chunk(c0);
     for (int c = c0, it = 0; c < c1; ++c, ++it) {
       const int st = it % kDStages;
       const uint32_t use = (uint32_t)(it / kDStages);
+      float4 cur[kDItems][4];
+#pragma unroll
+      for (int k = 0; k < kDItems; ++k)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cur[k][u] = nxt[k][u];
+      if (c + 1 < c1) load_chunk(c + 1);
       mbar_wait(&S.empty[st], (use & 1) ^ 1);
       if (ct == 0) {
         mbar_arrive_tx(&S.full[st], kDChunkBytes);
@@ -936,21 +960,14 @@ dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, i
       }
       // 128 rows x 4 quarters of 16 K, 4 threads per row
 #pragma unroll
-      for (int k = 0; k < 512 / kDCvtThreads; ++k) {
+      for (int k = 0; k < kDItems; ++k) {
         const int i = ct + k * kDCvtThreads;
         const int r = i >> 2, q = i & 3;
-        const float* rp = S.rowp[r];
         float v[16];
-        if (rp != nullptr) {
-          const float4* src = reinterpret_cast<const float4*>(rp + (int64_t)c * kDKC + 16 * q);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float4 t = __ldg(src + u);
-            v[4 * u] = t.x; v[4 * u + 1] = t.y; v[4 * u + 2] = t.z; v[4 * u + 3] = t.w;
-          }
-        } else {
-#pragma unroll
-          for (int u = 0; u < 16; ++u) v[u] = 0.f;
+        for (int u = 0; u < 4; ++u) {
+          v[4 * u] = cur[k][u].x; v[4 * u + 1] = cur[k][u].y;
+          v[4 * u + 2] = cur[k][u].z; v[4 * u + 3] = cur[k][u].w;
         }
         uint4 h0, l0, h1, l1;
         split8(v, h0, l0);
@@ -994,30 +1011,32 @@ dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, i
     mbar_wait(&S.acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
-    float y[kDN];
-#pragma unroll
-    for (int c = 0; c < kDN; c += 32) {
-      float t0[32], t1[32];
-      tmem_ld32(tl + c, t0);          // xh*wh + xl*wh, outputs c..c+31
-      tmem_ld32(tl + kDN + c, t1);    // xh*wl
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-      for (int u = 0; u < 32; ++u)
-        if (c + u < kDN) y[c + u] = __fadd_rn(t0[u], t1[u]);
-    }
     const int64_t m = (int64_t)mt * 128 + r;
     float* op = S.outp[r];
-    if (splits == 1) {
-      if (op != nullptr) {
+    float* mine = splits > 1 ? partial + ((int64_t)split * gridDim.x * 128 + m) * kDN : nullptr;
+    // 32 outputs at a time: [xh*wh + xl*wh] + [xh*wl]
+#pragma unroll 1
+    for (int c = 0; c < kDN; c += 32) {
+      float t0[32], t1[32];
+      tmem_ld32(tl + c, t0);
+      tmem_ld32(tl + kDN + c, t1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int o = 0; o < kDN; ++o)
-          if (o < a.nout) op[o] = __fadd_rn(y[o], __ldg(a.bias + o));
+      for (int u = 0; u < 32; ++u) t0[u] = __fadd_rn(t0[u], t1[u]);
+      if (splits == 1) {
+        if (op != nullptr) {
+#pragma unroll
+          for (int u = 0; u < 32; ++u)
+            if (c + u < a.nout) op[c + u] = __fadd_rn(t0[u], __ldg(a.bias + c + u));
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 32; u += 4)
+          if (c + u < kDN)
+            *reinterpret_cast<float4*>(mine + c + u) = make_float4(t0[u], t0[u + 1], t0[u + 2], t0[u + 3]);
       }
-    } else {
-      float* mine = partial + ((int64_t)split * gridDim.x * 128 + m) * kDN;
-#pragma unroll
-      for (int o = 0; o < kDN; o += 4)
-        *reinterpret_cast<float4*>(mine + o) = make_float4(y[o], y[o + 1], y[o + 2], y[o + 3]);
+    }
+    if (splits > 1) {
       __threadfence();
       asm volatile("bar.sync 1, %0;" ::"n"(kDEpiThreads));
       if (r == 0) S.last = (atomicAdd(counters + mt, 1) == splits - 1);
