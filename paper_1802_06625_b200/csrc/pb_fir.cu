@@ -755,6 +755,9 @@ bank_plan_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan
 #ifndef PB_MERGED_MINB
 #define PB_MERGED_MINB 4
 #endif
+#ifndef PB_MERGED_STREAMING   // 1: evict-first loads, 2: + streaming stores
+#define PB_MERGED_STREAMING 2
+#endif
 
 constexpr int kMergedThreads = 256;
 constexpr int kMPT = PB_MERGED_PT;             // outputs per thread
@@ -782,8 +785,13 @@ bank_merged_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
     const int64_t idx = n0 - kPad + 4 * k;   // multiple of 4: all-or-nothing pre-span
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
     if (live && idx >= 0) {
+#if PB_MERGED_STREAMING
+      a = __ldcs(reinterpret_cast<const float4*>(in + idx));
+      b = __ldcs(reinterpret_cast<const float4*>(in + B + idx));
+#else
       a = __ldg(reinterpret_cast<const float4*>(in + idx));
       b = __ldg(reinterpret_cast<const float4*>(in + B + idx));
+#endif
     }
     wr[4 * k] = a.x; wr[4 * k + 1] = a.y; wr[4 * k + 2] = a.z; wr[4 * k + 3] = a.w;
     wi[4 * k] = b.x; wi[4 * k + 1] = b.y; wi[4 * k + 2] = b.z; wi[4 * k + 3] = b.w;
@@ -821,8 +829,13 @@ bank_merged_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
   float4* oi = reinterpret_cast<float4*>(out + B + n0);
 #pragma unroll
   for (int k = 0; k < kMPT / 4; ++k) {
+#if PB_MERGED_STREAMING >= 2
+    __stcs(orr + k, make_float4(yr[4 * k], yr[4 * k + 1], yr[4 * k + 2], yr[4 * k + 3]));
+    __stcs(oi + k, make_float4(yi[4 * k], yi[4 * k + 1], yi[4 * k + 2], yi[4 * k + 3]));
+#else
     orr[k] = make_float4(yr[4 * k], yr[4 * k + 1], yr[4 * k + 2], yr[4 * k + 3]);
     oi[k] = make_float4(yi[4 * k], yi[4 * k + 1], yi[4 * k + 2], yi[4 * k + 3]);
+#endif
   }
 }
 
