@@ -261,9 +261,9 @@ __device__ __forceinline__ void store8(float* out, int64_t B, int n0, const u64 
   float4* orr = reinterpret_cast<float4*>(out + n0);
   float4* oi = reinterpret_cast<float4*>(out + B + n0);
 #pragma unroll
-  for (int k = 0; k < kPerThread / 4; ++k) {
-    orr[k] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
-    oi[k] = make_float4(i[4 * k], i[4 * k + 1], i[4 * k + 2], i[4 * k + 3]);
+  for (int k = 0; k < kPerThread / 4; ++k) {   // streaming stores: output is not re-read here
+    __stcs(orr + k, make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
+    __stcs(oi + k, make_float4(i[4 * k], i[4 * k + 1], i[4 * k + 2], i[4 * k + 3]));
   }
 }
 
