@@ -4,8 +4,9 @@ Streams are independent replicas of one analysed graph (their own rings,
 histories and control RNG), so the hot path needs no collective: rank r runs
 a contiguous range of streams on its own GPU (one process per GPU, launched
 by torchrun).  The only exchange is the final gather of the per-stream
-reports to rank 0, which torch.distributed performs over NCCL (NVLink) for
-sink bytes and as pickled objects for the small digest/count records.
+reports to rank 0: captured sink bytes as uint8 tensors through the process
+group's backend (NCCL over NVLink on the GPU box), the small digest/count
+records as pickled objects.
 """
 from __future__ import annotations
 
@@ -37,19 +38,49 @@ def gather_reports(local: Sequence[RunReport], streams: range, total: int,
                    dst: int = 0) -> list[RunReport] | None:
     """Collect every rank's per-stream reports on `dst`, ordered by stream id.
     Ranks other than dst return None.  Without an initialised process group
-    the local reports are returned as they are."""
+    the local reports are returned as they are.
+
+    The small records (digests, firing counts, occupancies) travel as pickled
+    objects; captured sink bytes travel as one uint8 tensor per rank through
+    the group's backend -- `dist.gather` over NCCL (NVLink, from the rank's
+    device) on the GPU box, gloo on the CPU -- padded to the largest rank."""
     dist = _dist()
     if dist is None:
         return list(local)
-    payload = (list(streams), [r.__dict__ for r in local])
-    gathered = [None] * dist.get_world_size() if dist.get_rank() == dst else None
-    dist.gather_object(payload, gathered, dst=dst)
-    if dist.get_rank() != dst:
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    meta = []
+    blobs = []
+    for sid, r in zip(streams, local):
+        rec = {k: v for k, v in r.__dict__.items() if k != "sink_data"}
+        names = sorted(r.sink_data)
+        meta.append((sid, rec, [(n, len(r.sink_data[n])) for n in names]))
+        blobs.extend(r.sink_data[n] for n in names)
+    blob = b"".join(blobs)
+    sizes = [None] * world
+    dist.all_gather_object(sizes, len(blob))
+    gathered_meta = [None] * world if rank == dst else None
+    dist.gather_object(meta, gathered_meta, dst=dst)
+    pad = max(1, max(sizes))
+    nccl = dist.get_backend() == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+    t = torch.zeros(pad, dtype=torch.uint8, device=dev)
+    if blob:
+        t[:len(blob)] = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(dev)
+    parts = [torch.empty_like(t) for _ in range(world)] if rank == dst else None
+    dist.gather(t, parts, dst=dst)
+    if rank != dst:
         return None
     out: list[RunReport | None] = [None] * total
-    for ids, reps in gathered:
-        for sid, d in zip(ids, reps):
-            out[sid] = RunReport(**d)
+    for r_meta, part, n in zip(gathered_meta, parts, sizes):
+        data = part[:n].cpu().numpy().tobytes()
+        off = 0
+        for sid, rec, lens in r_meta:
+            sinks = {}
+            for name, ln in lens:
+                sinks[name] = data[off:off + ln]
+                off += ln
+            out[sid] = RunReport(**rec, sink_data=sinks)
     return out  # type: ignore[return-value]
 
 
