@@ -125,3 +125,12 @@ def test_reference_graph_object_converts(golden):
     g_ref = build_graph(desc)
     g = as_graph(g_ref)
     assert g.description() == as_graph(desc).description()
+
+
+def test_mixed_graph_admitted():
+    """BASELINE config 5: the DPD region and the adaptive CNN in one graph."""
+    from paper_1802_06625_b200.apps import mixed
+    p = admit(as_graph(mixed.build_description(256, 4, 2)))
+    assert p.roles["dpd_conf"] == p.roles["cnn_conf"] == "config"
+    assert {p.roles[a] for a in ("cnn_l1", "cnn_l2", "cnn_l3", "dpd_b1")} == {"device"}
+    assert len(p.conds) == 6     # 4 DPD branches + CNN process / bypass
