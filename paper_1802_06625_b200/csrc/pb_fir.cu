@@ -749,6 +749,121 @@ bank_plan_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan
   if (lane == 0) p.have = 1;
 }
 
+// One block per stream: the whole epoch's plans at once.  Activity masks of
+// every span go to shared memory, each branch's "previous firing" index is a
+// warp max-scan over the spans, and every thread then plans one span: its
+// branch histories are one independent load each (the bank's own input span
+// at that firing -- the route copied the same samples to the branch), not a
+// prefix -> worklist -> ring-base chain.  Used when the tables fit in 48 KB.
+constexpr int kPlanStreamThreads = 256;
+
+__host__ __device__ inline size_t plan_stream_smem(int n_iter, int nb) {
+  return (size_t)n_iter * 4 + (size_t)n_iter + 15 + (size_t)nb * n_iter * 4 + (size_t)nb * kTaps * 16 + 16;
+}
+
+__global__ void __launch_bounds__(kPlanStreamThreads)
+bank_plan_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan) {
+  const int s = blockIdx.x, E = res.n_iter, tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const pb_fir_actor* br = bank.branches;
+  const int nb = bank.n_branches;
+  extern __shared__ float4 pss[];
+  float4* taps = pss;                                            // [nb][kTaps]
+  uint32_t* mask = reinterpret_cast<uint32_t*>(taps + nb * kTaps);   // [E]
+  int* prev = reinterpret_cast<int*>(mask + E);                  // [nb][E]
+  uint8_t* have = reinterpret_cast<uint8_t*>(prev + nb * E);     // [E]
+  for (int e = tid; e < nb * kTaps; e += kPlanStreamThreads) {
+    const int b = e / kTaps, t = e % kTaps;
+    const float cr = br[b].taps[t], ci = br[b].taps[kTaps + t];
+    taps[e] = make_float4(cr, ci, ci, cr);
+  }
+  for (int n = tid; n < E; n += kPlanStreamThreads) {
+    const bool h = pb::active(res, bank.actor_cond, s, n);
+    uint32_t m = 0;
+    if (h)
+      for (int b = 0; b < nb; ++b)
+        if (pb::active(res, br[b].cond, s, n)) m |= 1u << b;
+    mask[n] = m;
+    have[n] = h;
+  }
+  __syncthreads();
+  // previous firing of each branch before span n (exclusive max-scan)
+  const int chunk = (E + 31) / 32;
+  for (int b = warp; b < nb; b += kPlanStreamThreads / 32) {
+    const int lo = lane * chunk, hi = min(E, lo + chunk);
+    int last = -1;
+    for (int n = lo; n < hi; ++n)
+      if ((mask[n] >> b) & 1u) last = n;
+    int carry = last;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, carry, d);
+      if (lane >= d) carry = max(carry, o);
+    }
+    int cur = __shfl_up_sync(0xffffffffu, carry, 1);
+    if (lane == 0) cur = -1;
+    for (int n = lo; n < hi; ++n) {
+      prev[b * E + n] = cur;
+      if ((mask[n] >> b) & 1u) cur = n;
+    }
+  }
+  __syncthreads();
+  for (int n = tid; n < E; n += kPlanStreamThreads) {
+    BankPlan& p = plan[(int64_t)s * E + n];
+    if (!have[n]) {
+      p.have = 0;
+      continue;
+    }
+    const uint32_t m = mask[n];
+    float4 mt[kTaps];
+#pragma unroll
+    for (int t = 0; t < kTaps; ++t) mt[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float cr[kHist], ci[kHist];
+#pragma unroll
+    for (int k = 0; k < kHist; ++k) cr[k] = ci[k] = 0.f;
+    for (int b = 0; b < nb; ++b) {
+      if (!((m >> b) & 1u)) continue;
+      const int src = prev[b * E + n];
+      const float *hr, *hi;
+      if (src < 0) {
+        hr = br[b].state + (int64_t)s * 2 * kHist;
+        hi = hr + kHist;
+      } else {
+        const float* pv = reinterpret_cast<const float*>(pb::span_ptr(bank.in, res, s, src));
+        hr = pv + B - kHist;
+        hi = pv + 2 * B - kHist;
+      }
+      float h_r[kHist], h_i[kHist];
+#pragma unroll
+      for (int q = 0; q < kHist; ++q) {
+        h_r[q] = hr[q];
+        h_i[q] = hi[q];
+      }
+      const float4* tb = taps + b * kTaps;
+#pragma unroll
+      for (int t = 0; t < kTaps; ++t) {
+        const float4 c = tb[t];
+        mt[t].x += c.x; mt[t].y += c.y; mt[t].z += c.z; mt[t].w += c.w;
+      }
+      // output k reads pre-span sample k - t (history slot k - t + 9) for t > k
+#pragma unroll
+      for (int k = 0; k < kHist; ++k)
+#pragma unroll
+        for (int t = k + 1; t < kTaps; ++t) {
+          const float4 c = tb[t];
+          const float xr = h_r[k - t + kHist], xi = h_i[k - t + kHist];
+          cr[k] = __fmaf_rn(-c.y, xi, __fmaf_rn(c.x, xr, cr[k]));
+          ci[k] = __fmaf_rn(c.y, xr, __fmaf_rn(c.x, xi, ci[k]));
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < kTaps; ++t) p.taps[t] = mt[t];
+#pragma unroll
+    for (int k = 0; k < kHist; ++k) p.corr[k] = make_float2(cr[k], ci[k]);
+    p.have = 1;
+  }
+}
+
 #ifndef PB_MERGED_PT
 #define PB_MERGED_PT 8
 #endif
@@ -850,9 +965,14 @@ int launch_merged_bank(const pb_filter_bank& bank, const pb_resolved& res, int64
     plan_n = spans;
   }
   dim3 pgrid((res.n_iter + kPlanWarps - 1) / kPlanWarps, res.n_streams);
-  // per warp: nb x kTaps float4 taps + nb x 2 x kHist histories (<= 5 float4 per branch)
-  const size_t psmem = sizeof(float4) * kPlanWarps * bank.n_branches * (kTaps + 5);
-  bank_plan_kernel<<<pgrid, dim3(32, kPlanWarps), psmem, st>>>(bank, res, B, plan);
+  const size_t ssmem = plan_stream_smem(res.n_iter, bank.n_branches);
+  if (ssmem <= 48 * 1024) {
+    bank_plan_stream_kernel<<<res.n_streams, kPlanStreamThreads, ssmem, st>>>(bank, res, B, plan);
+  } else {
+    // per warp: nb x kTaps float4 taps + nb x 2 x kHist histories (<= 5 float4 per branch)
+    const size_t psmem = sizeof(float4) * kPlanWarps * bank.n_branches * (kTaps + 5);
+    bank_plan_kernel<<<pgrid, dim3(32, kPlanWarps), psmem, st>>>(bank, res, B, plan);
+  }
   PB_LAUNCHED("bank_plan_kernel");
   const int bps = (int)((B / kMPT + kMergedThreads - 1) / kMergedThreads);
   const int64_t blocks = spans * bps;
