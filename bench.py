@@ -309,6 +309,30 @@ def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
             parity = {"max_abs_logit_err": float(np.abs(got - want).max()),
                       "top1_equal": bool((got.argmax(-1) == want.argmax(-1)).all()),
                       "checked": "stream 0, first firing vs oracle/cnn.py (tolerance 1e-3)"}
+
+    # the adaptive graph as the paper runs it (alternate_policy: every other
+    # firing bypasses the CNN), same frames, device-resident
+    rta = DeviceRuntime(vision.build_description(R), config=RuntimeConfig(
+        source_firings=F, epoch=F, device=local), n_streams=S,
+        seeds=[rank * S + s for s in range(S)], sources={"src": [None] * S})
+    sta = rta.source_staging("src")
+    for s in range(S):
+        sta[s] = stage[s]
+    rta.reset()
+    rta.stage_sources(0, F, prestaged=True)
+    rta.stage_control(0, F)
+    for _ in range(3):
+        rta.fire_epoch(0, F)
+    _lib.check(lib.pb_stream_sync(rta.stream))
+    a0, a1 = ev(), ev()
+    lib.pb_event_record(a0, rta.stream)
+    for _ in range(args.cnn_steps):
+        rta.fire_epoch(0, F)
+    lib.pb_event_record(a1, rta.stream)
+    _lib.check(lib.pb_stream_sync(rta.stream))
+    _lib.check(lib.pb_event_elapsed_ms(a0, a1, C.byref(ms)))
+    adaptive_ms = max_over_ranks(ms.value / args.cnn_steps)
+    rta.close()
     rt.close()
 
     conv_flops = vision.flops_per_frame() - 18432 * 100 * 2
@@ -355,6 +379,10 @@ def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
                 "includes": "H2D pinned frames, native control actor, device firings, "
                             "logits D2H, SHA-256 per stream"},
         "gpu_launches": launches,
+        "adaptive": {"value": frames * world / (adaptive_ms / 1e3), "unit": "frames/s",
+                     "ms_per_step": adaptive_ms,
+                     "what": "the paper's adaptive graph (alternate_policy: every other "
+                             "24-frame firing bypasses the CNN), same frames"},
         "parity_stream0": parity,
         "cpu_baseline": cpu,
     }
