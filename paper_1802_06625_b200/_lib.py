@@ -11,7 +11,7 @@ import os
 from pathlib import Path
 
 from .errors import (ActorPanic, DeviceUnavailable, EndOfStream, InvalidParams, Poisoned,
-                     ProtocolError)
+                     ProtocolError, UnsupportedGraph)
 
 # PB_LIB_PATH selects an alternative build of the same library (profiling
 # experiments with different compile-time tunings); default: the in-tree build
@@ -234,8 +234,8 @@ def check(rc: int, what: str = "") -> int:
         raise EndOfStream(text)
     if rc == PB_E_POISONED:
         raise Poisoned("ring", text)
-    if rc == PB_E_UNSUPPORTED:
-        raise NotImplementedError(text)
+    if rc == PB_E_UNSUPPORTED:   # shape / size outside what the kernels implement
+        raise UnsupportedGraph(text)
     if rc == PB_E_ACTOR:
         raise ActorPanic(what or "device", RuntimeError(text))
     raise DeviceUnavailable(text or f"libprune_b200 status {rc}")
