@@ -397,11 +397,19 @@ def main():
         run_reference(args, rank, world)
         return
     dist = None
+    # PB_BENCH_BACKEND=gloo (testing the multi-rank path with several ranks on
+    # one GPU, which NCCL refuses): ranks share devices round-robin and the
+    # max-over-ranks reduction runs on the CPU
+    backend = os.environ.get("PB_BENCH_BACKEND", "nccl")
     if world > 1:
         import torch
         import torch.distributed as dist
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import ctypes as C
 
@@ -430,7 +438,8 @@ def main():
         if dist is None:
             return v
         import torch
-        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([v], dtype=torch.float64,
+                         device=f"cuda:{local}" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
