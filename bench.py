@@ -582,7 +582,7 @@ def main():
     fp32_peak = 1e12 * max(probe.get("fmul_tops", 0), probe.get("fadd_tops", 0)) or \
         148 * 128 * 1.965e9
     names = {exact_math: "fir_persistent<bank, EXACT>" if fused else "fir_persistent<actors>",
-             tol_math: "bank_plan_kernel + bank_merged_kernel" if fused else
+             tol_math: "bank_plan_par_kernel + bank_stream_kernel" if fused else
              "fir_persistent<actors, FMA>"}
 
     def roofline(math_mode, k_ms):

@@ -138,6 +138,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, u64* bar,
+                                              u64 policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ u64 pack2(float lo, float hi) {
   u64 r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
@@ -864,6 +872,182 @@ bank_plan_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPla
   }
 }
 
+// Chunk-parallel planner: block (s, c) plans spans [c*kPC, (c+1)*kPC) of
+// stream s.  The activity masks of spans 0..hi-1 (one byte load per
+// condition, all independent) and each branch's previous-firing max-scan are
+// recomputed per block -- cheap -- so the epoch is planned by
+// n_streams * E / kPC blocks instead of n_streams, and every dependent load
+// of a span's plan is issued at once: the branch histories are gathered into
+// shared memory by a flat (span, branch, sample) loop in one round trip, then
+// merged taps and corrections are one thread per (span, tap | output).
+#ifndef PB_PLAN_PAR
+#define PB_PLAN_PAR 1
+#endif
+#ifndef PB_PLAN_STOP   // profiling: end the planner after phase 1/2/3
+#define PB_PLAN_STOP 0
+#endif
+#ifndef PB_PLAN_PC
+#define PB_PLAN_PC 64
+#endif
+constexpr int kPC = PB_PLAN_PC;         // spans per block
+constexpr int kPlanParThreads = 256;
+
+__host__ __device__ inline size_t plan_par_smem(int n_iter, int nb) {
+  return (size_t)nb * kTaps * 16                 // taps
+         + (size_t)kPC * nb * 8                  // history source pointers
+         + (size_t)kPC * nb * 2 * kHist * 4      // hist
+         + (size_t)n_iter * 4                    // mask
+         + (size_t)nb * kPC * 4                  // prev
+         + (size_t)n_iter + 16;                  // have
+}
+
+__global__ void __launch_bounds__(kPlanParThreads)
+bank_plan_par_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan) {
+  const int s = blockIdx.x, E = res.n_iter, tid = threadIdx.x;
+  const int lo = blockIdx.y * kPC, hi = min(E, lo + kPC), np = hi - lo;
+  const int warp = tid >> 5, lane = tid & 31;
+  const pb_fir_actor* br = bank.branches;
+  const int nb = bank.n_branches;
+  extern __shared__ float4 ppar[];
+  float4* taps = ppar;                                                  // [nb][kTaps]
+  const float** hsrc = reinterpret_cast<const float**>(taps + nb * kTaps);   // [kPC][nb]
+  float* hist = reinterpret_cast<float*>(hsrc + kPC * nb);             // [kPC][nb][2][kHist]
+  uint32_t* mask = reinterpret_cast<uint32_t*>(hist + kPC * nb * 2 * kHist);  // [hi]
+  int* prev = reinterpret_cast<int*>(mask + E);                         // [nb][kPC]
+  uint8_t* have = reinterpret_cast<uint8_t*>(prev + nb * kPC);          // [hi]
+  const int64_t in_base = bank.in.base ? bank.in.base[s] : 0;
+  // 1. taps and activity masks: every load of a thread issued before use
+  for (int e = tid; e < nb * kTaps; e += kPlanParThreads) {
+    const int b = e / kTaps, t = e % kTaps;
+    const float* tp = br[b].taps;
+    const float cr = tp[t], ci = tp[kTaps + t];
+    taps[e] = make_float4(cr, ci, ci, cr);
+  }
+  for (int n = tid; n < hi; n += kPlanParThreads) {
+    const int64_t col = (int64_t)s * res.cap + n;
+    const int64_t stride = (int64_t)res.n_streams * res.cap;
+    uint8_t a[kMaxBr];
+#pragma unroll
+    for (int b = 0; b < kMaxBr; ++b) {
+      const int c = b < nb ? br[b].cond : -1;
+      a[b] = c < 0 ? 1 : res.act[c * stride + col];
+    }
+    const bool h = bank.actor_cond < 0 || res.act[bank.actor_cond * stride + col];
+    uint32_t m = 0;
+#pragma unroll
+    for (int b = 0; b < kMaxBr; ++b)
+      if (b < nb && a[b]) m |= 1u << b;
+    mask[n] = h ? m : 0u;
+    have[n] = h;
+  }
+  __syncthreads();
+#if PB_PLAN_STOP == 1
+  return;
+#endif
+  // 2. previous firing of each branch before span n, n in [lo, hi): warp
+  //    max-scan over [0, hi)
+  const int chunk = (hi + 31) / 32;
+  for (int b = warp; b < nb; b += kPlanParThreads / 32) {
+    const int a0 = lane * chunk, a1 = min(hi, a0 + chunk);
+    int last = -1;
+    for (int n = a0; n < a1; ++n)
+      if ((mask[n] >> b) & 1u) last = n;
+    int carry = last;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, carry, d);
+      if (lane >= d) carry = max(carry, o);
+    }
+    int cur = __shfl_up_sync(0xffffffffu, carry, 1);
+    if (lane == 0) cur = -1;
+    for (int n = a0; n < a1; ++n) {
+      if (n >= lo) prev[b * kPC + n - lo] = cur;
+      if ((mask[n] >> b) & 1u) cur = n;
+    }
+  }
+  __syncthreads();
+#if PB_PLAN_STOP == 2
+  return;
+#endif
+  // 3. history sources (one pointer per active (span, branch)), then every
+  //    history sample in flight at once (cp.async into shared memory)
+  for (int e = tid; e < np * nb; e += kPlanParThreads) {
+    const int i = e / nb, b = e - i * nb;
+    const int src = prev[b * kPC + i];
+    const float* p = nullptr;
+    if ((mask[lo + i] >> b) & 1u) {
+      if (src < 0)   // first firing of the branch: its carried state [2][kHist]
+        p = br[b].state + (int64_t)s * 2 * kHist;
+      else           // re plane tail; the im plane tail is p + B
+        p = reinterpret_cast<const float*>(span_ptr_b(bank.in, in_base, res, s, src)) + B - kHist;
+    }
+    hsrc[e] = p;
+  }
+  __syncthreads();
+  for (int e = tid; e < np * nb * 2 * kHist; e += kPlanParThreads) {
+    const int ib = e / (2 * kHist), q = e - ib * 2 * kHist;
+    const float* p = hsrc[ib];
+    if (!p) continue;
+    const int b = ib % nb, i = ib / nb;
+    const bool state = prev[b * kPC + i] < 0;
+    const int plane = q / kHist, k = q - plane * kHist;
+    cp_async4(hist + e, p + (state ? q : plane * B + k));
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+#if PB_PLAN_STOP == 3
+  return;
+#endif
+  // 4. one thread per span: merged taps and the 9 corrections in registers
+  //    (fully unrolled; a flat (span, slot) split diverges inside warps)
+  for (int i = tid; i < np; i += kPlanParThreads) {
+    const int n = lo + i;
+    BankPlan& p = plan[(int64_t)s * E + n];
+    if (!have[n]) {
+      p.have = 0;
+      continue;
+    }
+    const uint32_t m = mask[n];
+    float4 mt[kTaps];
+#pragma unroll
+    for (int t = 0; t < kTaps; ++t) mt[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float cr[kHist], ci[kHist];
+#pragma unroll
+    for (int k = 0; k < kHist; ++k) cr[k] = ci[k] = 0.f;
+    for (int b = 0; b < nb; ++b) {
+      if (!((m >> b) & 1u)) continue;
+      const float* h = hist + (i * nb + b) * 2 * kHist;
+      float h_r[kHist], h_i[kHist];
+#pragma unroll
+      for (int q = 0; q < kHist; ++q) {
+        h_r[q] = h[q];
+        h_i[q] = h[kHist + q];
+      }
+      const float4* tb = taps + b * kTaps;
+#pragma unroll
+      for (int t = 0; t < kTaps; ++t) {
+        const float4 c = tb[t];
+        mt[t].x += c.x; mt[t].y += c.y; mt[t].z += c.z; mt[t].w += c.w;
+      }
+      // output k reads pre-span sample k - t (history slot k - t + 9) for t > k
+#pragma unroll
+      for (int k = 0; k < kHist; ++k)
+#pragma unroll
+        for (int t = k + 1; t < kTaps; ++t) {
+          const float4 c = tb[t];
+          const float xr = h_r[k - t + kHist], xi = h_i[k - t + kHist];
+          cr[k] = __fmaf_rn(-c.y, xi, __fmaf_rn(c.x, xr, cr[k]));
+          ci[k] = __fmaf_rn(c.y, xr, __fmaf_rn(c.x, xi, ci[k]));
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < kTaps; ++t) p.taps[t] = mt[t];
+#pragma unroll
+    for (int k = 0; k < kHist; ++k) p.corr[k] = make_float2(cr[k], ci[k]);
+    p.have = 1;
+  }
+}
+
 #ifndef PB_MERGED_PT
 #define PB_MERGED_PT 8
 #endif
@@ -954,6 +1138,165 @@ bank_merged_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
   }
 }
 
+// Persistent form of the merged stencil: one CTA per SM slot walks a
+// contiguous range of (span, tile) items.  A producer warp streams each
+// tile's two sample planes (with the 12-sample halo from the same span) and
+// the span's BankPlan into a shared-memory stage with cp.async.bulk, kMSStages
+// tiles ahead; the consumer warps read their 20-sample windows from shared
+// memory, run the merged FIR and store straight to the output span.  Memory
+// requests therefore never wait on the FMA work, and the span addressing
+// (ring index arithmetic) runs once per 2048-sample tile in the producer
+// instead of once per thread.
+#ifndef PB_MS_WARPS
+#define PB_MS_WARPS 4
+#endif
+#ifndef PB_MS_L2HINT   // input planes are read once: evict-first in L2
+#define PB_MS_L2HINT 1
+#endif
+#ifndef PB_MS_STAGES
+#define PB_MS_STAGES 8
+#endif
+constexpr int kMSWarps = PB_MS_WARPS;
+constexpr int kMSThreads = 32 * (kMSWarps + 1);
+constexpr int kMSTile = 32 * kMSWarps * kPerThread;   // samples per item
+constexpr int kMSStages = PB_MS_STAGES;
+
+struct __align__(16) MSStage {
+  BankPlan plan;
+  float re[kPad + kMSTile];
+  float im[kPad + kMSTile];
+};
+struct __align__(16) MSSmem {
+  MSStage st[kMSStages];
+  u64 out[kMSStages];   // output span base of the staged tile
+  int t0[kMSStages];    // its first sample
+  u64 full[kMSStages];
+  u64 empty[kMSStages];
+};
+static_assert(sizeof(BankPlan) % 16 == 0, "BankPlan is bulk-copied");
+
+#ifndef PB_MS_MINB
+#define PB_MS_MINB 1
+#endif
+__global__ void __launch_bounds__(kMSThreads, PB_MS_MINB)
+bank_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPlan* plan,
+                   int tiles) {
+  extern __shared__ __align__(128) uint8_t ms_raw[];
+  MSSmem& sm = *reinterpret_cast<MSSmem*>(ms_raw);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kMSStages; ++k) {
+      mbar_init(&sm.full[k], 1);
+      mbar_init(&sm.empty[k], kMSWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t total = (int64_t)res.n_streams * res.n_iter * tiles;
+  // a contiguous item range per CTA (measured faster than interleaving the
+  // CTAs over neighbouring tiles: 75% vs 66% of the HBM roofline)
+  const int64_t w0 = total * blockIdx.x / gridDim.x;
+  const int64_t n_items = total * (blockIdx.x + 1) / gridDim.x - w0;
+  const int warp = threadIdx.x >> 5;
+
+  if (warp == kMSWarps) {
+    // ------------------------------------------------------------ producer
+    if ((threadIdx.x & 31) != 0) return;
+#if PB_MS_L2HINT
+    u64 pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
+    int64_t span = w0 / tiles;
+    int tile = (int)(w0 - span * tiles) - 1;
+    const float* in = nullptr;
+    u64 out = 0;
+    for (int64_t k = 0; k < n_items; ++k) {
+      if (k == 0 || ++tile == tiles) {   // (next) span: its ring addresses
+        if (k > 0) {
+          tile = 0;
+          ++span;
+        } else {
+          ++tile;
+        }
+        const int s = (int)(span / res.n_iter), n = (int)(span - (int64_t)s * res.n_iter);
+        in = reinterpret_cast<const float*>(pb::span_ptr(bank.in, res, s, n));
+        out = reinterpret_cast<u64>(pb::span_ptr(bank.out, res, s, n));
+      }
+      const int stage = (int)(k % kMSStages);
+      mbar_wait(&sm.empty[stage], (uint32_t)(((k / kMSStages) & 1) ^ 1));
+      MSStage& sb = sm.st[stage];
+      const int64_t t0 = (int64_t)tile * kMSTile;
+      const int64_t rem = B - t0;
+      const int len = (int)(rem < kMSTile ? rem : kMSTile);
+      const int lead = t0 > 0 ? kPad : 0;   // tile > 0: halo from the same span
+      const uint32_t bytes = (uint32_t)(len + lead) * 4u;
+      sm.out[stage] = out;
+      sm.t0[stage] = (int)t0;
+      mbar_arrive_tx(&sm.full[stage], 2 * bytes + (uint32_t)sizeof(BankPlan));
+      bulk_g2s(&sb.plan, plan + span, (uint32_t)sizeof(BankPlan), &sm.full[stage]);
+#if PB_MS_L2HINT
+      bulk_g2s_hint(sb.re + kPad - lead, in + t0 - lead, bytes, &sm.full[stage], pol);
+      bulk_g2s_hint(sb.im + kPad - lead, in + B + t0 - lead, bytes, &sm.full[stage], pol);
+#else
+      bulk_g2s(sb.re + kPad - lead, in + t0 - lead, bytes, &sm.full[stage]);
+      bulk_g2s(sb.im + kPad - lead, in + B + t0 - lead, bytes, &sm.full[stage]);
+#endif
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int ct = threadIdx.x;   // 0 .. 32*kMSWarps-1
+  for (int64_t k = 0; k < n_items; ++k) {
+    const int stage = (int)(k % kMSStages);
+    mbar_wait(&sm.full[stage], (uint32_t)((k / kMSStages) & 1));
+    const MSStage& sb = sm.st[stage];
+    const int64_t t0 = sm.t0[stage];
+    const int64_t n0 = t0 + (int64_t)kPerThread * ct;
+    if (sb.plan.have && n0 < B) {
+      float wr[kWin], wi[kWin];
+      {
+        const float4* a = reinterpret_cast<const float4*>(sb.re + kPerThread * ct);
+        const float4* b = reinterpret_cast<const float4*>(sb.im + kPerThread * ct);
+#pragma unroll
+        for (int q = 0; q < kWin / 4; ++q) {
+          const float4 x = a[q], z = b[q];
+          wr[4 * q + 0] = x.x; wr[4 * q + 1] = x.y; wr[4 * q + 2] = x.z; wr[4 * q + 3] = x.w;
+          wi[4 * q + 0] = z.x; wi[4 * q + 1] = z.y; wi[4 * q + 2] = z.z; wi[4 * q + 3] = z.w;
+        }
+      }
+      const bool patch = n0 < kPad;   // pre-span samples: zero here, history in corr
+      if (patch) {
+#pragma unroll
+        for (int i = 0; i < kPad; ++i)
+          if (n0 - kPad + i < 0) wr[i] = wi[i] = 0.0f;
+      }
+      u64 y[kPerThread];
+#ifdef PB_MS_COPYONLY   // profiling variant: the memory pipeline without the FIR
+#pragma unroll
+      for (int v = 0; v < kPerThread; ++v) y[v] = pack2(wr[kPad + v], wi[kPad + v]);
+#else
+      fir8_fma(wr, wi, sb.plan.taps, y);
+#endif
+      if (patch) {
+#pragma unroll
+        for (int v = 0; v < kPerThread; ++v)
+          if (n0 + v < kHist) {
+            float yr, yi;
+            unpack2(y[v], yr, yi);
+            y[v] = pack2(yr + sb.plan.corr[n0 + v].x, yi + sb.plan.corr[n0 + v].y);
+          }
+      }
+      store8(reinterpret_cast<float*>(sm.out[stage]), B, (int)n0, y);
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.empty[stage]);
+  }
+}
+
+#ifndef PB_MERGED_STREAM
+#define PB_MERGED_STREAM 1
+#endif
+
 int launch_merged_bank(const pb_filter_bank& bank, const pb_resolved& res, int64_t B,
                        cudaStream_t st) {
   static BankPlan* plan = nullptr;
@@ -966,7 +1309,11 @@ int launch_merged_bank(const pb_filter_bank& bank, const pb_resolved& res, int64
   }
   dim3 pgrid((res.n_iter + kPlanWarps - 1) / kPlanWarps, res.n_streams);
   const size_t ssmem = plan_stream_smem(res.n_iter, bank.n_branches);
-  if (ssmem <= 48 * 1024) {
+  const size_t parsmem = plan_par_smem(res.n_iter, bank.n_branches);
+  if (PB_PLAN_PAR && parsmem <= 48 * 1024) {
+    dim3 g(res.n_streams, (res.n_iter + kPC - 1) / kPC);
+    bank_plan_par_kernel<<<g, kPlanParThreads, parsmem, st>>>(bank, res, B, plan);
+  } else if (ssmem <= 48 * 1024) {
     bank_plan_stream_kernel<<<res.n_streams, kPlanStreamThreads, ssmem, st>>>(bank, res, B, plan);
   } else {
     // per warp: nb x kTaps float4 taps + nb x 2 x kHist histories (<= 5 float4 per branch)
@@ -974,6 +1321,28 @@ int launch_merged_bank(const pb_filter_bank& bank, const pb_resolved& res, int64
     bank_plan_kernel<<<pgrid, dim3(32, kPlanWarps), psmem, st>>>(bank, res, B, plan);
   }
   PB_LAUNCHED("bank_plan_kernel");
+  if (PB_MERGED_STREAM) {
+    const int tiles = (int)((B + kMSTile - 1) / kMSTile);
+    const size_t smem = sizeof(MSSmem);
+    static int sms = 0, per_sm = 0;
+    if (sms == 0) {
+      PB_CUDA(cudaFuncSetAttribute(bank_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      PB_CUDA(cudaFuncSetAttribute(bank_stream_kernel,
+                                   cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      int dev = 0;
+      PB_CUDA(cudaGetDevice(&dev));
+      PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      PB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bank_stream_kernel,
+                                                            kMSThreads, smem));
+      per_sm = std::max(per_sm, 1);
+    }
+    const int64_t items = spans * tiles;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)sms * per_sm));
+    bank_stream_kernel<<<grid, kMSThreads, smem, st>>>(bank, res, B, plan, tiles);
+    PB_LAUNCHED("bank_stream_kernel");
+    return PB_OK;
+  }
   const int bps = (int)((B / kMPT + kMergedThreads - 1) / kMergedThreads);
   const int64_t blocks = spans * bps;
   if (blocks >= ((int64_t)1 << 31)) return pb::fail(PB_E_UNSUPPORTED, "filter bank: too many spans");

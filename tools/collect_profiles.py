@@ -51,9 +51,9 @@ def last(kname):
     return xs[-1] if xs else None
 
 
-m, p = last("bank_merged_kernel"), last("bank_plan_kernel")
+m, p = last("bank_stream_kernel"), last("bank_plan")
 if m and p:
-    traffic["bank_plan_kernel + bank_merged_kernel"] = \
+    traffic["bank_plan_par_kernel + bank_stream_kernel"] = \
         m["dram_read"] + m["dram_write"] + p["dram_read"] + p["dram_write"]
 e = last("fir_persistent<1, 0>")
 if e:
