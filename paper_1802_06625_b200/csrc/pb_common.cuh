@@ -21,6 +21,38 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 }  // namespace pb
 
+// Programmatic dependent launch for the short kernels of an epoch step: the
+// next kernel of the stream is scheduled while this one runs and parks in
+// griddepcontrol.wait, so the launch latency between the step's kernels
+// overlaps work.  Every PDL kernel calls pb::pdl_wait() before its first
+// global memory access, so stream order semantics are unchanged.
+#ifndef PB_PDL
+#define PB_PDL 1
+#endif
+namespace pb {
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = PB_PDL;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+}  // namespace pb
+
+#define PB_LAUNCH_PDL(kern, grid, block, smem, st, ...)                            \
+  do {                                                                           \
+    cudaError_t err__ = pb::launch_pdl(kern, grid, block, smem, st, __VA_ARGS__); \
+    if (err__ != cudaSuccess) return pb::cuda_fail(err__, #kern);                \
+  } while (0)
+
 #define PB_CUDA(call)                                        \
   do {                                                       \
     cudaError_t err__ = (call);                              \
@@ -37,6 +69,13 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 // ----------------------------------------------------------------- device side
 namespace pb {
+
+// wait for the previous kernel of the stream (PDL), then let the next one be
+// scheduled
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // Index of the span a port uses at iteration n of stream s (pb_span_ref doc).
 __device__ __forceinline__ int64_t span_index(const pb_span_ref& r, const pb_resolved& res,

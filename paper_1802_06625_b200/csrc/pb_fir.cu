@@ -291,6 +291,7 @@ template <bool kBank, int kMath>
 __global__ void __launch_bounds__(kThreads, 4)
 fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actors, int n_actors,
                pb_resolved res, int64_t B, int tiles) {
+  pb::pdl_enter();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const pb_fir_actor* br = kBank ? bank.branches : actors;
@@ -656,6 +657,7 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
 
 __global__ void fir_carry_kernel(const pb_fir_actor* __restrict__ actors, pb_resolved res,
                                  int64_t B) {
+  pb::pdl_enter();
   const pb_fir_actor& a = actors[blockIdx.y];
   const int s = blockIdx.x;
   const int cnt = pb::cond_count(res, a.cond, s);
@@ -687,6 +689,7 @@ constexpr int kPlanWarps = 8;   // spans per block (one warp each)
 
 __global__ void __launch_bounds__(32 * kPlanWarps)
 bank_plan_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan) {
+  pb::pdl_enter();
   const int n = blockIdx.x * kPlanWarps + threadIdx.y, s = blockIdx.y, lane = threadIdx.x;
   if (n >= res.n_iter) return;
   BankPlan& p = plan[(int64_t)s * res.n_iter + n];
@@ -771,6 +774,7 @@ __host__ __device__ inline size_t plan_stream_smem(int n_iter, int nb) {
 
 __global__ void __launch_bounds__(kPlanStreamThreads)
 bank_plan_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan) {
+  pb::pdl_enter();
   const int s = blockIdx.x, E = res.n_iter, tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const pb_fir_actor* br = bank.branches;
@@ -903,6 +907,7 @@ __host__ __device__ inline size_t plan_par_smem(int n_iter, int nb) {
 
 __global__ void __launch_bounds__(kPlanParThreads)
 bank_plan_par_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan) {
+  pb::pdl_enter();
   const int s = blockIdx.x, E = res.n_iter, tid = threadIdx.x;
   const int lo = blockIdx.y * kPC, hi = min(E, lo + kPC), np = hi - lo;
   const int warp = tid >> 5, lane = tid & 31;
@@ -1065,6 +1070,7 @@ constexpr int kMWin = kMPT + kPad;             // window (samples)
 __global__ void __launch_bounds__(kMergedThreads, PB_MERGED_MINB)
 bank_merged_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPlan* plan,
                    int blocks_per_span) {
+  pb::pdl_enter();
   const int64_t span = blockIdx.x / blocks_per_span;
   const int part = (int)(blockIdx.x % blocks_per_span);
   const int s = (int)(span / res.n_iter), n = (int)(span % res.n_iter);
@@ -1181,6 +1187,7 @@ static_assert(sizeof(BankPlan) % 16 == 0, "BankPlan is bulk-copied");
 __global__ void __launch_bounds__(kMSThreads, PB_MS_MINB)
 bank_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPlan* plan,
                    int tiles) {
+  pb::pdl_enter();
   extern __shared__ __align__(128) uint8_t ms_raw[];
   MSSmem& sm = *reinterpret_cast<MSSmem*>(ms_raw);
   if (threadIdx.x == 0) {
@@ -1312,13 +1319,13 @@ int launch_merged_bank(const pb_filter_bank& bank, const pb_resolved& res, int64
   const size_t parsmem = plan_par_smem(res.n_iter, bank.n_branches);
   if (PB_PLAN_PAR && parsmem <= 48 * 1024) {
     dim3 g(res.n_streams, (res.n_iter + kPC - 1) / kPC);
-    bank_plan_par_kernel<<<g, kPlanParThreads, parsmem, st>>>(bank, res, B, plan);
+    PB_LAUNCH_PDL(bank_plan_par_kernel, g, kPlanParThreads, parsmem, st, bank, res, B, plan);
   } else if (ssmem <= 48 * 1024) {
-    bank_plan_stream_kernel<<<res.n_streams, kPlanStreamThreads, ssmem, st>>>(bank, res, B, plan);
+    PB_LAUNCH_PDL(bank_plan_stream_kernel, res.n_streams, kPlanStreamThreads, ssmem, st, bank, res, B, plan);
   } else {
     // per warp: nb x kTaps float4 taps + nb x 2 x kHist histories (<= 5 float4 per branch)
     const size_t psmem = sizeof(float4) * kPlanWarps * bank.n_branches * (kTaps + 5);
-    bank_plan_kernel<<<pgrid, dim3(32, kPlanWarps), psmem, st>>>(bank, res, B, plan);
+    PB_LAUNCH_PDL(bank_plan_kernel, pgrid, dim3(32, kPlanWarps), psmem, st, bank, res, B, plan);
   }
   PB_LAUNCHED("bank_plan_kernel");
   if (PB_MERGED_STREAM) {
@@ -1339,7 +1346,7 @@ int launch_merged_bank(const pb_filter_bank& bank, const pb_resolved& res, int64
     }
     const int64_t items = spans * tiles;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)sms * per_sm));
-    bank_stream_kernel<<<grid, kMSThreads, smem, st>>>(bank, res, B, plan, tiles);
+    PB_LAUNCH_PDL(bank_stream_kernel, grid, kMSThreads, smem, st, bank, res, B, plan, tiles);
     PB_LAUNCHED("bank_stream_kernel");
     return PB_OK;
   }
@@ -1427,7 +1434,7 @@ int pb_fir_carry(const pb_fir_actor* actors, int n_actors, pb_resolved res, int6
                  void* stream) {
   if (n_actors == 0 || res.n_iter == 0) return PB_OK;
   dim3 grid(res.n_streams, n_actors);
-  fir_carry_kernel<<<grid, 32, 0, pb::as_stream(stream)>>>(actors, res, block);
+  PB_LAUNCH_PDL(fir_carry_kernel, grid, 32, 0, pb::as_stream(stream), actors, res, block);
   PB_LAUNCHED("fir_carry_kernel");
   return PB_OK;
 }

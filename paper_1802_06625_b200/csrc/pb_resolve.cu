@@ -30,6 +30,7 @@ constexpr int kScanItems = 4;  // iterations per thread per tile
 // condition's element for every iteration, exclusive scan, compaction.
 __global__ void __launch_bounds__(kScanThreads) resolve_kernel(CondTable table, int cond0,
                                                                pb_resolved res) {
+  pb::pdl_enter();
   const int s = blockIdx.x;
   const int c = cond0 + blockIdx.y;
   const pb_condition& cd = table.c[blockIdx.y];
@@ -91,6 +92,7 @@ __global__ void __launch_bounds__(kScanThreads) resolve_kernel(CondTable table, 
 
 // Eq. 1 recheck: one CTA per (stream, DRP).
 __global__ void eq1_kernel(Eq1Table table, int n_ports, pb_resolved res, int64_t* counters) {
+  pb::pdl_enter();
   const int s = blockIdx.x;
   const pb_eq1_port& p = table.p[blockIdx.y];
   int checks = 0, failures = 0;
@@ -115,6 +117,7 @@ __global__ void eq1_kernel(Eq1Table table, int n_ports, pb_resolved res, int64_t
 // 310-323): producer kernels publish all their spans before the consumer
 // kernels run, so the epoch's peak occupancy is delay + rate*(w + cnt - r).
 __global__ void advance_kernel(RingTable table, int n_rings, pb_resolved res) {
+  pb::pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_rings * res.n_streams) return;
   const int r = i / res.n_streams, s = i % res.n_streams;
@@ -146,7 +149,7 @@ int pb_resolve(const pb_condition* conds, pb_resolved res, void* stream) {
         return pb::fail(PB_E_INVALID, "pb_resolve: bad condition " + std::to_string(c0 + k));
     }
     dim3 grid(res.n_streams, nc);
-    resolve_kernel<<<grid, kScanThreads, 0, pb::as_stream(stream)>>>(t, c0, res);
+    PB_LAUNCH_PDL(resolve_kernel, grid, kScanThreads, 0, pb::as_stream(stream), t, c0, res);
     PB_LAUNCHED("resolve_kernel");
   }
   return PB_OK;
@@ -160,7 +163,7 @@ int pb_eq1_check(const pb_eq1_port* ports, int n_ports, pb_resolved res, int64_t
     Eq1Table t{};
     for (int k = 0; k < np; ++k) t.p[k] = ports[p0 + k];
     dim3 grid(res.n_streams, np);
-    eq1_kernel<<<grid, 128, 0, pb::as_stream(stream)>>>(t, np, res, counters);
+    PB_LAUNCH_PDL(eq1_kernel, grid, 128, 0, pb::as_stream(stream), t, np, res, counters);
     PB_LAUNCHED("eq1_kernel");
   }
   return PB_OK;
@@ -174,7 +177,7 @@ int pb_rings_advance(const pb_ring_advance_t* rings, int n_rings, pb_resolved re
     RingTable t{};
     for (int k = 0; k < nr; ++k) t.r[k] = rings[r0 + k];
     int total = nr * res.n_streams;
-    advance_kernel<<<(total + 127) / 128, 128, 0, pb::as_stream(stream)>>>(t, nr, res);
+    PB_LAUNCH_PDL(advance_kernel, (total + 127) / 128, 128, 0, pb::as_stream(stream), t, nr, res);
     PB_LAUNCHED("advance_kernel");
   }
   return PB_OK;
