@@ -27,6 +27,7 @@ from __future__ import annotations
 import ctypes as C
 import hashlib
 import os
+import queue
 import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
@@ -988,33 +989,74 @@ class DeviceRuntime:
                for a in g.actors if self.plan.roles[a.id] == "source"]
         sinks = [(a, g.fifo_into(PortRef(a.id, a.input_ports[0].id)))
                  for a in g.actors if self.plan.roles[a.id] == "sink"]
-        # Hashing: each host thread owns a fixed set of (sink, stream) digests
-        # and walks the chunks in order (a digest's updates are sequential),
-        # waiting for "chunk c copied out" itself -- no per-chunk fan-out or
-        # join, so deep pipelines do not pay a barrier per chunk.
+        # Hashing: a digest's updates are sequential (chunk c before c+1), so
+        # the unit of work is one (sink, stream) job's next chunk.  A watcher
+        # thread waits for "chunk c copied out" in order and queues every job
+        # that was waiting for it; hashers pop any ready job, hash its next
+        # chunk and requeue it if its following chunk is already out.  Work
+        # is balanced dynamically across the hashing threads (a static split
+        # stalls the whole pipeline on whichever thread loses its core).
         jobs = [(a, f, s) for a, f in sinks for s in range(S)]
         n_thr = max(1, min(len(jobs), int(self.config.host_threads or 16)))
         recorded = [threading.Event() for _ in chunks]     # d2h_ev[c] has been recorded
-        hashed = [0] * len(chunks)                          # hashers done with chunk c
+        hashed = [0] * len(chunks)                          # jobs done with chunk c
         hashed_cv = threading.Condition()
         failure: list[BaseException] = []
+        ready_q: queue.SimpleQueue = queue.SimpleQueue()
+        nxt = [0] * len(jobs)          # next chunk each job hashes
+        idle = [True] * len(jobs)      # job waits for its next chunk to be copied out
+        out_done = [0]                 # chunks [0, out_done) are copied out
+        finished = [0]                 # jobs that hashed every chunk
+        state_lock = threading.Lock()
 
-        def hasher(t):
-            mine = jobs[t::n_thr]
+        def watcher():
             try:
-                for c, (it0, n) in enumerate(chunks):
+                for c in range(len(chunks)):
                     recorded[c].wait()
                     if failure:
-                        return
+                        break
                     _lib.check(lib.pb_event_sync(d2h_ev[c]))
+                    with state_lock:
+                        out_done[0] = c + 1
+                        for j in range(len(jobs)):
+                            if idle[j] and nxt[j] == c:
+                                idle[j] = False
+                                ready_q.put(j)
+            except BaseException as e:  # noqa: BLE001
+                failure.append(e)
+            if failure:
+                stop_hashers()
+
+        def stop_hashers():
+            for _ in range(n_thr):
+                ready_q.put(-1)
+
+        def hasher(t):
+            try:
+                while True:
+                    j = ready_q.get()
+                    if j < 0 or failure:
+                        return
+                    a, f, s = jobs[j]
+                    c = nxt[j]
+                    it0, n = chunks[c]
                     w = it0 % E
-                    for a, f, s in mine:
-                        span = f.rate * f.token_bytes
-                        arr = self.sink_host[f.id][1][:S * E * span].reshape(S, E, span)
-                        data = arr[s, w:w + n].reshape(-1)
-                        self.digests[a.id][s].update(data)
-                        if self.captured is not None:
-                            self.captured[a.id][s] += memoryview(np.ascontiguousarray(data)).cast("B")
+                    span = f.rate * f.token_bytes
+                    arr = self.sink_host[f.id][1][:S * E * span].reshape(S, E, span)
+                    data = arr[s, w:w + n].reshape(-1)
+                    self.digests[a.id][s].update(data)
+                    if self.captured is not None:
+                        self.captured[a.id][s] += memoryview(np.ascontiguousarray(data)).cast("B")
+                    with state_lock:
+                        nxt[j] = c + 1
+                        if c + 1 == len(chunks):
+                            finished[0] += 1
+                            if finished[0] == len(jobs):
+                                stop_hashers()
+                        elif c + 1 < out_done[0]:
+                            ready_q.put(j)
+                        else:
+                            idle[j] = True
                     with hashed_cv:
                         hashed[c] += 1
                         hashed_cv.notify_all()
@@ -1025,11 +1067,12 @@ class DeviceRuntime:
 
         def wait_hashed(c):
             with hashed_cv:
-                hashed_cv.wait_for(lambda: hashed[c] == n_thr or failure)
+                hashed_cv.wait_for(lambda: hashed[c] == len(jobs) or failure)
             if failure:
                 raise failure[0]
 
         hashers = [threading.Thread(target=hasher, args=(t,), daemon=True) for t in range(n_thr)]
+        hashers.append(threading.Thread(target=watcher, daemon=True))
         for th in hashers:
             th.start()
         try:
@@ -1114,6 +1157,8 @@ class DeviceRuntime:
                 failure.append(RuntimeError("pipeline aborted"))
             for ev in recorded:
                 ev.set()
+            if failure:
+                stop_hashers()
             for th in hashers:
                 th.join()
             lib.pb_stream_sync(self.copy_in)
