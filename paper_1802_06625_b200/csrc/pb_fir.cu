@@ -1160,11 +1160,15 @@ bank_merged_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
 #define PB_MS_L2HINT 1
 #endif
 #ifndef PB_MS_STAGES
-#define PB_MS_STAGES 8
+#define PB_MS_STAGES 5
 #endif
 constexpr int kMSWarps = PB_MS_WARPS;
 constexpr int kMSThreads = 32 * (kMSWarps + 1);
-constexpr int kMSTile = 32 * kMSWarps * kPerThread;   // samples per item
+#ifndef PB_MS_PASSES   // consumer passes per tile (8 outputs per thread each)
+#define PB_MS_PASSES 2
+#endif
+constexpr int kMSPass = 32 * kMSWarps * kPerThread;   // samples per consumer pass
+constexpr int kMSTile = kMSPass * PB_MS_PASSES;       // samples per item
 constexpr int kMSStages = PB_MS_STAGES;
 
 struct __align__(16) MSStage {
@@ -1258,12 +1262,15 @@ bank_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
     mbar_wait(&sm.full[stage], (uint32_t)((k / kMSStages) & 1));
     const MSStage& sb = sm.st[stage];
     const int64_t t0 = sm.t0[stage];
-    const int64_t n0 = t0 + (int64_t)kPerThread * ct;
+#pragma unroll 1
+    for (int pass = 0; pass < PB_MS_PASSES; ++pass) {
+    const int off = pass * kMSPass + kPerThread * ct;   // first output, relative to t0
+    const int64_t n0 = t0 + off;
     if (sb.plan.have && n0 < B) {
       float wr[kWin], wi[kWin];
       {
-        const float4* a = reinterpret_cast<const float4*>(sb.re + kPerThread * ct);
-        const float4* b = reinterpret_cast<const float4*>(sb.im + kPerThread * ct);
+        const float4* a = reinterpret_cast<const float4*>(sb.re + off);
+        const float4* b = reinterpret_cast<const float4*>(sb.im + off);
 #pragma unroll
         for (int q = 0; q < kWin / 4; ++q) {
           const float4 x = a[q], z = b[q];
@@ -1294,6 +1301,7 @@ bank_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
           }
       }
       store8(reinterpret_cast<float*>(sm.out[stage]), B, (int)n0, y);
+    }
     }
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.empty[stage]);
