@@ -637,6 +637,21 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {e!r}"}
 
+    # output gather (outside the timed region): every rank's per-stream reports
+    # of the last e2e run to rank 0 through the process group -- NCCL over
+    # NVLink on a multi-GPU box -- the only exchange the sharded path has
+    gather = None if dist is not None else {"streams": S, "backend": "none (one rank)"}
+    if reps is not None and dist is not None:
+        from paper_1802_06625_b200.sharding import gather_reports
+        barrier()
+        t0 = time.perf_counter()
+        try:
+            allr = gather_reports(reps, range(rank * S, rank * S + S), S * world)
+            gather = {"streams": len(allr) if allr is not None else None,
+                      "backend": dist.get_backend(), "seconds": time.perf_counter() - t0}
+        except Exception as e:  # noqa: BLE001
+            gather = {"error": f"{type(e).__name__}: {e}"}
+
     cnn = None
     if not args.skip_cnn:
         rt.close()
@@ -665,6 +680,7 @@ def main():
                                 "sink D2H, SHA-256 per stream"},
             "gpu_launches": launches,
             "parity_stream0": parity,
+            "output_gather": gather,
             "cpu_baseline": cpu,
             "cnn": cnn,
         }
