@@ -337,6 +337,13 @@ def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
 
     conv_flops = vision.flops_per_frame() - 18432 * 100 * 2
     conv_ms = kern.get("conv_l1", 0.0) + kern.get("conv_l2", 0.0)
+    conv_traffic = None
+    try:   # per-launch DRAM bytes of the two conv kernels (same 6144-frame launch, ncu)
+        tr = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        if frames == 6144:
+            conv_traffic = tr["conv_pool_kernel<0, 3>"] + tr["conv_pool_kernel<1, 32>"]
+    except Exception:  # noqa: BLE001
+        conv_traffic = None
     achieved = frames * conv_flops / (conv_ms / 1e3) / 1e12 if conv_ms else None
     peak = float(peaks.get("bf16_tflops_sustained", 0) or 0)
     peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained (measured)" if peak else \
@@ -367,11 +374,15 @@ def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
                    "l2": f"inputs {frames * vision.FRAME_BYTES / 1e6:.0f} MB/GPU > L2; no flush"},
         "kernel_ms": kern,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "frac": achieved / peak if achieved else None, "traffic": conv_traffic,
                      "kernel": "conv_pool_kernel (layers 1+2)", "kernel_ms": conv_ms,
                      "algorithmic_flops_per_frame": conv_flops, "peak_source": peak_src,
-                     "note": "useful FLOPs; bf16x3 issues 3 MMA products per useful one, "
-                             "layer 2 at N=32/64 is shared-memory-read bound (tools/conv_probe)"},
+                     "issued_tflops": 3 * achieved if achieved else None,
+                     "issued_frac": 3 * achieved / peak if achieved else None,
+                     "note": "useful FLOPs; bf16x3 issues 3 MMA products per useful one "
+                             "(issued_*: the tensor pipe's bf16 work), layer 2 at N=32/64 is "
+                             "shared-memory-read bound (tools/conv_probe); traffic: DRAM bytes "
+                             "of both conv launches from profiles/ncu_traffic.json"},
         "e2e": {"value": frames * world / e2e_s, "unit": "frames/s",
                 "h2d_bytes_per_step": frames * vision.FRAME_BYTES,
                 "d2h_bytes_per_step": frames * vision.N_CLASSES * 4,
