@@ -787,11 +787,13 @@ int launch_conv(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t
   using Cfg = ConvCfg<MODE, CIN>;
   const size_t smem = 1024 + Cfg::SMEM + sizeof(ConvBars);
   static_assert(1024 + Cfg::SMEM + sizeof(ConvBars) <= 227 * 1024, "conv smem");
-  static bool configured = false;
-  if (!configured) {
+  const int dev = pb::device();
+  if (dev < 0) return PB_E_CUDA;
+  static bool configured[pb::kMaxDevices] = {};
+  if (!configured[dev]) {
     PB_CUDA(cudaFuncSetAttribute(conv_pool_kernel<MODE, CIN>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
+    configured[dev] = true;
   }
   const int Ho = actor.h + 2 * actor.pad - 4, Wo = actor.w + 2 * actor.pad - 4;
   const int64_t per_frame = (int64_t)((Ho + kTH - 1) / kTH) * ((Wo + Cfg::ST * kTW - 1) / (Cfg::ST * kTW));
@@ -820,14 +822,11 @@ int launch_conv(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t
                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return pb::fail(PB_E_CUDA, "conv: cuTensorMapEncodeTiled failed");
   }
-  static UnitSpans* units = nullptr;
-  static int64_t units_n = 0;
   const int64_t n_units = (int64_t)res.n_streams * res.n_iter;
-  if (n_units > units_n) {
-    if (units) PB_CUDA(cudaFree(units));
-    PB_CUDA(cudaMalloc(&units, sizeof(UnitSpans) * n_units));
-    units_n = n_units;
-  }
+  UnitSpans* units = nullptr;
+  int rc = pb::scratch(pb::kScratchConvUnits, sizeof(UnitSpans) * n_units,
+                       reinterpret_cast<void**>(&units));
+  if (rc) return rc;
   conv_units_kernel<<<(unsigned)((n_units + 255) / 256), 256, 0, st>>>(actor, res, units);
   PB_LAUNCHED("conv_units_kernel");
   conv_pool_kernel<MODE, CIN><<<grid, kConvThreads, smem, st>>>(actor, res, units, tmap);
@@ -1117,12 +1116,11 @@ int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream) {
   const int Ho = actor.h + 2 * actor.pad - 4, Wo = actor.w + 2 * actor.pad - 4;
   if (Ho < 2 || Wo < 2 || Ho % 2 || Wo % 2)
     return pb::fail(PB_E_UNSUPPORTED, "conv: output must be even-sized for the 2x2 pool");
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    PB_CUDA(cudaGetDevice(&dev));
-    PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  const int dev = pb::device();
+  if (dev < 0) return PB_E_CUDA;
+  static int sms_d[pb::kMaxDevices] = {};
+  int& sms = sms_d[dev];
+  if (sms == 0) PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   cudaStream_t st = pb::as_stream(stream);
   switch (actor.cin) {
     case 3: return launch_conv<0, 3>(actor, res, st, sms);
@@ -1136,16 +1134,15 @@ int pb_fire_dense(pb_dense_actor actor, pb_resolved res, void* stream) {
   if (res.n_iter == 0) return PB_OK;
   if (actor.nout > kDN || actor.nin % kDKC != 0)
     return pb::fail(PB_E_UNSUPPORTED, "dense: nout <= 112 and nin a multiple of 64");
-  static int sms = 0;
-  static float* partial = nullptr;
-  static size_t partial_bytes = 0;
-  static int* counters = nullptr;
-  static int counters_n = 0;
+  const int dev = pb::device();
+  if (dev < 0) return PB_E_CUDA;
+  static int sms_d[pb::kMaxDevices] = {};
+  int& sms = sms_d[dev];
+  float* partial = nullptr;
+  int* counters = nullptr;
   if (sms == 0) {
     PB_CUDA(cudaFuncSetAttribute(dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sizeof(DenseSmem) + 1024)));
-    int dev = 0;
-    PB_CUDA(cudaGetDevice(&dev));
     PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const int64_t rows = (int64_t)res.n_streams * res.n_iter * actor.frames;
@@ -1157,17 +1154,12 @@ int pb_fire_dense(pb_dense_actor actor, pb_resolved res, void* stream) {
   cudaStream_t st = pb::as_stream(stream);
   if (splits > 1) {
     const size_t need = (size_t)splits * m_tiles * 128 * kDN * sizeof(float);
-    if (need > partial_bytes) {
-      if (partial) PB_CUDA(cudaFree(partial));
-      PB_CUDA(cudaMalloc(&partial, need));
-      partial_bytes = need;
-    }
-    if (m_tiles > counters_n) {
-      if (counters) PB_CUDA(cudaFree(counters));
-      PB_CUDA(cudaMalloc(&counters, sizeof(int) * m_tiles));
-      PB_CUDA(cudaMemsetAsync(counters, 0, sizeof(int) * m_tiles, st));
-      counters_n = m_tiles;
-    }
+    int rc = pb::scratch(pb::kScratchDensePartial, need, reinterpret_cast<void**>(&partial));
+    if (rc) return rc;
+    // arrival counters: zero when allocated, left zero by each launch's last CTA
+    rc = pb::scratch(pb::kScratchDenseCounters, sizeof(int) * m_tiles,
+                     reinterpret_cast<void**>(&counters), true, st);
+    if (rc) return rc;
   }
   dim3 grid(m_tiles, splits);
   dense_kernel<<<grid, kDThreads, sizeof(DenseSmem) + 1024, st>>>(actor, res, partial, counters,

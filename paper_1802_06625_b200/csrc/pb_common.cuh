@@ -17,6 +17,18 @@ int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t err, const char* what);
 void count_launch(int n = 1);
 
+// Per-device library state (one process may drive several devices in turn):
+// the current device's ordinal, and grow-only scratch buffers owned by the
+// library, one per (device, slot).  Launches on one device are stream-ordered
+// by the caller (one compute stream per runtime).
+constexpr int kMaxDevices = 16;
+int device();   // current device ordinal, < kMaxDevices, or -1 on error (pb_last_error set)
+enum ScratchSlot { kScratchBankPlan = 0, kScratchConvUnits, kScratchDensePartial,
+                   kScratchDenseCounters, kScratchSlots };
+// at least `bytes` of device memory for `slot` on the current device; newly
+// allocated memory is zeroed on `st` when zero_new
+int scratch(int slot, size_t bytes, void** out, bool zero_new = false, cudaStream_t st = 0);
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 }  // namespace pb

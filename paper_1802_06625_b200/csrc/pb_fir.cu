@@ -1314,14 +1314,13 @@ bank_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
 
 int launch_merged_bank(const pb_filter_bank& bank, const pb_resolved& res, int64_t B,
                        cudaStream_t st) {
-  static BankPlan* plan = nullptr;
-  static int64_t plan_n = 0;
   const int64_t spans = (int64_t)res.n_streams * res.n_iter;
-  if (spans > plan_n) {
-    if (plan) PB_CUDA(cudaFree(plan));
-    PB_CUDA(cudaMalloc(&plan, sizeof(BankPlan) * spans));
-    plan_n = spans;
-  }
+  BankPlan* plan = nullptr;
+  int rc = pb::scratch(pb::kScratchBankPlan, sizeof(BankPlan) * spans,
+                       reinterpret_cast<void**>(&plan));
+  if (rc) return rc;
+  const int dev = pb::device();
+  if (dev < 0) return PB_E_CUDA;
   dim3 pgrid((res.n_iter + kPlanWarps - 1) / kPlanWarps, res.n_streams);
   const size_t ssmem = plan_stream_smem(res.n_iter, bank.n_branches);
   const size_t parsmem = plan_par_smem(res.n_iter, bank.n_branches);
@@ -1339,14 +1338,14 @@ int launch_merged_bank(const pb_filter_bank& bank, const pb_resolved& res, int64
   if (PB_MERGED_STREAM) {
     const int tiles = (int)((B + kMSTile - 1) / kMSTile);
     const size_t smem = sizeof(MSSmem);
-    static int sms = 0, per_sm = 0;
+    static int sms_d[pb::kMaxDevices] = {}, per_sm_d[pb::kMaxDevices] = {};
+    int& sms = sms_d[dev];
+    int& per_sm = per_sm_d[dev];
     if (sms == 0) {
       PB_CUDA(cudaFuncSetAttribute(bank_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
       PB_CUDA(cudaFuncSetAttribute(bank_stream_kernel,
                                    cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      int dev = 0;
-      PB_CUDA(cudaGetDevice(&dev));
       PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       PB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bank_stream_kernel,
                                                             kMSThreads, smem));
@@ -1378,16 +1377,14 @@ int launch_variant(const pb_filter_bank& bank, const pb_fir_actor* actors, int n
                    const pb_resolved& res, int64_t B, cudaStream_t st) {
   const int tiles = (int)((B + kTile - 1) / kTile);
   const size_t smem = sizeof(Smem);
-  static bool configured = false;
-  if (!configured) {
+  const int dev = pb::device();
+  if (dev < 0) return PB_E_CUDA;
+  static int sms_d[pb::kMaxDevices] = {}, per_sm_d[pb::kMaxDevices] = {};
+  int& sms = sms_d[dev];
+  int& per_sm = per_sm_d[dev];
+  if (sms == 0) {
     PB_CUDA(cudaFuncSetAttribute(fir_persistent<kBank, kMath>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
-  static int sms = 0, per_sm = 0;
-  if (sms == 0) {
-    int dev = 0;
-    PB_CUDA(cudaGetDevice(&dev));
     PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     PB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fir_persistent<kBank, kMath>,
                                                           kThreads, smem));

@@ -27,6 +27,40 @@ int cuda_fail(cudaError_t err, const char* what) {
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+int device() {
+  int dev = 0;
+  const cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) {
+    cuda_fail(err, "cudaGetDevice");
+    return -1;
+  }
+  if (dev >= kMaxDevices) {
+    fail(PB_E_UNSUPPORTED, "device ordinal " + std::to_string(dev) + " >= " +
+                               std::to_string(kMaxDevices));
+    return -1;
+  }
+  return dev;
+}
+
+int scratch(int slot, size_t bytes, void** out, bool zero_new, cudaStream_t st) {
+  static std::mutex mu;
+  static void* bufs[kMaxDevices][kScratchSlots] = {};
+  static size_t sizes[kMaxDevices][kScratchSlots] = {};
+  const int dev = device();
+  if (dev < 0) return PB_E_CUDA;
+  std::lock_guard<std::mutex> lock(mu);
+  if (bytes > sizes[dev][slot]) {
+    if (bufs[dev][slot]) PB_CUDA(cudaFree(bufs[dev][slot]));   // synchronising
+    bufs[dev][slot] = nullptr;
+    sizes[dev][slot] = 0;
+    PB_CUDA(cudaMalloc(&bufs[dev][slot], bytes));
+    sizes[dev][slot] = bytes;
+    if (zero_new) PB_CUDA(cudaMemsetAsync(bufs[dev][slot], 0, bytes, st));
+  }
+  *out = bufs[dev][slot];
+  return PB_OK;
+}
+
 }  // namespace pb
 
 using pb::fail;
