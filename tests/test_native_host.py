@@ -187,3 +187,16 @@ def test_no_fma_in_fir_kernels():
                 bad.append((fn, line.strip()))
     assert len(seen) >= 6 and not bad, bad[:5]
     assert "FMUL2" in sass and "FADD2" in sass
+
+
+def test_no_cpu_fallback_without_a_device(tmp_path):
+    """The product path has no CPU fallback: without a visible CUDA device the
+    drop-in run() raises DeviceUnavailable instead of computing anything."""
+    if _lib.device_count() > 0:
+        pytest.skip("a CUDA device is visible")
+    from paper_1802_06625_b200 import DeviceUnavailable, RuntimeConfig, run
+    from paper_1802_06625_b200.apps import predistortion as pd
+    p = tmp_path / "input.bin"
+    p.write_bytes(pd.make_input(11, 4))
+    with pytest.raises(DeviceUnavailable):
+        run(pd.build_description(256, 4, str(p)), config=RuntimeConfig(source_firings=4, seed=11))
