@@ -16,6 +16,9 @@
 namespace {
 
 constexpr int kImgThreads = 256;
+#ifndef PB_IMG_FAST
+#define PB_IMG_FAST 1
+#endif
 constexpr int kMaxSide = 128;
 
 __global__ void __launch_bounds__(kImgThreads)
@@ -86,6 +89,161 @@ image_kernel(pb_image_actor a, pb_resolved res) {
   }
 }
 
+// Word-parallel path for power-of-two sides 8..128 (64 in the reference
+// app): a thread owns 4-pixel words, 128 threads per firing.
+//   blur: horizontal pass with __dp4a over byte windows assembled by
+//     __byte_perm (taps 1 4 6 4 | 1), int16 rows in shared memory, then the
+//     vertical pass on two packed 16-bit lanes per register (max 255*16*16 =
+//     65280 fits a lane) -- the same integers as the reference's row-then-
+//     column int32 sums, so the >> 8 is the same floor;
+//   diff: __vabsdiffu4 + __vcmpgtu4 on 16 pixels per thread;
+//   median: the 7-exchange network of the generic kernel on 4 byte lanes at
+//     once (__vminu4 / __vmaxu4), left/right neighbours by __byte_perm.
+constexpr int kFastThreads = 128;
+
+// median of five per 16-bit lane (byte values), 10 VIMNMX.U16x2:
+// median3(e, max(min(a,b), min(c,d)), min(max(a,b), max(c,d)))
+__device__ __forceinline__ uint32_t med5_u16(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                             uint32_t e) {
+  const uint32_t f = __vmaxu2(__vminu2(a, b), __vminu2(c, d));
+  const uint32_t g = __vminu2(__vmaxu2(a, b), __vmaxu2(c, d));
+  return __vmaxu2(__vminu2(e, f), __vminu2(__vmaxu2(e, f), g));
+}
+// byte-wise median of five words: even and odd bytes as two u16x2 lane sets
+__device__ __forceinline__ uint32_t med5(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                         uint32_t e) {
+  constexpr uint32_t M = 0x00FF00FFu;
+  const uint32_t ev = med5_u16(a & M, b & M, c & M, d & M, e & M);
+  const uint32_t od = med5_u16((a >> 8) & M, (b >> 8) & M, (c >> 8) & M, (d >> 8) & M,
+                               (e >> 8) & M);
+  return ev | (od << 8);
+}
+
+// frames per CTA: the span addressing of each frame (ring index arithmetic)
+// is done once per frame by one thread and shared, not by every thread
+constexpr int kFPC = 4;
+
+struct FramePtrs {
+  const uint8_t* in0;
+  const uint8_t* in1;
+  uint32_t* o0;
+  uint32_t* o1;
+};
+
+__global__ void __launch_bounds__(kFastThreads)
+image_fast_kernel(pb_image_actor a, pb_resolved res, int lw) {
+  const int s = blockIdx.y, tid = threadIdx.x;
+  const int side = a.side, W = 1 << lw, nw = side * W;
+  __shared__ FramePtrs fp[kFPC];
+  __shared__ int n_frames;
+  if (tid < kFPC) {
+    const int cnt = pb::cond_count(res, a.cond, s);
+    const int j = blockIdx.x * kFPC + tid;
+    if (tid == 0) n_frames = max(0, min(kFPC, cnt - (int)blockIdx.x * kFPC));
+    if (j < cnt) {
+      const int n = pb::firing_iter(res, a.cond, s, j);
+      FramePtrs f{pb::span_ptr(a.in[0], res, s, n),
+                  a.op == PB_IMG_DIFF ? pb::span_ptr(a.in[1], res, s, n) : nullptr, nullptr,
+                  nullptr};
+      // live outputs (at most two on this path: blur feeds f_cur and the
+      // delayed f_prev)
+      for (int k = 0; k < a.n_out; ++k)
+        if (pb::active(res, a.out[k].act_cond, s, n)) {
+          uint32_t* o = reinterpret_cast<uint32_t*>(pb::span_ptr(a.out[k], res, s, n));
+          if (!f.o0) f.o0 = o;
+          else f.o1 = o;
+        }
+      fp[tid] = f;
+    }
+  }
+  __syncthreads();
+  const int nf = n_frames;
+  extern __shared__ uint4 img_smem[];
+  uint32_t* fr = reinterpret_cast<uint32_t*>(img_smem);            // [side][W] words
+  uint32_t* hs = fr + nw;                                          // [side][W][2] int16 pairs
+  const int xw0 = tid & (W - 1), rows = kFastThreads >> lw;
+  for (int f = 0; f < nf; ++f) {
+    const FramePtrs P = fp[f];
+    uint32_t* const o0 = P.o0;
+    uint32_t* const o1 = P.o1;
+    auto put = [&](int idx, uint32_t w) {
+      if (o0) o0[idx] = w;
+      if (o1) o1[idx] = w;
+    };
+    if (a.op == PB_IMG_DIFF) {
+      const uint4* c4 = reinterpret_cast<const uint4*>(P.in0);
+      const uint4* p4 = reinterpret_cast<const uint4*>(P.in1);
+      const int thr = a.threshold;
+      const uint32_t t4 = (uint32_t)min(max(thr, 0), 255) * 0x01010101u;
+      auto m4 = [&](uint32_t c, uint32_t p) -> uint32_t {
+        if (thr < 0) return 0xFFFFFFFFu;
+        if (thr >= 255) return 0u;
+        return __vcmpgtu4(__vabsdiffu4(c, p), t4);
+      };
+      for (int i = tid; i < nw / 4; i += kFastThreads) {
+        const uint4 c = c4[i], p = p4[i];
+        const uint4 m = make_uint4(m4(c.x, p.x), m4(c.y, p.y), m4(c.z, p.z), m4(c.w, p.w));
+        if (o0) reinterpret_cast<uint4*>(o0)[i] = m;
+        if (o1) reinterpret_cast<uint4*>(o1)[i] = m;
+      }
+      continue;
+    }
+    if (f > 0) __syncthreads();   // the previous frame's readers are done with fr / hs
+    for (int i = tid; i < nw / 4; i += kFastThreads)
+      img_smem[i] = reinterpret_cast<const uint4*>(P.in0)[i];
+    __syncthreads();
+    if (a.op == PB_IMG_BLUR) {
+      constexpr uint32_t K4 = 0x04060401u;   // taps 1 4 6 4 on bytes 0..3 of a window
+      for (int y = tid >> lw; y < side; y += rows) {
+        const int xw = xw0;
+        const uint32_t* row = fr + y * W;
+        const uint32_t wa = xw > 0 ? row[xw - 1] : 0u, wb = row[xw];
+        const uint32_t wc = xw < W - 1 ? row[xw + 1] : 0u;
+        const uint32_t h0 = __dp4a(__byte_perm(wa, wb, 0x5432), K4, (wb >> 16) & 0xFFu);
+        const uint32_t h1 = __dp4a(__byte_perm(wa, wb, 0x6543), K4, wb >> 24);
+        const uint32_t h2 = __dp4a(wb, K4, wc & 0xFFu);
+        const uint32_t h3 = __dp4a(__byte_perm(wb, wc, 0x4321), K4, (wc >> 8) & 0xFFu);
+        reinterpret_cast<uint2*>(hs)[y * W + xw] = make_uint2(h0 | (h1 << 16), h2 | (h3 << 16));
+      }
+      __syncthreads();
+      for (int y = tid >> lw; y < side; y += rows) {
+        const int xw = xw0;
+        const uint32_t orig = fr[y * W + xw];
+        uint32_t word = orig;
+        if (y >= 2 && y < side - 2) {
+          const uint2* h = reinterpret_cast<const uint2*>(hs) + (y - 2) * W + xw;
+          const uint2 r0 = h[0], r1 = h[W], r2 = h[2 * W], r3 = h[3 * W], r4 = h[4 * W];
+          uint32_t lo = r0.x + 4u * r1.x + 6u * r2.x + 4u * r3.x + r4.x;
+          uint32_t hi = r0.y + 4u * r1.y + 6u * r2.y + 4u * r3.y + r4.y;
+          lo = (lo >> 8) & 0x00FF00FFu;
+          hi = (hi >> 8) & 0x00FF00FFu;
+          word = __byte_perm(lo, hi, 0x6420);
+          if (xw == 0) word = __byte_perm(word, orig, 0x3254);       // x = 0, 1 pass through
+          if (xw == W - 1) word = __byte_perm(word, orig, 0x7610);   // x = side-2, side-1
+        }
+        put(y * W + xw, word);
+      }
+      continue;
+    }
+    // PB_IMG_MEDIAN
+    for (int y = tid >> lw; y < side; y += rows) {
+      const int xw = xw0;
+      const uint32_t c = fr[y * W + xw];
+      uint32_t word = c;
+      if (y >= 1 && y < side - 1) {
+        const uint32_t up = fr[(y - 1) * W + xw], dn = fr[(y + 1) * W + xw];
+        const uint32_t pl = xw > 0 ? fr[y * W + xw - 1] : 0u;
+        const uint32_t nx = xw < W - 1 ? fr[y * W + xw + 1] : 0u;
+        const uint32_t lf = __byte_perm(pl, c, 0x6543), rt = __byte_perm(c, nx, 0x4321);
+        word = med5(c, up, dn, lf, rt);
+        if (xw == 0) word = __byte_perm(word, c, 0x3214);       // x = 0 passes through
+        if (xw == W - 1) word = __byte_perm(word, c, 0x7210);   // x = side-1
+      }
+      put(y * W + xw, word);
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -99,6 +257,24 @@ int pb_fire_image(pb_image_actor actor, pb_resolved res, void* stream) {
       actor.n_out > PB_MAX_PORTS)
     return pb::fail(PB_E_INVALID, "image actor: bad op or output count");
   dim3 grid(res.n_iter, res.n_streams);
+  const int side = actor.side;
+  if (PB_IMG_FAST && side >= 8 && (side & (side - 1)) == 0 && actor.n_out <= 2) {
+    int lw = 0;
+    while ((4 << lw) < side) ++lw;   // words per row = side / 4 = 1 << lw
+    const size_t smem = actor.op == PB_IMG_DIFF ? 0 : (size_t)side * side * 3;
+    static bool attr[pb::kMaxDevices] = {};   // side 128: 48 KB dynamic + the static part
+    const int dev = pb::device();
+    if (dev < 0) return PB_E_CUDA;
+    if (!attr[dev]) {
+      PB_CUDA(cudaFuncSetAttribute(image_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   3 * kMaxSide * kMaxSide));
+      attr[dev] = true;
+    }
+    dim3 fgrid((res.n_iter + kFPC - 1) / kFPC, res.n_streams);
+    image_fast_kernel<<<fgrid, kFastThreads, smem, pb::as_stream(stream)>>>(actor, res, lw);
+    PB_LAUNCHED("image_fast_kernel");
+    return PB_OK;
+  }
   image_kernel<<<grid, kImgThreads, 0, pb::as_stream(stream)>>>(actor, res);
   PB_LAUNCHED("image_kernel");
   return PB_OK;
