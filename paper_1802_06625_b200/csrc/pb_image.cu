@@ -162,6 +162,7 @@ image_fast_kernel(pb_image_actor a, pb_resolved res, int lw) {
   uint32_t* fr = reinterpret_cast<uint32_t*>(img_smem);            // [side][W] words
   uint32_t* hs = fr + nw;                                          // [side][W][2] int16 pairs
   const int xw0 = tid & (W - 1), rows = kFastThreads >> lw;
+  uint4 pre[2];
   for (int f = 0; f < nf; ++f) {
     const FramePtrs P = fp[f];
     uint32_t* const o0 = P.o0;
@@ -188,9 +189,30 @@ image_fast_kernel(pb_image_actor a, pb_resolved res, int lw) {
       }
       continue;
     }
+    // this frame into shared memory: its words were loaded into registers
+    // while the previous frame was computed (side <= 64: at most 2 uint4 per
+    // thread; larger sides load here)
     if (f > 0) __syncthreads();   // the previous frame's readers are done with fr / hs
-    for (int i = tid; i < nw / 4; i += kFastThreads)
-      img_smem[i] = reinterpret_cast<const uint4*>(P.in0)[i];
+    if (nw / 4 <= 2 * kFastThreads) {
+      if (f == 0) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          if (tid + q * kFastThreads < nw / 4)
+            pre[q] = reinterpret_cast<const uint4*>(P.in0)[tid + q * kFastThreads];
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (tid + q * kFastThreads < nw / 4) img_smem[tid + q * kFastThreads] = pre[q];
+      if (f + 1 < nf) {   // next frame's words in flight during this frame's math
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          if (tid + q * kFastThreads < nw / 4)
+            pre[q] = reinterpret_cast<const uint4*>(fp[f + 1].in0)[tid + q * kFastThreads];
+      }
+    } else {
+      for (int i = tid; i < nw / 4; i += kFastThreads)
+        img_smem[i] = reinterpret_cast<const uint4*>(P.in0)[i];
+    }
     __syncthreads();
     if (a.op == PB_IMG_BLUR) {
       constexpr uint32_t K4 = 0x04060401u;   // taps 1 4 6 4 on bytes 0..3 of a window
