@@ -110,6 +110,92 @@ __global__ void path_merge_kernel(pb_path_merge_actor a, pb_resolved res) {
   }
 }
 
+// MatMul.fire for N*N/4 <= 32 dividing 32 (the reference's 8x8: 16 lanes
+// per firing, two firings per warp): the group's first lane resolves the
+// firing's spans once; each lane computes 4 consecutive outputs of one row
+// (acc = 0, then acc + w[i][k] * x[k][j] in ascending k, every product and
+// sum rounded) from float4 rows of x.
+__global__ void __launch_bounds__(256)
+matmul_packed_kernel(pb_matmul_actor a, pb_resolved res, int L) {
+  const int s = blockIdx.y, lane = threadIdx.x & 31, N = a.n;
+  __shared__ float w[32 * 4];   // N*N <= 128
+  for (int e = threadIdx.x; e < N * N; e += blockDim.x) w[e] = a.weights[e];
+  __syncthreads();
+  const int fpw = 32 / L;
+  const int g = lane / L, sub = lane - g * L;
+  const int j = ((int)blockIdx.x * 8 + (threadIdx.x >> 5)) * fpw + g;   // firing index
+  const int leader = g * L;
+  const unsigned grp = (L == 32 ? 0xffffffffu : ((1u << L) - 1u) << leader);
+  if (j >= pb::cond_count(res, a.cond, s)) return;   // whole lane groups leave together
+  const float* x = nullptr;
+  float* out = nullptr;
+  if (sub == 0) {
+    const int n = pb::firing_iter(res, a.cond, s, j);
+    x = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n));
+    out = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
+  }
+  x = reinterpret_cast<const float*>(__shfl_sync(grp, reinterpret_cast<unsigned long long>(x), leader));
+  out = reinterpret_cast<float*>(__shfl_sync(grp, reinterpret_cast<unsigned long long>(out), leader));
+  const int e0 = 4 * sub, i = e0 / N, c0 = e0 - i * N;
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  for (int k = 0; k < N; ++k) {
+    const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k * N + c0));
+    const float wk = w[i * N + k];
+    acc[0] = __fadd_rn(acc[0], __fmul_rn(wk, xv.x));
+    acc[1] = __fadd_rn(acc[1], __fmul_rn(wk, xv.y));
+    acc[2] = __fadd_rn(acc[2], __fmul_rn(wk, xv.z));
+    acc[3] = __fadd_rn(acc[3], __fmul_rn(wk, xv.w));
+  }
+  reinterpret_cast<float4*>(out)[sub] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+}
+
+// Packed form for tokens of 16..512 bytes in 16-byte units (the reference's
+// 256-B matrices: 16 lanes per firing, two firings per warp): the first lane
+// of each firing's lane group resolves the firing (activity, live input,
+// span addresses) once and broadcasts it; every lane moves one float4.
+__global__ void __launch_bounds__(256)
+path_merge_packed_kernel(pb_path_merge_actor a, pb_resolved res, int L) {
+  const int s = blockIdx.y, lane = threadIdx.x & 31;
+  const int fpw = 32 / L;                                // firings per warp
+  const int g = lane / L, sub = lane - g * L;
+  const int n = ((int)blockIdx.x * 8 + (threadIdx.x >> 5)) * fpw + g;
+  const int leader = g * L;
+  const unsigned grp = (L == 32 ? 0xffffffffu : ((1u << L) - 1u) << leader);
+  if (n >= res.n_iter) return;   // whole lane groups leave together
+  int state = 0;                 // 0: idle, 1: forward, 2: forward + marker, 3: error
+  const float4* x = nullptr;
+  float4* out = nullptr;
+  if (sub == 0 && pb::active(res, a.cond, s, n)) {
+    int live = -1, n_live = 0;
+    for (int p = 0; p < a.n_in; ++p)
+      if (pb::active(res, a.in[p].act_cond, s, n)) {
+        live = p;
+        ++n_live;
+      }
+    if (n_live != 1) {
+      state = 3;
+    } else {
+      x = reinterpret_cast<const float4*>(pb::span_ptr(a.in[live], res, s, n));
+      out = reinterpret_cast<float4*>(pb::span_ptr(a.out, res, s, n));
+      state = live == a.bypass_index ? 2 : 1;
+    }
+  }
+  state = __shfl_sync(grp, state, leader);
+  if (state == 0) return;
+  if (state == 3) {
+    if (sub == 0) atomicExch(a.error_flag, 1);
+    return;
+  }
+  x = reinterpret_cast<const float4*>(__shfl_sync(grp, reinterpret_cast<unsigned long long>(x), leader));
+  out = reinterpret_cast<float4*>(__shfl_sync(grp, reinterpret_cast<unsigned long long>(out), leader));
+  float4 v = x[sub];
+  if (state == 2) {
+    v.x = __fadd_rn(v.x, a.marker); v.y = __fadd_rn(v.y, a.marker);
+    v.z = __fadd_rn(v.z, a.marker); v.w = __fadd_rn(v.w, a.marker);
+  }
+  out[sub] = v;
+}
+
 }  // namespace
 
 extern "C" {
@@ -141,6 +227,13 @@ int pb_fire_matmul(pb_matmul_actor actor, pb_resolved res, void* stream) {
   if (res.n_iter == 0) return PB_OK;
   const int NN = actor.n * actor.n;
   if (actor.n < 1 || NN > 1024) return pb::fail(PB_E_UNSUPPORTED, "matmul: N*N must be <= 1024");
+  if (actor.n % 4 == 0 && NN <= 128 && 32 % (NN / 4) == 0) {
+    const int L = NN / 4, per_cta = 8 * (32 / L);
+    dim3 grid((unsigned)((res.n_iter + per_cta - 1) / per_cta), res.n_streams);
+    matmul_packed_kernel<<<grid, 256, 0, pb::as_stream(stream)>>>(actor, res, L);
+    PB_LAUNCHED("matmul_packed_kernel");
+    return PB_OK;
+  }
   const int per_cta = std::max(1, 256 / NN);
   dim3 grid((unsigned)((res.n_iter + per_cta - 1) / per_cta), res.n_streams);
   matmul_kernel<<<grid, per_cta * NN, NN * sizeof(float), pb::as_stream(stream)>>>(actor, res,
@@ -152,6 +245,14 @@ int pb_fire_matmul(pb_matmul_actor actor, pb_resolved res, void* stream) {
 int pb_fire_path_merge(pb_path_merge_actor actor, pb_resolved res, void* stream) {
   if (res.n_iter == 0) return PB_OK;
   if (actor.n_in > PB_MAX_PORTS) return pb::fail(PB_E_INVALID, "path_merge: too many ports");
+  const int64_t sb = actor.out.span_bytes;
+  if (sb % 16 == 0 && sb >= 16 && sb <= 512 && 32 % (sb / 16) == 0) {
+    const int L = (int)(sb / 16), per_cta = 8 * (32 / L);
+    dim3 grid((res.n_iter + per_cta - 1) / per_cta, res.n_streams);
+    path_merge_packed_kernel<<<grid, 256, 0, pb::as_stream(stream)>>>(actor, res, L);
+    PB_LAUNCHED("path_merge_packed_kernel");
+    return PB_OK;
+  }
   dim3 grid(res.n_iter, res.n_streams);
   path_merge_kernel<<<grid, 128, 0, pb::as_stream(stream)>>>(actor, res);
   PB_LAUNCHED("path_merge_kernel");

@@ -96,7 +96,11 @@ __device__ __forceinline__ int64_t span_index(const pb_span_ref& r, const pb_res
   if (r.index_cond >= 0)
     idx = res.prefix[((int64_t)r.index_cond * res.n_streams + s) * res.cap + n];
   int64_t b = r.base ? r.base[s] : 0;
-  return (b + idx + r.offset) % r.slots;
+  const int64_t x = b + idx + r.offset;
+  // 32-bit remainder while the ring counter fits (the 64-bit one is a long
+  // software sequence, executed per firing by every actor kernel)
+  if ((uint64_t)x <= 0xFFFFFFFFull) return (int64_t)((uint32_t)x % (uint32_t)r.slots);
+  return x % r.slots;
 }
 
 __device__ __forceinline__ uint8_t* span_ptr(const pb_span_ref& r, const pb_resolved& res,

@@ -181,7 +181,10 @@ __device__ __forceinline__ const uint8_t* span_ptr_b(const pb_span_ref& r, int64
   int64_t idx = n;
   if (r.index_cond >= 0)
     idx = res.prefix[((int64_t)r.index_cond * res.n_streams + s) * res.cap + n];
-  return r.data + (int64_t)s * r.stream_stride + ((base + idx + r.offset) % r.slots) * r.span_bytes;
+  const int64_t x = base + idx + r.offset;
+  const int64_t chunk = (uint64_t)x <= 0xFFFFFFFFull ? (int64_t)((uint32_t)x % (uint32_t)r.slots)
+                                                     : x % r.slots;
+  return r.data + (int64_t)s * r.stream_stride + chunk * r.span_bytes;
 }
 
 // ------------------------------------------------------------- FIR math

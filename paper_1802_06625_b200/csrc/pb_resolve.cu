@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kScanThreads) resolve_kernel(CondTable table, 
       int n = t0 + threadIdx.x * kScanItems + k;
       int f = 0;
       if (n < res.n_iter) {
-        int64_t chunk = ((int64_t)cd.base + n) % cd.slots;
+        const int64_t chunk = (uint32_t)(cd.base + n) % (uint32_t)cd.slots;   // base, n >= 0, int32
         f = tok[chunk * cd.token_stride + cd.element] != 0;
       }
       flags[k] = f;

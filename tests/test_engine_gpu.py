@@ -13,52 +13,8 @@ pytestmark = pytest.mark.gpu
 
 def bypass_desc(path):
     """apps/bypass.py:69-132 (the reference's adaptive-bypass graph)."""
-    import json
-    from pathlib import Path
-    ref = json.loads((Path(__file__).parent / "golden" / "fixtures.json").read_text())
-    del ref
-    N = 8
-
-    def w(layer):
-        return [float(np.float32(0.1 + 0.05 * layer - 0.01 * i + 0.02 * k))
-                for i in range(N) for k in range(N)]
-    tb = N * N * 4
-    actors = [
-        {"id": "src", "kind": "static", "behavior": "file_source", "params": {"path": path},
-         "ports": [{"id": "out", "dir": "out"}]},
-        {"id": "conf", "kind": "config", "behavior": "alternate_policy", "params": {"length": 2},
-         "ports": [{"id": "ctl", "dir": "out", "kind": "control_out"}]},
-        {"id": "fork", "kind": "dynamic", "behavior": "route",
-         "ports": [{"id": "in", "dir": "in"}, {"id": "ctl", "dir": "in", "kind": "control_in"},
-                   {"id": "d1", "dir": "out", "kind": "drp"},
-                   {"id": "d2", "dir": "out", "kind": "drp"}]},
-        {"id": "join", "kind": "dynamic", "behavior": "path_merge",
-         "params": {"marker": 0.5, "bypass_port": "e2"},
-         "ports": [{"id": "ctl", "dir": "in", "kind": "control_in"},
-                   {"id": "e1", "dir": "in", "kind": "drp"},
-                   {"id": "e2", "dir": "in", "kind": "drp"}, {"id": "out", "dir": "out"}]},
-        {"id": "sink", "kind": "static", "behavior": "null_sink",
-         "ports": [{"id": "in", "dir": "in"}]}]
-    for layer in (1, 2, 3):
-        actors.append({"id": f"l{layer}", "kind": "static", "behavior": "matmul",
-                       "params": {"w": w(layer)},
-                       "ports": [{"id": "in", "dir": "in"}, {"id": "out", "dir": "out"}]})
-    fifos = [
-        {"id": "f_src", "src": "src.out", "dst": "fork.in", "token_bytes": tb},
-        {"id": "c_fork", "src": "conf.ctl", "dst": "fork.ctl", "token_bytes": 2},
-        {"id": "c_join", "src": "conf.ctl", "dst": "join.ctl", "token_bytes": 2},
-        {"id": "f_l1", "src": "fork.d1", "dst": "l1.in", "token_bytes": tb},
-        {"id": "f_l2", "src": "l1.out", "dst": "l2.in", "token_bytes": tb},
-        {"id": "f_l3", "src": "l2.out", "dst": "l3.in", "token_bytes": tb},
-        {"id": "f_chain", "src": "l3.out", "dst": "join.e1", "token_bytes": tb},
-        {"id": "f_bypass", "src": "fork.d2", "dst": "join.e2", "token_bytes": tb},
-        {"id": "f_out", "src": "join.out", "dst": "sink.in", "token_bytes": tb}]
-    table = [{"port": "conf.ctl", "drp": "fork.d1", "element": 1},
-             {"port": "conf.ctl", "drp": "join.e1", "element": 1},
-             {"port": "conf.ctl", "drp": "fork.d2", "element": 2},
-             {"port": "conf.ctl", "drp": "join.e2", "element": 2}]
-    return {"name": "bypass", "actors": actors, "fifos": fifos,
-            "control": {"value_lengths": {"conf.ctl": 2}, "table": table}}
+    from paper_1802_06625_b200.apps import bypass
+    return bypass.build_description(path)
 
 
 @pytest.mark.parametrize("epoch", [4096, 5])

@@ -1,0 +1,101 @@
+"""The reference's adaptive-bypass matrix pipeline (SURVEY §8 a13,
+apps/bypass.py) on one B200: device-resident matrices/s over many independent
+streams (alternating chain / bypass firings), per-kernel device times, and the
+reference interpreter (oracle/_ref, one process per core) beside it."""
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import tempfile
+import time
+from concurrent.futures import ProcessPoolExecutor
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import numpy as np
+
+from paper_1802_06625_b200 import RuntimeConfig
+from paper_1802_06625_b200.apps import bypass
+from paper_1802_06625_b200.engine import DeviceRuntime
+
+
+def _ref_stream(args):
+    seed, mats = args
+    sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
+    from tokenflow.interp import interpret
+    from tokenflow.model import build_graph
+    with tempfile.TemporaryDirectory() as d:
+        p = Path(d) / "input.bin"
+        p.write_bytes(bypass.make_input(seed, mats))
+        g = build_graph(bypass.build_description(str(p)))
+        t0 = time.perf_counter()
+        interpret(g, source_firings=mats, seed=seed)
+        return time.perf_counter() - t0
+
+
+def measure(S=1024, mats=1024, steps=50):
+    rt = DeviceRuntime(bypass.build_description(), config=RuntimeConfig(
+        source_firings=mats, epoch=mats), n_streams=S, seeds=list(range(S)),
+        sources={"src": [None] * S})
+    st = rt.source_staging("src")
+    for s in range(S):
+        st[s] = np.frombuffer(bypass.make_input(s, mats), np.uint8).reshape(mats, -1)
+    lib = rt.lib
+    rt.reset()
+    rt.stage_sources(0, mats, prestaged=True)
+    rt.stage_control(0, mats)
+    for _ in range(3):
+        rt.fire_epoch(0, mats)
+    lib.pb_stream_sync(rt.stream)
+
+    def ev():
+        e = C.c_void_p()
+        lib.pb_event_create(C.byref(e))
+        return e.value
+    marks = {}
+
+    def hook(kind, phase):
+        e = ev()
+        lib.pb_event_record(e, rt.stream)
+        marks.setdefault(kind, []).append(e)
+    e0, e1 = ev(), ev()
+    lib.pb_event_record(e0, rt.stream)
+    for _ in range(steps):
+        rt.fire_epoch(0, mats, hook=hook)
+    lib.pb_event_record(e1, rt.stream)
+    lib.pb_stream_sync(rt.stream)
+    ms = C.c_float()
+    lib.pb_event_elapsed_ms(e0, e1, C.byref(ms))
+    step_ms = ms.value / steps
+    per_kind = {}
+    for kind, evs in marks.items():
+        ts = []
+        for i in range(0, len(evs) - 1, 2):
+            lib.pb_event_elapsed_ms(evs[i], evs[i + 1], C.byref(ms))
+            ts.append(ms.value)
+        per_kind[kind] = sum(ts) / steps
+    n = S * mats
+    rt.close()
+    out = {"metric": "bypass matrices/s (8x8 fp32, alternating 3-matmul chain / bypass, "
+                     "device-resident)",
+           "streams": S, "matrices_per_stream": mats, "matrices_per_step": n,
+           "step_ms": step_ms, "matrices_per_s": n / (step_ms / 1e3),
+           "kernel_ms_per_step": per_kind,
+           "note": "half the firings run l1 -> l2 -> l3 (3 x 512 rounded mul/add per matrix), "
+                   "half the bypass; every firing moves 256-B tokens through rings"}
+    if (ROOT / "oracle" / "_ref").is_dir():
+        cores = os.cpu_count() or 1
+        ref_mats = 256
+        with ProcessPoolExecutor(cores) as ex:
+            ts = list(ex.map(_ref_stream, [(s, ref_mats) for s in range(cores)]))
+        out["cpu_baseline"] = {"value": cores * ref_mats / max(ts), "unit": "matrices/s",
+                               "cores": cores, "kind": "reference",
+                               "sample": f"{cores} streams x {ref_mats} matrices through "
+                                         "tokenflow.interp.interpret, one process per core"}
+    return out
+
+
+if __name__ == "__main__":
+    print(json.dumps(measure(*[int(a) for a in sys.argv[1:]])))
