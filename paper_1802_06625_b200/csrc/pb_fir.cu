@@ -890,6 +890,9 @@ bank_plan_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPla
 #ifndef PB_PLAN_PAR
 #define PB_PLAN_PAR 1
 #endif
+#ifndef PB_PLAN_TAILS
+#define PB_PLAN_TAILS 1
+#endif
 #ifndef PB_PLAN_STOP   // profiling: end the planner after phase 1/2/3
 #define PB_PLAN_STOP 0
 #endif
@@ -905,9 +908,19 @@ __host__ __device__ inline size_t plan_par_smem(int n_iter, int nb) {
          + (size_t)kPC * nb * 2 * kHist * 4      // hist
          + (size_t)n_iter * 4                    // mask
          + (size_t)nb * kPC * 4                  // prev
-         + (size_t)n_iter + 16;                  // have
+         + (size_t)((n_iter + 15) & ~15);        // have
+}
+// + every span tail up to the chunk end and the branch states (kTails)
+__host__ __device__ inline size_t plan_par_tails_smem(int n_iter, int nb) {
+  return plan_par_smem(n_iter, nb) + (size_t)(n_iter + nb) * 2 * kHist * 4;
 }
 
+// kTails: every span tail of the stream's spans 0..hi-1 (and each branch's
+// carried state) is requested at kernel start, before the activity masks and
+// the scan are known -- a branch's history is the tail of the bank input at
+// its previous firing, the same bytes for every branch -- so the gather's
+// round trip overlaps phases 1-2 instead of following them.
+template <bool kTails>
 __global__ void __launch_bounds__(kPlanParThreads)
 bank_plan_par_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan) {
   pb::pdl_enter();
@@ -924,6 +937,24 @@ bank_plan_par_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* 
   int* prev = reinterpret_cast<int*>(mask + E);                         // [nb][kPC]
   uint8_t* have = reinterpret_cast<uint8_t*>(prev + nb * kPC);          // [hi]
   const int64_t in_base = bank.in.base ? bank.in.base[s] : 0;
+  // kTails layout: tails[hi][2][kHist], then state tails [nb][2][kHist]
+  float* tails = reinterpret_cast<float*>(have + ((E + 15) & ~15));
+  float* stails = tails + (size_t)hi * 2 * kHist;
+  if (kTails) {
+    for (int e = tid; e < (hi + nb) * 2 * kHist; e += kPlanParThreads) {
+      const int t = e / (2 * kHist), q = e - t * 2 * kHist;
+      const float* src;
+      if (t < hi) {
+        const int plane = q / kHist, kk = q - plane * kHist;
+        src = reinterpret_cast<const float*>(span_ptr_b(bank.in, in_base, res, s, t)) +
+              plane * B + B - kHist + kk;
+      } else {
+        src = br[t - hi].state + (int64_t)s * 2 * kHist + q;
+      }
+      cp_async4(tails + e, src);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   // 1. taps and activity masks: every load of a thread issued before use
   for (int e = tid; e < nb * kTaps; e += kPlanParThreads) {
     const int b = e / kTaps, t = e % kTaps;
@@ -979,30 +1010,35 @@ bank_plan_par_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* 
 #endif
   // 3. history sources (one pointer per active (span, branch)), then every
   //    history sample in flight at once (cp.async into shared memory)
-  for (int e = tid; e < np * nb; e += kPlanParThreads) {
-    const int i = e / nb, b = e - i * nb;
-    const int src = prev[b * kPC + i];
-    const float* p = nullptr;
-    if ((mask[lo + i] >> b) & 1u) {
-      if (src < 0)   // first firing of the branch: its carried state [2][kHist]
-        p = br[b].state + (int64_t)s * 2 * kHist;
-      else           // re plane tail; the im plane tail is p + B
-        p = reinterpret_cast<const float*>(span_ptr_b(bank.in, in_base, res, s, src)) + B - kHist;
+  if (kTails) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+  } else {
+    for (int e = tid; e < np * nb; e += kPlanParThreads) {
+      const int i = e / nb, b = e - i * nb;
+      const int src = prev[b * kPC + i];
+      const float* p = nullptr;
+      if ((mask[lo + i] >> b) & 1u) {
+        if (src < 0)   // first firing of the branch: its carried state [2][kHist]
+          p = br[b].state + (int64_t)s * 2 * kHist;
+        else           // re plane tail; the im plane tail is p + B
+          p = reinterpret_cast<const float*>(span_ptr_b(bank.in, in_base, res, s, src)) + B - kHist;
+      }
+      hsrc[e] = p;
     }
-    hsrc[e] = p;
+    __syncthreads();
+    for (int e = tid; e < np * nb * 2 * kHist; e += kPlanParThreads) {
+      const int ib = e / (2 * kHist), q = e - ib * 2 * kHist;
+      const float* p = hsrc[ib];
+      if (!p) continue;
+      const int b = ib % nb, i = ib / nb;
+      const bool state = prev[b * kPC + i] < 0;
+      const int plane = q / kHist, kk = q - plane * kHist;
+      cp_async4(hist + e, p + (state ? q : plane * B + kk));
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
   }
-  __syncthreads();
-  for (int e = tid; e < np * nb * 2 * kHist; e += kPlanParThreads) {
-    const int ib = e / (2 * kHist), q = e - ib * 2 * kHist;
-    const float* p = hsrc[ib];
-    if (!p) continue;
-    const int b = ib % nb, i = ib / nb;
-    const bool state = prev[b * kPC + i] < 0;
-    const int plane = q / kHist, k = q - plane * kHist;
-    cp_async4(hist + e, p + (state ? q : plane * B + k));
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncthreads();
 #if PB_PLAN_STOP == 3
   return;
 #endif
@@ -1024,7 +1060,9 @@ bank_plan_par_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* 
     for (int k = 0; k < kHist; ++k) cr[k] = ci[k] = 0.f;
     for (int b = 0; b < nb; ++b) {
       if (!((m >> b) & 1u)) continue;
-      const float* h = hist + (i * nb + b) * 2 * kHist;
+      const int pv = prev[b * kPC + i];
+      const float* h = !kTails ? hist + (i * nb + b) * 2 * kHist
+                               : (pv >= 0 ? tails + pv * 2 * kHist : stails + b * 2 * kHist);
       float h_r[kHist], h_i[kHist];
 #pragma unroll
       for (int q = 0; q < kHist; ++q) {
@@ -1327,9 +1365,13 @@ int launch_merged_bank(const pb_filter_bank& bank, const pb_resolved& res, int64
   dim3 pgrid((res.n_iter + kPlanWarps - 1) / kPlanWarps, res.n_streams);
   const size_t ssmem = plan_stream_smem(res.n_iter, bank.n_branches);
   const size_t parsmem = plan_par_smem(res.n_iter, bank.n_branches);
-  if (PB_PLAN_PAR && parsmem <= 48 * 1024) {
+  const size_t tailsmem = plan_par_tails_smem(res.n_iter, bank.n_branches);
+  if (PB_PLAN_PAR && PB_PLAN_TAILS && tailsmem <= 48 * 1024) {
     dim3 g(res.n_streams, (res.n_iter + kPC - 1) / kPC);
-    PB_LAUNCH_PDL(bank_plan_par_kernel, g, kPlanParThreads, parsmem, st, bank, res, B, plan);
+    PB_LAUNCH_PDL(bank_plan_par_kernel<true>, g, kPlanParThreads, tailsmem, st, bank, res, B, plan);
+  } else if (PB_PLAN_PAR && parsmem <= 48 * 1024) {
+    dim3 g(res.n_streams, (res.n_iter + kPC - 1) / kPC);
+    PB_LAUNCH_PDL(bank_plan_par_kernel<false>, g, kPlanParThreads, parsmem, st, bank, res, B, plan);
   } else if (ssmem <= 48 * 1024) {
     PB_LAUNCH_PDL(bank_plan_stream_kernel, res.n_streams, kPlanStreamThreads, ssmem, st, bank, res, B, plan);
   } else {
