@@ -254,6 +254,9 @@ typedef struct {
   int32_t math;                      /* PB_FIR_* arithmetic mode */
   int32_t pad_;
 } pb_filter_bank;
+/* The call includes the history carry of every branch (pb_fir_carry's work:
+ * state[s] <- the last 9 input samples of the branch's last firing this
+ * epoch); callers do not carry bank branches themselves. */
 int pb_fire_filter_bank(pb_filter_bank bank, pb_resolved res, int64_t block, void* stream);
 
 /* branch_sum (predistortion.py:68-83): ins in sorted port-id order. */

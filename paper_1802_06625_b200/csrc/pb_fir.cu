@@ -1197,6 +1197,9 @@ bank_merged_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
 #ifndef PB_MS_WARPS
 #define PB_MS_WARPS 4
 #endif
+#ifndef PB_MS_CARRY   // 1: the stream kernel also carries the branch histories
+#define PB_MS_CARRY 1
+#endif
 #ifndef PB_MS_L2HINT   // input planes are read once: evict-first in L2
 #define PB_MS_L2HINT 1
 #endif
@@ -1251,8 +1254,29 @@ bank_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
   const int warp = threadIdx.x >> 5;
 
   if (warp == kMSWarps) {
+    if ((threadIdx.x & 31) != 0) {
+#if PB_MS_CARRY
+      // lanes 1..18 of the producer warp: the history carry of this CTA's
+      // (stream, branch) items -- state <- the last 9 input samples of the
+      // branch's last firing this epoch (fir_carry_kernel's work; the planner
+      // that reads the old state has completed before this grid started)
+      const int q = (threadIdx.x & 31) - 1;
+      if (q < 2 * kHist) {
+        const int nb = bank.n_branches, plane = q / kHist, k = q - plane * kHist;
+        for (int64_t i = blockIdx.x; i < (int64_t)res.n_streams * nb; i += gridDim.x) {
+          const int s = (int)(i / nb);
+          const pb_fir_actor& fa = bank.branches[i - (int64_t)s * nb];
+          const int cnt = pb::cond_count(res, fa.cond, s);
+          if (cnt == 0) continue;
+          const int nl = pb::firing_iter(res, fa.cond, s, cnt - 1);
+          const float* in = reinterpret_cast<const float*>(pb::span_ptr(fa.in, res, s, nl));
+          fa.state[(int64_t)s * 2 * kHist + plane * kHist + k] = in[plane * B + B - kHist + k];
+        }
+      }
+#endif
+      return;
+    }
     // ------------------------------------------------------------ producer
-    if ((threadIdx.x & 31) != 0) return;
 #if PB_MS_L2HINT
     u64 pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -1496,7 +1520,15 @@ int pb_fire_filter_bank(pb_filter_bank bank, pb_resolved res, int64_t block, voi
                                           " branches");
   int rc = check_block(block);
   if (rc) return rc;
-  return launch<true>(bank, nullptr, 0, res, block, bank.math, pb::as_stream(stream));
+  rc = launch<true>(bank, nullptr, 0, res, block, bank.math, pb::as_stream(stream));
+  if (rc) return rc;
+  // the history carry is part of the bank's firing: done inside the stream
+  // kernel on the merged path, a carry launch otherwise
+  if (bank.math == PB_FIR_MERGED && PB_MERGED_STREAM == 1 && PB_MS_CARRY) return PB_OK;
+  dim3 grid(res.n_streams, bank.n_branches);
+  PB_LAUNCH_PDL(fir_carry_kernel, grid, 32, 0, pb::as_stream(stream), bank.branches, res, block);
+  PB_LAUNCHED("fir_carry_kernel");
+  return PB_OK;
 }
 
 }  // extern "C"

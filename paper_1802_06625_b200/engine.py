@@ -434,7 +434,7 @@ class DeviceRuntime:
                                        self.mem.malloc(16), self.fir_math, 0)
                 block = fin.rate * fin.token_bytes // 8
                 self.launches.append(("bank", bank, block))
-                self.fir_groups.append((dev, len(grp.branches), block))
+                # (no fir_groups entry: pb_fire_filter_bank carries its branches)
                 done.add(aid)
                 continue
             if kind == "fir":
