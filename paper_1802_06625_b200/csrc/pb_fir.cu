@@ -69,11 +69,6 @@ struct __align__(16) Desc {
   int first;      // tile 0: window entries before the span come from hist
   int8_t br[kMaxBr];
   float hist[kMaxBr][2][kHist];
-  // PB_FIR_MERGED (bank): the active branches' taps summed per tap
-  // ({cr, ci, ci, cr}), and for the span's first kHist outputs the
-  // contribution of each branch's own history (pre-span samples)
-  float4 mtaps[kTaps];
-  float corr[kHist][2];
 };
 
 struct __align__(16) Smem {
@@ -157,11 +152,6 @@ __device__ __forceinline__ void unpack2(u64 v, float& lo, float& hi) {
 __device__ __forceinline__ u64 fmul2(u64 a, u64 b) {
   u64 r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
-  u64 r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
 }
 __device__ __forceinline__ u64 fadd2(u64 a, u64 b) {
@@ -284,12 +274,9 @@ __device__ __forceinline__ void store8(float* out, int64_t B, int n0, const u64 
 //                region; output = sum over active branches (combiner order)
 // kBank = false: items (actor, s, j, tile) of per-actor batched firings;
 //                output = the actor's own output span
-// PB_FIR_MERGED (bank launches only): every active branch sees the same
-// input inside a span, so sum_k FIR_k(x) = FIR_{sum_k c_k}(x) there; the
-// consumers run ONE fused-multiply-add FIR per output with the producer's
-// merged taps, and the first kHist outputs add the producer's correction for
-// the pre-span samples, which differ per branch (each branch's own history).
-// Reassociated sums: within ~1e-7 of the exact path (tolerance 1e-5).
+// (The tolerance mode of the bank, PB_FIR_MERGED, runs as bank_plan_par_kernel
+// + bank_stream_kernel below; this kernel serves the bit-exact bank and the
+// per-actor firings.)
 template <bool kBank, int kMath>
 __global__ void __launch_bounds__(kThreads, 4)
 fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actors, int n_actors,
@@ -329,7 +316,7 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
     // ranges leave a tail); otherwise each CTA takes one contiguous range.
     // (MERGED work per span is constant: static ranges balance, and keep the
     // per-branch history source in registers across the CTA's spans)
-    const bool dynamic = kBank && bank.sched != nullptr && kMath != PB_FIR_MERGED;
+    const bool dynamic = kBank && bank.sched != nullptr;
     const int64_t chunk = dynamic ? (int64_t)kChunkSpans * tiles : 0;
     int64_t w0 = total * blockIdx.x / gridDim.x;
     int64_t w1 = total * (blockIdx.x + 1) / gridDim.x;
@@ -340,7 +327,6 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
     bool have = false;
     unsigned mask = 0;
     int prev_n = -2;   // lane b: iteration branch b last fired at (-1: none yet, -2: unknown)
-    float4 mtap = make_float4(0.f, 0.f, 0.f, 0.f);   // MERGED: lane t's merged tap
     int64_t in_base = 0, out_base = 0;               // ring bases of the current stream
     const float* span_in = nullptr;                  // current span's input / output
     u64 span_out = 0;
@@ -350,7 +336,6 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
     int64_t pf_unit = -1;
     int pf_n = -1;
     bool pf_have = false, pf_act = false, pf_ok = false, cur_pf_ok = false;
-    constexpr bool kMerged = kBank && kMath == PB_FIR_MERGED;
     for (;;) {
     if (dynamic) {
       int64_t c = 0;
@@ -452,15 +437,6 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
           span_out = reinterpret_cast<u64>(
               span_ptr_b(kBank ? bank.out : actors[a].out, out_base, res, s, n));
         }
-        if (kMerged && have && lane < kTaps) {
-          float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int b = 0; b < nb; ++b)
-            if ((mask >> b) & 1u) {
-              const float4 c = sm.taps[b][lane];
-              m.x += c.x; m.y += c.y; m.z += c.z; m.w += c.w;
-            }
-          mtap = m;
-        }
       }
       if (!have) continue;
       const int stage = k % kStages;
@@ -522,29 +498,6 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
           }
         }
       }
-      if (kMerged) {
-        if (lane < kTaps) d.mtaps[lane] = mtap;
-        if (t0 == 0) {
-          __syncwarp();   // d.br / d.hist of the active lanes are written
-          if (lane < kHist) {
-            // output `lane` reads pre-span sample lane - t (< 0) for taps t > lane
-            float cr = 0.f, ci = 0.f;
-            const int na = __popc(mask);
-            for (int r = 0; r < na; ++r) {
-              const float4* tp = sm.taps[d.br[r]];
-              for (int t = lane + 1; t < kTaps; ++t) {
-                const int q = lane - t + kHist;
-                const float hr = d.hist[r][0][q], hi = d.hist[r][1][q];
-                const float4 c = tp[t];
-                cr = __fmaf_rn(-c.y, hi, __fmaf_rn(c.x, hr, cr));
-                ci = __fmaf_rn(c.y, hr, __fmaf_rn(c.x, hi, ci));
-              }
-            }
-            d.corr[lane][0] = cr;
-            d.corr[lane][1] = ci;
-          }
-        }
-      }
       if (lane == 0) {
         d.out = span_out;
         d.valid = 1;
@@ -599,30 +552,6 @@ fir_persistent(const pb_filter_bank bank, const pb_fir_actor* __restrict__ actor
       float wr[kWin], wi[kWin];
       load_window(sm.buf[stage], ct, wr, wi);
       const bool patch = d.first && ct * kPerThread < kPad;
-      if constexpr (kBank && kMath == PB_FIR_MERGED) {
-        if (patch) {   // pre-span samples: zero here, per-branch history in d.corr
-#pragma unroll
-          for (int i = 0; i < kPad; ++i)
-            if (kPerThread * ct - kPad + i < 0) wr[i] = wi[i] = 0.0f;
-        }
-        u64 y[kPerThread];
-        fir8_fma(wr, wi, d.mtaps, y);
-        if (patch) {
-#pragma unroll
-          for (int v = 0; v < kPerThread; ++v) {
-            const int m = kPerThread * ct + v;
-            if (m < kHist) {
-              float yr, yi;
-              unpack2(y[v], yr, yi);
-              y[v] = pack2(yr + d.corr[m][0], yi + d.corr[m][1]);
-            }
-          }
-        }
-        store8(out, B, n0, y);
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.empty[stage]);
-        continue;
-      }
       u64 acc[kPerThread];
 #pragma unroll
       for (int v = 0; v < kPerThread; ++v) acc[v] = pack2(0.0f, 0.0f);
