@@ -20,6 +20,9 @@ constexpr int kImgThreads = 256;
 #define PB_IMG_FAST 1
 #endif
 constexpr int kMaxSide = 128;
+#ifndef PB_MED_PRMT
+#define PB_MED_PRMT 1
+#endif
 
 __global__ void __launch_bounds__(kImgThreads)
 image_kernel(pb_image_actor a, pb_resolved res) {
@@ -112,11 +115,19 @@ __device__ __forceinline__ uint32_t med5_u16(uint32_t a, uint32_t b, uint32_t c,
 // byte-wise median of five words: even and odd bytes as two u16x2 lane sets
 __device__ __forceinline__ uint32_t med5(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
                                          uint32_t e) {
+#if PB_MED_PRMT
+  auto ev = [](uint32_t x) { return __byte_perm(x, 0u, 0x4240); };   // bytes 0, 2
+  auto od = [](uint32_t x) { return __byte_perm(x, 0u, 0x4341); };   // bytes 1, 3
+  const uint32_t me = med5_u16(ev(a), ev(b), ev(c), ev(d), ev(e));
+  const uint32_t mo = med5_u16(od(a), od(b), od(c), od(d), od(e));
+  return __byte_perm(me, mo, 0x6240);   // pixels 0 (me.b0), 1 (mo.b0), 2 (me.b2), 3 (mo.b2)
+#else
   constexpr uint32_t M = 0x00FF00FFu;
   const uint32_t ev = med5_u16(a & M, b & M, c & M, d & M, e & M);
   const uint32_t od = med5_u16((a >> 8) & M, (b >> 8) & M, (c >> 8) & M, (d >> 8) & M,
                                (e >> 8) & M);
   return ev | (od << 8);
+#endif
 }
 
 // frames per CTA: the span addressing of each frame (ring index arithmetic)
@@ -130,10 +141,12 @@ struct FramePtrs {
   uint32_t* o1;
 };
 
+template <int LW>   // words per row = 1 << LW, side = 4 << LW (compile time)
 __global__ void __launch_bounds__(kFastThreads)
-image_fast_kernel(pb_image_actor a, pb_resolved res, int lw) {
+image_fast_kernel(pb_image_actor a, pb_resolved res) {
+  constexpr int lw = LW;
   const int s = blockIdx.y, tid = threadIdx.x;
-  const int side = a.side, W = 1 << lw, nw = side * W;
+  constexpr int W = 1 << lw, side = 4 * W, nw = side * W;
   __shared__ FramePtrs fp[kFPC];
   __shared__ int n_frames;
   if (tid < kFPC) {
@@ -161,7 +174,8 @@ image_fast_kernel(pb_image_actor a, pb_resolved res, int lw) {
   extern __shared__ uint4 img_smem[];
   uint32_t* fr = reinterpret_cast<uint32_t*>(img_smem);            // [side][W] words
   uint32_t* hs = fr + nw;                                          // [side][W][2] int16 pairs
-  const int xw0 = tid & (W - 1), rows = kFastThreads >> lw;
+  const int xw0 = tid & (W - 1);
+  constexpr int rows = kFastThreads >> lw;
   uint4 pre[2];
   for (int f = 0; f < nf; ++f) {
     const FramePtrs P = fp[f];
@@ -281,19 +295,25 @@ int pb_fire_image(pb_image_actor actor, pb_resolved res, void* stream) {
   dim3 grid(res.n_iter, res.n_streams);
   const int side = actor.side;
   if (PB_IMG_FAST && side >= 8 && (side & (side - 1)) == 0 && actor.n_out <= 2) {
-    int lw = 0;
-    while ((4 << lw) < side) ++lw;   // words per row = side / 4 = 1 << lw
     const size_t smem = actor.op == PB_IMG_DIFF ? 0 : (size_t)side * side * 3;
     static bool attr[pb::kMaxDevices] = {};   // side 128: 48 KB dynamic + the static part
     const int dev = pb::device();
     if (dev < 0) return PB_E_CUDA;
     if (!attr[dev]) {
-      PB_CUDA(cudaFuncSetAttribute(image_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      PB_CUDA(cudaFuncSetAttribute(image_fast_kernel<5>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    3 * kMaxSide * kMaxSide));
       attr[dev] = true;
     }
     dim3 fgrid((res.n_iter + kFPC - 1) / kFPC, res.n_streams);
-    image_fast_kernel<<<fgrid, kFastThreads, smem, pb::as_stream(stream)>>>(actor, res, lw);
+    cudaStream_t st = pb::as_stream(stream);
+    switch (side) {
+      case 8: image_fast_kernel<1><<<fgrid, kFastThreads, smem, st>>>(actor, res); break;
+      case 16: image_fast_kernel<2><<<fgrid, kFastThreads, smem, st>>>(actor, res); break;
+      case 32: image_fast_kernel<3><<<fgrid, kFastThreads, smem, st>>>(actor, res); break;
+      case 64: image_fast_kernel<4><<<fgrid, kFastThreads, smem, st>>>(actor, res); break;
+      default: image_fast_kernel<5><<<fgrid, kFastThreads, smem, st>>>(actor, res); break;
+    }
     PB_LAUNCHED("image_fast_kernel");
     return PB_OK;
   }
