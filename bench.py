@@ -55,7 +55,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-streams", type=int, default=64)
-    ap.add_argument("--cpu-blocks", type=int, default=32)
+    ap.add_argument("--cpu-blocks", type=int, default=256,
+                    help="blocks per stream of the CPU reference sample (256: the whole C2 "
+                         "workload, about 9 s of CPU work per step on 16 cores)")
     ap.add_argument("--skip-cnn", action="store_true")
     ap.add_argument("--cnn-streams", type=int, default=4, help="CNN streams per GPU")
     ap.add_argument("--cnn-firings", type=int, default=64, help="24-frame firings per stream")
