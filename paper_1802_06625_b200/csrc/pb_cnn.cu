@@ -37,6 +37,8 @@
 //   * Patches and accumulators: NB buffers (layer 1: 3, layer 2: 2).
 #include <algorithm>
 
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -71,9 +73,9 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
 }
 
-// kind::f16 instruction descriptor: bf16 A/B, fp32 D, K-major, M = 128.
-__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+// kind::f16 instruction descriptor: bf16 A/B, fp32 D, K-major, M = 128 (256: a CTA pair).
+__host__ __device__ constexpr uint32_t idesc_bf16(int n, int m = 128) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_bf16(uint32_t tmem, uint64_t a, uint64_t b, uint32_t id,
@@ -89,6 +91,50 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(bar))
       : "memory");
+}
+
+// ---- CTA-pair (cta_group::2) helpers, layer 2 with PB_CONV_PAIR
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// M = 256 over the pair: A rows 0-127 from the leader's shared memory, 128-255
+// from the peer's (same offset); B split by N (first half leader, second
+// half peer); D = each CTA's own 128 TMEM lanes.  Issued by the leader.
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem, uint64_t a, uint64_t b, uint32_t id,
+                                              uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+// completion of the leader's MMAs arrives on the barrier at this offset in
+// both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)), "h"((uint16_t)3)
+      : "memory");
+}
+// arrive on the leader's (rank 0) barrier at this offset, release at cluster scope
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\nWC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t@!p bra WC_%=;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
@@ -491,11 +537,21 @@ __device__ __forceinline__ bool elect_one() {
   return p != 0;
 }
 
-template <int MODE, int CIN>
+// PAIR (layer 2): clusters of two CTAs; each CTA still builds the patch of
+// its own super-tiles, and the even CTA issues cta_group::2 MMAs (M = 256)
+// that read both patches, so each SM reads only half of B (the weights) per
+// MMA.  Both CTAs walk the pair's two work lists in lockstep (a half without
+// a live super-tile gets a dummy one), so every MMA has both halves.
+template <int MODE, int CIN, bool PAIR = false>
 __global__ void __launch_bounds__(kConvThreads, 1)
 conv_pool_kernel(pb_conv_actor a, pb_resolved res, const UnitSpans* __restrict__ units,
                  const __grid_constant__ CUtensorMap tmap) {
   using Cfg = ConvCfg<MODE, CIN>;
+  constexpr bool kPair = PAIR && MODE == 1;
+  const uint32_t crank = kPair ? cluster_ctarank() : 0u;
+  // pair weights per K-step: 32 B rows (the N = 64 MMA's half: wh on the
+  // leader, wl on the peer) then 16 B rows (the N = 32 MMA's half of wh)
+  constexpr int kPairStep = 1536;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -510,24 +566,41 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const UnitSpans* __restrict__
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.weights);
     uint4* dst = reinterpret_cast<uint4*>(wsm);
-    for (int i = tid; i < Cfg::WBYTES / 16; i += kConvThreads) dst[i] = __ldg(src + i);
+    if constexpr (kPair) {
+      for (int i = tid; i < Cfg::STEPS * (kPairStep / 16); i += kConvThreads) {
+        const int st = i / (kPairStep / 16), o = i - st * (kPairStep / 16);   // 16-B units
+        const int srco = o < 64 ? (int)crank * 64 + o : (int)crank * 32 + (o - 64);
+        dst[i] = __ldg(src + st * (kStepBytes / 16) + srco);
+      }
+    } else {
+      for (int i = tid; i < Cfg::WBYTES / 16; i += kConvThreads) dst[i] = __ldg(src + i);
+    }
     if (tid < kCout) B.bias[tid] = __ldg(a.bias + tid);
     for (int st = tid; st < res.n_streams; st += kConvThreads) B.cnt[st] = pb::cond_count(res, a.cond, st);
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&B.tmem_base)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&B.tmem_base)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&B.tmem_base)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   if (tid == 0) {
     for (int b = 0; b < Cfg::NB; ++b) {
-      mbar_init(&B.full[b], kCvtThreads);
+      // pair: the leader's full / acc_empty also count the peer's converters
+      // and epilogue; acc_full is the multicast MMA completion alone
+      mbar_init(&B.full[b], kPair ? 2 * kCvtThreads : kCvtThreads);
       mbar_init(&B.empty[b], 1);
       // acc_full: the MMA completion (tcgen05.commit) and a plain release
       // arrive of the MMA thread, which orders the descriptor it read
-      mbar_init(&B.acc_full[b], 2);
-      mbar_init(&B.acc_empty[b], kEpiThreads);
+      mbar_init(&B.acc_full[b], kPair ? 1 : 2);
+      mbar_init(&B.acc_empty[b], kPair ? 2 * kEpiThreads : kEpiThreads);
     }
     for (int b = 0; b < kRawBufs; ++b) mbar_init(&B.raw_full[b], 1);
     for (int k = 0; k < kSchedRing; ++k) {
@@ -539,10 +612,53 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const UnitSpans* __restrict__
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if constexpr (kPair) cluster_sync();   // both CTAs' barriers exist before any remote arrive
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = B.tmem_base;
 
-  if (warp == kSchedWarp) {
+  if (kPair && warp == kSchedWarp) {
+    // ================================================ pair scheduler
+    // both halves' cursors (super-tiles w0 + k*grid and w0 + 1 + k*grid),
+    // stepped together; steps where neither half is live are skipped
+    const int w0 = (int)(blockIdx.x & ~1u);
+    auto at = [&](int w) {
+      Cursor c;
+      c.unit = w / G.per_unit;
+      c.rem = w - c.unit * G.per_unit;
+      c.live = false;
+      cursor_fix(c, G, B.cnt, res);
+      return c;
+    };
+    Cursor c0 = at(w0), c1 = at(w0 + 1);
+    auto live = [&](const Cursor& c) { return c.unit < G.n_units && c.live; };
+    for (int k = 0;; ++k) {
+      while (c0.unit < G.n_units && !live(c0) && !live(c1)) {
+        cursor_step(c0, G, B.cnt, res);
+        cursor_step(c1, G, B.cnt, res);
+      }
+      const bool more = c0.unit < G.n_units;
+      const int slot = k % kSchedRing;
+      mbar_wait(&B.sched_empty[slot], ((uint32_t)(k / kSchedRing) & 1) ^ 1);
+      SuperTile t{};
+      if (more) {
+        const Cursor& me = crank ? c1 : c0;
+        if (live(me)) {
+          t = finish_tile(pending_tile<Cfg>(me, G, units), G);
+        } else {   // dummy half: converters skip it, the epilogue stores nothing
+          t.fout = reinterpret_cast<float*>(uintptr_t(16));
+          t.pad_ = 1;
+        }
+        cursor_step(c0, G, B.cnt, res);
+        cursor_step(c1, G, B.cnt, res);
+      }
+      if (lane == 0) {
+        B.sched[slot] = t;
+        mbar_arrive(&B.sched_full[slot]);
+      }
+      __syncwarp();
+      if (!more) break;
+    }
+  } else if (warp == kSchedWarp) {
     // ================================================ scheduler
     // Walks this CTA's work list (the latency-bound cursor arithmetic and the
     // unit-table loads, one super-tile ahead) and publishes one SuperTile per
@@ -603,7 +719,8 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const UnitSpans* __restrict__
       if (t.fout == nullptr) {   // end of work: an empty descriptor through the normal handoff
         mbar_wait(&B.empty[b], (use & 1) ^ 1);
         if (ct == 0) B.desc[it % kDescRing].fout = nullptr;
-        mbar_arrive(&B.full[b]);
+        if (kPair && crank) mbar_arrive_leader(&B.full[b]);
+        else mbar_arrive(&B.full[b]);
         break;
       }
       const int rb = it % kRawBufs;
@@ -612,11 +729,13 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const UnitSpans* __restrict__
       PROF(pon, 1);
       mbar_wait(&B.empty[b], (use & 1) ^ 1);
       PROF(pon, 2);
-      if (!(a.debug & 1)) fill_patch<MODE, CIN>(patch0 + b * Cfg::PATCH, raw0 + rb * Cfg::RAW, G, t, ct);
+      if (!(a.debug & 1) && t.pad_ == 0)
+        fill_patch<MODE, CIN>(patch0 + b * Cfg::PATCH, raw0 + rb * Cfg::RAW, G, t, ct);
       if (ct == 0) B.desc[it % kDescRing] = t;
       PROF(pon, 3);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&B.full[b]);
+      if (kPair && crank) mbar_arrive_leader(&B.full[b]);
+      else mbar_arrive(&B.full[b]);
       PROF(pon, 4);
       // all converters are done with sched[slot] (and, layer 1, raw[rb])
       asm volatile("bar.sync 2, %0;" ::"n"(kCvtThreads));
@@ -624,6 +743,45 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const UnitSpans* __restrict__
       PROF(pon, 5);
       if constexpr (MODE == 0) issue_raw(it + kRawBufs - 1);
       PROF(pon, 6);
+    }
+  } else if (kPair && warp == kMmaWarp) {
+    // ================================================ pair MMA issue (the leader only)
+    if (crank == 0) {
+      constexpr uint32_t id64 = idesc_bf16(64, 256), id32 = idesc_bf16(32, 256);
+      const uint64_t db0 = sdesc(smem_u32(wsm), 128, 256);
+      for (int it = 0;; ++it) {
+        const int b = it % Cfg::NB;
+        const uint32_t use = (uint32_t)(it / Cfg::NB);
+        mbar_wait_cluster(&B.full[b], use & 1);   // both CTAs' converters
+        const SuperTile& t = B.desc[it % kDescRing];
+        const bool end = t.fout == nullptr;
+        mbar_wait_cluster(&B.acc_empty[b], (use & 1) ^ 1);   // both CTAs' epilogues
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (end) {   // let both epilogues see the end
+          if (elect_one()) mma_commit_pair(&B.acc_full[b]);
+          __syncwarp();
+          break;
+        }
+        const uint64_t da0 = sdesc(smem_u32(patch0 + b * Cfg::PATCH), Cfg::PS, Cfg::PW * 16);
+        if (elect_one()) {
+#pragma unroll
+          for (int tt = 0; tt < Cfg::ST; ++tt) {
+            if (a.debug & 4) break;
+            const uint32_t d = tmem + (uint32_t)((b * Cfg::ST + tt) * Cfg::ACC);
+#pragma unroll
+            for (int st = 0; st < Cfg::STEPS; ++st) {
+              const uint64_t dah = da0 + (uint64_t)((Cfg::a_off(st) + tt * kTW * 16) >> 4);
+              const uint64_t dal = dah + (uint64_t)((Cfg::NP * Cfg::PS) >> 4);
+              const uint64_t db = db0 + (uint64_t)(st * (kPairStep >> 4));
+              mma_bf16_pair(d, dah, db, id64, st > 0 ? 1u : 0u);            // [xh*wh | xh*wl]
+              mma_bf16_pair(d, dal, db + (1024 >> 4), id32, 1u);            // + xl*wh
+            }
+          }
+          mma_commit_pair(&B.empty[b]);
+          mma_commit_pair(&B.acc_full[b]);
+        }
+        __syncwarp();
+      }
     }
   } else if (warp == kMmaWarp) {
     // ================================================ MMA issue (warp-uniform loop, one lane issues)
@@ -703,7 +861,7 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const UnitSpans* __restrict__
 #pragma unroll
       for (int u = 0; u < TPW; ++u) {
         const int tt = h + 2 * u;
-        ok[u] = t.ox0 + tt * kTW < G.Wo && !(a.debug & 2);
+        ok[u] = t.ox0 + tt * kTW < G.Wo && !(a.debug & 2) && t.pad_ == 0;
         if (ok[u]) {
           const uint32_t taddr =
               tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((b * Cfg::ST + tt) * Cfg::ACC);
@@ -719,7 +877,8 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const UnitSpans* __restrict__
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(&B.acc_empty[b]);
+      if (kPair && crank) mbar_arrive_leader(&B.acc_empty[b]);
+      else mbar_arrive(&B.acc_empty[b]);
       PROF(pon, 13);
 #pragma unroll
       for (int u = 0; u < TPW; ++u) {
@@ -761,9 +920,15 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const UnitSpans* __restrict__
 
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0)
+  if constexpr (kPair) {
+    cluster_sync();   // the peer's TMEM is written by this pair's MMAs until both are done
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(kTmemCols));
+  } else if (warp == 0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(kTmemCols));
+  }
 }
 
 using EncodeTiled = PFN_cuTensorMapEncodeTiled_v12000;
@@ -829,6 +994,36 @@ int launch_conv(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t
   if (rc) return rc;
   conv_units_kernel<<<(unsigned)((n_units + 255) / 256), 256, 0, st>>>(actor, res, units);
   PB_LAUNCHED("conv_units_kernel");
+  if constexpr (MODE == 1) {
+    // CTA pairs (cta_group::2; clusters of 2, an even grid), opt-in with
+    // PB_CONV_PAIR=1: correct, but slower than single CTAs while the
+    // converters bound layer 2
+    const char* pe = getenv("PB_CONV_PAIR");
+    if (pe && pe[0] == '1' && grid >= 2) {
+      static bool pconf[pb::kMaxDevices] = {};
+      if (!pconf[dev]) {
+        PB_CUDA(cudaFuncSetAttribute(conv_pool_kernel<MODE, CIN, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        pconf[dev] = true;
+      }
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((unsigned)(grid & ~1));
+      cfg.blockDim = dim3(kConvThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      PB_CUDA(cudaLaunchKernelEx(&cfg, conv_pool_kernel<MODE, CIN, true>, actor, res,
+                                 (const UnitSpans*)units, tmap));
+      PB_LAUNCHED("conv_pool_kernel<pair>");
+      return PB_OK;
+    }
+  }
   conv_pool_kernel<MODE, CIN><<<grid, kConvThreads, smem, st>>>(actor, res, units, tmap);
   PB_LAUNCHED("conv_pool_kernel");
   return PB_OK;

@@ -112,3 +112,23 @@ def test_conv_shapes(h, w, cin, pad):
     want = oc.conv_relu_pool(x, wt, b, pad)
     got = np.frombuffer(rep.sink_data["sink"], np.float32).reshape(want.shape)
     assert rel_err(got, want) <= ACT_TOL
+
+
+def test_conv_layer2_cta_pair_matches(monkeypatch):
+    """Layer 2 on CTA pairs (cta_group::2 MMAs, M = 256 over a cluster of two,
+    PB_CONV_PAIR=1) gives the same logits as the single-CTA kernel: the same
+    products accumulated in the same order per output."""
+    from paper_1802_06625_b200 import RuntimeConfig, run_streams
+    from paper_1802_06625_b200.apps import vision
+    R, F, S = 4, 5, 3
+    desc = vision.build_description(R, policy="fixed_policy")
+    xs = [vision.make_frames(s, R * F) for s in range(S)]
+
+    def logits():
+        reps = run_streams(desc, S, RuntimeConfig(source_firings=F, capture_sinks=True),
+                           seeds=list(range(S)), sources={"src": [x.tobytes() for x in xs]})
+        return [r.sink_data["sink"] for r in reps]
+    monkeypatch.delenv("PB_CONV_PAIR", raising=False)
+    single = logits()
+    monkeypatch.setenv("PB_CONV_PAIR", "1")
+    assert logits() == single
