@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--exact", action="store_true",
                     help="headline in the bit-exact FIR mode (default: the <= 1e-5 tolerance "
                          "mode the north star states; both modes are always reported)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=7)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-streams", type=int, default=64)
     ap.add_argument("--cpu-blocks", type=int, default=256,
