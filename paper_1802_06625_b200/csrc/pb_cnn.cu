@@ -203,6 +203,7 @@ struct ConvCfg {
 #ifndef PB_CONV_SPLIT3_0
 #define PB_CONV_SPLIT3_0 1
 #endif
+  static constexpr int CIN_ = CIN;
   static constexpr int ST = MODE ? 2 : PB_CONV_ST0;       // tiles per super-tile
   static constexpr int NP = MODE ? CIN / 8 : 2;           // 16-B planes per precision piece
   static constexpr int PW = ST * kTW + (MODE ? 4 : 0);    // patch width (entries)
@@ -222,6 +223,9 @@ struct ConvCfg {
   static constexpr int RAW_W = MODE ? 0 : ((PW + 4) * 3 + 3 + 3) / 4 * 4;   // floats per raw row
   static constexpr int RAW_TX = kPH * RAW_W * 4;          // bytes per box
   static constexpr int RAW = MODE ? 0 : ((RAW_TX + 127) / 128) * 128;
+#ifndef PB_CONV_PAIR_STAGED
+#define PB_CONV_PAIR_STAGED 1
+#endif
 #ifndef PB_CONV_NB0
 #define PB_CONV_NB0 3
 #endif
@@ -440,6 +444,66 @@ __device__ __forceinline__ void raw_issue(uint8_t* raw, uint64_t* bar, const CUt
       : "memory");
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+
+// Layer-2 converter with a cp.async staging ring (CTA-pair kernel, which has
+// the 25 KB the single-CTA weights would occupy free): each thread copies the
+// fp32 items it will convert, two batches ahead, straight into shared memory
+// (out-of-frame items as a zero-size copy, i.e. zero fill) and splits a batch
+// once its own copies have landed -- no registers held across the global-load
+// latency and no barrier (a thread converts exactly the items it copied).
+template <class Cfg>
+__device__ __forceinline__ void fill_patch_staged(uint8_t* patch, uint8_t* stage,
+                                                  const ConvRun& g, const SuperTile& t, int ct) {
+  constexpr int kS = 2;                                   // items per thread per batch
+  constexpr int kBatch = kS * kCvtThreads;
+  constexpr int items = kPH * Cfg::PW * Cfg::NP;
+  constexpr int nb = (items + kBatch - 1) / kBatch;
+  constexpr int kBufBytes = kBatch * 32;
+  auto issue = [&](int bt) {
+    float4* buf = reinterpret_cast<float4*>(stage + (bt & 1) * kBufBytes);
+#pragma unroll
+    for (int u = 0; u < kS; ++u) {
+      const int i = bt * kBatch + u * kCvtThreads + ct;
+      if (i < items) {
+        const int e = i / Cfg::NP, q = i % Cfg::NP;
+        const int iy = t.oy0 + e / Cfg::PW - g.pad, ix = t.ox0 + e % Cfg::PW - g.pad;
+        const bool in = iy >= 0 && iy < g.H && ix >= 0 && ix < g.W;
+        const float* src = in ? t.fin + ((int64_t)iy * g.W + ix) * Cfg::CIN_ + 8 * q : t.fin;
+        float4* d = buf + 2 * (u * kCvtThreads + ct);
+        cp_async16(d, src, in ? 16u : 0u);
+        cp_async16(d + 1, in ? src + 4 : src, in ? 16u : 0u);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue(0);
+  if (nb > 1) issue(1);
+#pragma unroll 1
+  for (int bt = 0; bt < nb; ++bt) {
+    if (bt + 1 < nb) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    const float4* buf = reinterpret_cast<const float4*>(stage + (bt & 1) * kBufBytes);
+#pragma unroll
+    for (int u = 0; u < kS; ++u) {
+      const int i = bt * kBatch + u * kCvtThreads + ct;
+      if (i >= items) break;
+      const float4 a = buf[2 * (u * kCvtThreads + ct)], b = buf[2 * (u * kCvtThreads + ct) + 1];
+      const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      const int e = i / Cfg::NP, q = i % Cfg::NP;
+      uint4 hi, lo;
+      split8(v, hi, lo);
+      *reinterpret_cast<uint4*>(patch + q * Cfg::PS + e * 16) = hi;
+      *reinterpret_cast<uint4*>(patch + (Cfg::NP + q) * Cfg::PS + e * 16) = lo;
+    }
+    if (bt + 2 < nb) issue(bt + 2);
+  }
+}
+
 // Converter: build the bf16 hi/lo entry planes of super-tile `t` in `patch`.
 template <int MODE, int CIN>
 __device__ __forceinline__ void fill_patch(uint8_t* patch, const uint8_t* raw, const ConvRun& g,
@@ -552,6 +616,10 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const UnitSpans* __restrict__
   // pair weights per K-step: 32 B rows (the N = 64 MMA's half: wh on the
   // leader, wl on the peer) then 16 B rows (the N = 32 MMA's half of wh)
   constexpr int kPairStep = 1536;
+  // the converters' cp.async staging ring lives in the tail of the weights
+  // region the pair weights leave free (when it fits: Cin = 32)
+  constexpr bool kStaged = kPair && PB_CONV_PAIR_STAGED &&
+                           Cfg::STEPS * kPairStep + 2 * 2 * kCvtThreads * 32 <= Cfg::WBYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -729,8 +797,12 @@ conv_pool_kernel(pb_conv_actor a, pb_resolved res, const UnitSpans* __restrict__
       PROF(pon, 1);
       mbar_wait(&B.empty[b], (use & 1) ^ 1);
       PROF(pon, 2);
-      if (!(a.debug & 1) && t.pad_ == 0)
-        fill_patch<MODE, CIN>(patch0 + b * Cfg::PATCH, raw0 + rb * Cfg::RAW, G, t, ct);
+      if (!(a.debug & 1) && t.pad_ == 0) {
+        if constexpr (kStaged)   // the free tail of the weights region
+          fill_patch_staged<Cfg>(patch0 + b * Cfg::PATCH, wsm + Cfg::STEPS * kPairStep, G, t, ct);
+        else
+          fill_patch<MODE, CIN>(patch0 + b * Cfg::PATCH, raw0 + rb * Cfg::RAW, G, t, ct);
+      }
       if (ct == 0) B.desc[it % kDescRing] = t;
       PROF(pon, 3);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -995,11 +1067,10 @@ int launch_conv(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t
   conv_units_kernel<<<(unsigned)((n_units + 255) / 256), 256, 0, st>>>(actor, res, units);
   PB_LAUNCHED("conv_units_kernel");
   if constexpr (MODE == 1) {
-    // CTA pairs (cta_group::2; clusters of 2, an even grid), opt-in with
-    // PB_CONV_PAIR=1: correct, but slower than single CTAs while the
-    // converters bound layer 2
+    // CTA pairs (cta_group::2; clusters of 2, an even grid): the default for
+    // layer 2; PB_CONV_PAIR=0 selects the single-CTA kernel
     const char* pe = getenv("PB_CONV_PAIR");
-    if (pe && pe[0] == '1' && grid >= 2) {
+    if (!(pe && pe[0] == '0') && grid >= 2) {
       static bool pconf[pb::kMaxDevices] = {};
       if (!pconf[dev]) {
         PB_CUDA(cudaFuncSetAttribute(conv_pool_kernel<MODE, CIN, true>,

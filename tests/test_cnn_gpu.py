@@ -115,9 +115,9 @@ def test_conv_shapes(h, w, cin, pad):
 
 
 def test_conv_layer2_cta_pair_matches(monkeypatch):
-    """Layer 2 on CTA pairs (cta_group::2 MMAs, M = 256 over a cluster of two,
-    PB_CONV_PAIR=1) gives the same logits as the single-CTA kernel: the same
-    products accumulated in the same order per output."""
+    """Layer 2 on CTA pairs (cta_group::2 MMAs, M = 256 over a cluster of two;
+    the default) gives the same logits as the single-CTA kernel
+    (PB_CONV_PAIR=0): the same products accumulated in the same order."""
     from paper_1802_06625_b200 import RuntimeConfig, run_streams
     from paper_1802_06625_b200.apps import vision
     R, F, S = 4, 5, 3
@@ -128,7 +128,7 @@ def test_conv_layer2_cta_pair_matches(monkeypatch):
         reps = run_streams(desc, S, RuntimeConfig(source_firings=F, capture_sinks=True),
                            seeds=list(range(S)), sources={"src": [x.tobytes() for x in xs]})
         return [r.sink_data["sink"] for r in reps]
-    monkeypatch.delenv("PB_CONV_PAIR", raising=False)
+    monkeypatch.setenv("PB_CONV_PAIR", "0")
     single = logits()
     monkeypatch.setenv("PB_CONV_PAIR", "1")
     assert logits() == single
