@@ -223,6 +223,9 @@ struct ConvCfg {
   static constexpr int RAW_W = MODE ? 0 : ((PW + 4) * 3 + 3 + 3) / 4 * 4;   // floats per raw row
   static constexpr int RAW_TX = kPH * RAW_W * 4;          // bytes per box
   static constexpr int RAW = MODE ? 0 : ((RAW_TX + 127) / 128) * 128;
+#ifndef PB_CONV_L1_EPT   // layer-1 entries per converter thread per batch (loads in flight)
+#define PB_CONV_L1_EPT 4
+#endif
 #ifndef PB_CONV_PAIR_STAGED
 #define PB_CONV_PAIR_STAGED 1
 #endif
@@ -551,10 +554,10 @@ __device__ __forceinline__ void fill_patch(uint8_t* patch, const uint8_t* raw, c
     // entries in pairs: both entries' 30 loads are issued before either is
     // split (one shared-memory latency per pair)
 #pragma unroll 1
-    for (int e0 = ct; e0 < items; e0 += 2 * kCvtThreads) {
-      float v[2][16];
+    for (int e0 = ct; e0 < items; e0 += PB_CONV_L1_EPT * kCvtThreads) {
+      float v[PB_CONV_L1_EPT][16];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < PB_CONV_L1_EPT; ++u) {
         const int e = min(e0 + u * kCvtThreads, items - 1);
         const int r = e / Cfg::PW, c = e % Cfg::PW;
         const float* src = rawf + r * Cfg::RAW_W + c * 3;
@@ -563,7 +566,7 @@ __device__ __forceinline__ void fill_patch(uint8_t* patch, const uint8_t* raw, c
         v[u][15] = 0.f;
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < PB_CONV_L1_EPT; ++u) {
         const int e = e0 + u * kCvtThreads;
         if (e >= items) break;
         uint4 h0, l0, h1, l1;

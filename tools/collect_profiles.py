@@ -58,8 +58,10 @@ if m and p:
 e = last("fir_persistent<1, 0>")
 if e:
     traffic["fir_persistent<bank, EXACT>"] = e["dram_read"] + e["dram_write"]
-for nm in ("conv_pool_kernel<0, 3>", "conv_pool_kernel<1, 32>", "dense_kernel"):
-    x = last(nm)
+# (layer 2 runs as conv_pool_kernel<1, 32, true> on CTA pairs; same key)
+for nm, pat in (("conv_pool_kernel<0, 3>", "conv_pool_kernel<0, 3"),
+                ("conv_pool_kernel<1, 32>", "conv_pool_kernel<1, 32"), ("dense_kernel", "dense_kernel")):
+    x = last(pat)
     if x:
         traffic[nm] = x["dram_read"] + x["dram_write"]
 (prof / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1))
