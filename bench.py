@@ -382,9 +382,10 @@ def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
                      "issued_tflops": 3 * achieved if achieved else None,
                      "issued_frac": 3 * achieved / peak if achieved else None,
                      "note": "useful FLOPs; bf16x3 issues 3 MMA products per useful one "
-                             "(issued_*: the tensor pipe's bf16 work), layer 2 at N=32/64 is "
-                             "shared-memory-read bound (tools/conv_probe); traffic: DRAM bytes "
-                             "of both conv launches from profiles/ncu_traffic.json"},
+                             "(issued_*: the tensor pipe's bf16 work); N=32/64 MMAs are "
+                             "shared-memory-read bound (tools/conv_probe); layer 2 runs on CTA "
+                             "pairs (cta_group::2, half the B reads per SM); traffic: DRAM "
+                             "bytes of both conv launches from profiles/ncu_traffic.json"},
         "e2e": {"value": frames * world / e2e_s, "unit": "frames/s",
                 "h2d_bytes_per_step": frames * vision.FRAME_BYTES,
                 "d2h_bytes_per_step": frames * vision.N_CLASSES * 4,
