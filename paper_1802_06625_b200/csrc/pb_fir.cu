@@ -160,6 +160,10 @@ __device__ __forceinline__ u64 fadd2(u64 a, u64 b) {
   return r;
 }
 
+__device__ __forceinline__ void cp_async16_plan(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
                : "memory");
@@ -839,9 +843,13 @@ __host__ __device__ inline size_t plan_par_smem(int n_iter, int nb) {
          + (size_t)nb * kPC * 4                  // prev
          + (size_t)((n_iter + 15) & ~15);        // have
 }
-// + every span tail up to the chunk end and the branch states (kTails)
+// kTails: the 48-byte aligned tail window (last 12 samples) of both planes of
+// the spans [lo - kTailWin, hi), and the branch states
+constexpr int kTailWin = 32;                      // spans before the chunk with staged tails
+constexpr int kTailF = 12;                        // floats per plane window (16-B multiple)
 __host__ __device__ inline size_t plan_par_tails_smem(int n_iter, int nb) {
-  return plan_par_smem(n_iter, nb) + (size_t)(n_iter + nb) * 2 * kHist * 4;
+  return plan_par_smem(n_iter, nb) + 16 + (size_t)(kPC + kTailWin) * 2 * kTailF * 4 +
+         (size_t)nb * 2 * kHist * 4;
 }
 
 // kTails: every span tail of the stream's spans 0..hi-1 (and each branch's
@@ -866,22 +874,22 @@ bank_plan_par_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* 
   int* prev = reinterpret_cast<int*>(mask + E);                         // [nb][kPC]
   uint8_t* have = reinterpret_cast<uint8_t*>(prev + nb * kPC);          // [hi]
   const int64_t in_base = bank.in.base ? bank.in.base[s] : 0;
-  // kTails layout: tails[hi][2][kHist], then state tails [nb][2][kHist]
-  float* tails = reinterpret_cast<float*>(have + ((E + 15) & ~15));
-  float* stails = tails + (size_t)hi * 2 * kHist;
+  // kTails layout: tails[t0 .. hi)[2][kTailF] (16-byte copies of each plane's
+  // last 12 samples; the history is samples 3..11), then the states [nb][2][kHist]
+  const int t0 = max(0, lo - kTailWin);
+  float* tails = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(have + E) + 15) & ~uintptr_t(15));   // 16-B copies
+  float* stails = tails + (size_t)(kPC + kTailWin) * 2 * kTailF;
   if (kTails) {
-    for (int e = tid; e < (hi + nb) * 2 * kHist; e += kPlanParThreads) {
-      const int t = e / (2 * kHist), q = e - t * 2 * kHist;
-      const float* src;
-      if (t < hi) {
-        const int plane = q / kHist, kk = q - plane * kHist;
-        src = reinterpret_cast<const float*>(span_ptr_b(bank.in, in_base, res, s, t)) +
-              plane * B + B - kHist + kk;
-      } else {
-        src = br[t - hi].state + (int64_t)s * 2 * kHist + q;
-      }
-      cp_async4(tails + e, src);
+    const int nt = hi - t0;
+    for (int e = tid; e < nt * 6; e += kPlanParThreads) {   // 2 planes x 3 x 16 B per span
+      const int t = e / 6, r = e - t * 6, plane = r / 3, part = r - plane * 3;
+      const float* src = reinterpret_cast<const float*>(span_ptr_b(bank.in, in_base, res, s, t0 + t)) +
+                         plane * B + B - kTailF + 4 * part;
+      cp_async16_plan(tails + (t * 2 + plane) * kTailF + 4 * part, src);
     }
+    for (int e = tid; e < nb * 2 * kHist; e += kPlanParThreads)
+      cp_async4(stails + e, br[e / (2 * kHist)].state + (int64_t)s * 2 * kHist + e % (2 * kHist));
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   // 1. taps and activity masks: every load of a thread issued before use
@@ -990,13 +998,35 @@ bank_plan_par_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* 
     for (int b = 0; b < nb; ++b) {
       if (!((m >> b) & 1u)) continue;
       const int pv = prev[b * kPC + i];
-      const float* h = !kTails ? hist + (i * nb + b) * 2 * kHist
-                               : (pv >= 0 ? tails + pv * 2 * kHist : stails + b * 2 * kHist);
       float h_r[kHist], h_i[kHist];
+      if (!kTails) {
+        const float* h = hist + (i * nb + b) * 2 * kHist;
 #pragma unroll
-      for (int q = 0; q < kHist; ++q) {
-        h_r[q] = h[q];
-        h_i[q] = h[kHist + q];
+        for (int q = 0; q < kHist; ++q) {
+          h_r[q] = h[q];
+          h_i[q] = h[kHist + q];
+        }
+      } else if (pv < 0) {   // first firing of the branch: its carried state
+        const float* h = stails + b * 2 * kHist;
+#pragma unroll
+        for (int q = 0; q < kHist; ++q) {
+          h_r[q] = h[q];
+          h_i[q] = h[kHist + q];
+        }
+      } else if (pv >= t0) {   // a staged tail window: samples 3..11
+        const float* h = tails + (pv - t0) * 2 * kTailF;
+#pragma unroll
+        for (int q = 0; q < kHist; ++q) {
+          h_r[q] = h[kTailF - kHist + q];
+          h_i[q] = h[kTailF + kTailF - kHist + q];
+        }
+      } else {   // a firing further back than the window: straight from the ring
+        const float* pvp = reinterpret_cast<const float*>(span_ptr_b(bank.in, in_base, res, s, pv));
+#pragma unroll
+        for (int q = 0; q < kHist; ++q) {
+          h_r[q] = pvp[B - kHist + q];
+          h_i[q] = pvp[2 * B - kHist + q];
+        }
       }
       const float4* tb = taps + b * kTaps;
 #pragma unroll
