@@ -23,8 +23,8 @@ for th in (8, 16, 32):
         t0 = time.perf_counter()
         list(ex.map(lambda s: hashlib.sha256(buf[s]).hexdigest(), range(S)))
         out[f"sha256_GBps_{th}thr"] = buf.nbytes / (time.perf_counter() - t0) / 1e9
-for pipe in (8, 16):
-    for th in (12, 15, 16):
+for pipe in (8, 16, 32):
+    for th in (15, 16):
         rt = DeviceRuntime(pd.build_description(B, 4), config=RuntimeConfig(
             source_firings=blocks, epoch=blocks, pipeline=pipe, exact=False, host_threads=th),
             n_streams=S, seeds=[1000 + s for s in range(S)], sources={"src": [None] * S})
