@@ -971,6 +971,20 @@ class DeviceRuntime:
             sub -= 1
         R = E // sub
         chunks = [(it, min(sub, N - it)) for it in range(0, N, sub)]
+        if N <= E and sub >= 8 and len(chunks) > 2:
+            # one window holds the whole run (no slot reuse): ramp the first
+            # chunks up (sub/4, sub/4, sub/2, then sub) so the hashing threads
+            # -- the end-to-end bottleneck -- start after a quarter of the
+            # copy-in / copy-out latency of a full chunk
+            chunks, it = [], 0
+            for n in (sub // 4, sub // 4, sub // 2):
+                if it < N:
+                    chunks.append((it, min(n, N - it)))
+                    it += chunks[-1][1]
+            while it < N:
+                chunks.append((it, min(sub, N - it)))
+                it += chunks[-1][1]
+            R = len(chunks)
         self._events = []
         h2d_ev = [self._event() for _ in chunks]
         comp_ev = [self._event() for _ in chunks]
@@ -1118,7 +1132,7 @@ class DeviceRuntime:
                             raise ValueError(f"{length} control elements exceed {min_tb} bytes")
                     except Exception as e:  # noqa: BLE001
                         raise ActorPanic(a.id, e) from e
-                    slot = hptr + (c % R) * S * sub * stride
+                    slot = hptr + (it0 % E) * S * stride   # this chunk's [S][n] tokens
                     rc = lib.pb_policy_tokens_streams(
                         C.addressof(self.policy_state[ref]), S, native_policy_kind(b0), length,
                         param, it0, n, slot, stride, int(self.config.host_threads))
