@@ -185,6 +185,13 @@ typedef struct {
 int pb_rings_advance(const pb_ring_advance_t* rings /* host array */, int n_rings,
                      pb_resolved res, void* stream);
 
+/* pb_eq1_check + pb_rings_advance of one epoch in one launch (independent
+ * blocks; at most 256 ports and 256 rings).  The Eq. 1 recheck only reads the
+ * resolution, so it can close the epoch after the actor firings. */
+int pb_epoch_close(const pb_eq1_port* ports /* host array */, int n_ports, int64_t* counters,
+                   const pb_ring_advance_t* rings /* host array */, int n_rings,
+                   pb_resolved res, void* stream);
+
 /* --------------------------------------------------------- span addressing */
 /* Where the span of a port lives for firing at iteration n of stream s:
  *   idx   = index_cond < 0 ? n : prefix[index_cond][s][n]

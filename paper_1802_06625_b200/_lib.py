@@ -172,6 +172,8 @@ SIGNATURES = {
     "pb_resolve": (C.c_int, [C.POINTER(Condition), Resolved, vp]),
     "pb_eq1_check": (C.c_int, [C.POINTER(Eq1Port), C.c_int, Resolved, vp, vp]),
     "pb_rings_advance": (C.c_int, [C.POINTER(RingAdvance), C.c_int, Resolved, vp]),
+    "pb_epoch_close": (C.c_int, [C.POINTER(Eq1Port), C.c_int, vp, C.POINTER(RingAdvance),
+                                 C.c_int, Resolved, vp]),
     "pb_fire_fir": (C.c_int, [vp, C.c_int, Resolved, i64, C.c_int, vp]),
     "pb_fir_carry": (C.c_int, [vp, C.c_int, Resolved, i64, vp]),
     "pb_fire_filter_bank": (C.c_int, [FilterBank, Resolved, i64, vp]),

@@ -132,9 +132,71 @@ __global__ void advance_kernel(RingTable table, int n_rings, pb_resolved res) {
   *rd += cnt;
 }
 
+// Eq. 1 recheck and ring advance of one epoch in one launch: blocks
+// [0, S * n_ports) are eq1_kernel's (stream, port) blocks, the rest
+// advance_kernel's.  The two touch disjoint data (Eq. 1 reads the resolution
+// and adds to its counters; the advance updates ring counters), so the
+// launch is one kernel's latency instead of two.
+__global__ void __launch_bounds__(128)
+epoch_close_kernel(Eq1Table eq, int n_ports, int64_t* counters, RingTable rings, int n_rings,
+                   pb_resolved res) {
+  pb::pdl_enter();
+  const int n_eq1_blocks = res.n_streams * n_ports;
+  if ((int)blockIdx.x < n_eq1_blocks) {
+    const int s = blockIdx.x % res.n_streams;
+    const pb_eq1_port& p = eq.p[blockIdx.x / res.n_streams];
+    int checks = 0, failures = 0;
+    for (int n = threadIdx.x; n < res.n_iter; n += blockDim.x) {
+      if (!pb::active(res, p.actor_cond, s, n)) continue;
+      ++checks;
+      failures += pb::active(res, p.own_cond, s, n) != pb::active(res, p.moved_cond, s, n);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      checks += __shfl_down_sync(0xffffffffu, checks, o);
+      failures += __shfl_down_sync(0xffffffffu, failures, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (checks) atomicAdd((unsigned long long*)&counters[0], (unsigned long long)checks);
+      if (failures) atomicAdd((unsigned long long*)&counters[1], (unsigned long long)failures);
+    }
+    return;
+  }
+  const int i = ((int)blockIdx.x - n_eq1_blocks) * blockDim.x + threadIdx.x;
+  if (i >= n_rings * res.n_streams) return;
+  const int r = i / res.n_streams, s = i % res.n_streams;
+  const pb_ring_advance_t& ra = rings.r[r];
+  int64_t* w = ra.counters + s;
+  int64_t* rd = ra.counters + res.n_streams + s;
+  int64_t* mx = ra.counters + 2 * (int64_t)res.n_streams + s;
+  const int64_t cnt = pb::cond_count(res, ra.cond, s);
+  const int64_t occ = ra.delay + (int64_t)ra.rate * (*w + cnt - *rd);
+  if (occ > *mx) *mx = occ;
+  *w += cnt;
+  *rd += cnt;
+}
+
 }  // namespace
 
 extern "C" {
+
+int pb_epoch_close(const pb_eq1_port* ports, int n_ports, int64_t* counters,
+                   const pb_ring_advance_t* rings, int n_rings, pb_resolved res, void* stream) {
+  if (n_ports < 0 || n_ports > kMaxEq1 || n_rings < 0 || n_rings > kMaxRings)
+    return pb::fail(PB_E_UNSUPPORTED, "pb_epoch_close: at most " + std::to_string(kMaxEq1) +
+                                          " ports and " + std::to_string(kMaxRings) + " rings");
+  if (res.n_iter == 0) n_ports = 0;
+  if (n_ports == 0 && n_rings == 0) return PB_OK;
+  Eq1Table e{};
+  for (int k = 0; k < n_ports; ++k) e.p[k] = ports[k];
+  RingTable t{};
+  for (int k = 0; k < n_rings; ++k) t.r[k] = rings[k];
+  const int blocks = res.n_streams * n_ports + (n_rings * res.n_streams + 127) / 128;
+  PB_LAUNCH_PDL(epoch_close_kernel, blocks, 128, 0, pb::as_stream(stream), e, n_ports, counters,
+                t, n_rings, res);
+  PB_LAUNCHED("epoch_close_kernel");
+  return PB_OK;
+}
+
 
 int pb_resolve(const pb_condition* conds, pb_resolved res, void* stream) {
   if (res.n_cond == 0 || res.n_iter == 0) return PB_OK;

@@ -761,7 +761,11 @@ class DeviceRuntime:
         if self.plan.conds:
             conds = self._conditions(it0)
             _lib.check(lib.pb_resolve(conds, res, st), "pb_resolve")
-        if self.n_eq1:
+        # the Eq. 1 recheck closes the epoch together with the ring advance
+        # (pb_epoch_close: one launch); PB_EPOCH_CLOSE=0 keeps them apart
+        close = (self.n_eq1 <= 256 and len(self.advance) <= 256 and
+                 os.environ.get("PB_EPOCH_CLOSE", "1") != "0")
+        if self.n_eq1 and not close:
             _lib.check(lib.pb_eq1_check(self.eq1, self.n_eq1, res, self.eq1_ctr, st),
                        "pb_eq1_check")
         for item in self.launches:
@@ -793,8 +797,12 @@ class DeviceRuntime:
                 hook(kind, "post")
         for dev, n, block in self.fir_groups:
             _lib.check(lib.pb_fir_carry(dev, n, res, block, st), "fir_carry")
-        _lib.check(lib.pb_rings_advance(self.advance, len(self.advance), res, st),
-                   "pb_rings_advance")
+        if close:
+            _lib.check(lib.pb_epoch_close(self.eq1, self.n_eq1, self.eq1_ctr, self.advance,
+                                          len(self.advance), res, st), "pb_epoch_close")
+        else:
+            _lib.check(lib.pb_rings_advance(self.advance, len(self.advance), res, st),
+                       "pb_rings_advance")
         return lib.pb_launch_count() - n0
 
     def set_fir_math(self, math: int) -> None:
