@@ -826,6 +826,9 @@ bank_plan_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPla
 #ifndef PB_PLAN_TAILS
 #define PB_PLAN_TAILS 1
 #endif
+#ifndef PB_PLAN_PREFIX   // previous firings from the resolution's prefix / worklist
+#define PB_PLAN_PREFIX 1
+#endif
 #ifndef PB_PLAN_STOP   // profiling: end the planner after phase 1/2/3
 #define PB_PLAN_STOP 0
 #endif
@@ -899,49 +902,75 @@ bank_plan_par_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* 
     const float cr = tp[t], ci = tp[kTaps + t];
     taps[e] = make_float4(cr, ci, ci, cr);
   }
+  if (PB_PLAN_PREFIX && kTails && bank.actor_cond < 0) {
+    // 1-2 from the resolution: per (span of this chunk, branch) the activity
+    // and the previous firing (worklist[prefix - 1]), two dependent loads, no
+    // mask walk over [0, hi) and no scan
+    for (int n = lo + tid; n < hi; n += kPlanParThreads) {
+      mask[n] = 0u;
+      have[n] = 1;
+    }
+    __syncthreads();
+    for (int e = tid; e < np * nb; e += kPlanParThreads) {
+      const int i = e / nb, b = e - i * nb, n = lo + i;
+      const int c = br[b].cond;
+      bool act = true;
+      int pv = n - 1;   // a branch without its own condition fires every iteration
+      if (c >= 0) {
+        const int64_t row = ((int64_t)c * res.n_streams + s) * res.cap;
+        act = res.act[row + n] != 0;
+        const int j = res.prefix[row + n];
+        pv = j == 0 ? -1 : res.worklist[row + j - 1];
+      }
+      prev[b * kPC + i] = pv;
+      if (act) atomicOr(&mask[n], 1u << b);
+    }
+    __syncthreads();
+  } else {
   for (int n = tid; n < hi; n += kPlanParThreads) {
-    const int64_t col = (int64_t)s * res.cap + n;
-    const int64_t stride = (int64_t)res.n_streams * res.cap;
-    uint8_t a[kMaxBr];
-#pragma unroll
-    for (int b = 0; b < kMaxBr; ++b) {
-      const int c = b < nb ? br[b].cond : -1;
-      a[b] = c < 0 ? 1 : res.act[c * stride + col];
+      const int64_t col = (int64_t)s * res.cap + n;
+      const int64_t stride = (int64_t)res.n_streams * res.cap;
+      uint8_t a[kMaxBr];
+  #pragma unroll
+      for (int b = 0; b < kMaxBr; ++b) {
+        const int c = b < nb ? br[b].cond : -1;
+        a[b] = c < 0 ? 1 : res.act[c * stride + col];
+      }
+      const bool h = bank.actor_cond < 0 || res.act[bank.actor_cond * stride + col];
+      uint32_t m = 0;
+  #pragma unroll
+      for (int b = 0; b < kMaxBr; ++b)
+        if (b < nb && a[b]) m |= 1u << b;
+      mask[n] = h ? m : 0u;
+      have[n] = h;
     }
-    const bool h = bank.actor_cond < 0 || res.act[bank.actor_cond * stride + col];
-    uint32_t m = 0;
-#pragma unroll
-    for (int b = 0; b < kMaxBr; ++b)
-      if (b < nb && a[b]) m |= 1u << b;
-    mask[n] = h ? m : 0u;
-    have[n] = h;
+    __syncthreads();
+  #if PB_PLAN_STOP == 1
+    return;
+  #endif
+    // 2. previous firing of each branch before span n, n in [lo, hi): warp
+    //    max-scan over [0, hi)
+    const int chunk = (hi + 31) / 32;
+    for (int b = warp; b < nb; b += kPlanParThreads / 32) {
+      const int a0 = lane * chunk, a1 = min(hi, a0 + chunk);
+      int last = -1;
+      for (int n = a0; n < a1; ++n)
+        if ((mask[n] >> b) & 1u) last = n;
+      int carry = last;
+  #pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, carry, d);
+        if (lane >= d) carry = max(carry, o);
+      }
+      int cur = __shfl_up_sync(0xffffffffu, carry, 1);
+      if (lane == 0) cur = -1;
+      for (int n = a0; n < a1; ++n) {
+        if (n >= lo) prev[b * kPC + n - lo] = cur;
+        if ((mask[n] >> b) & 1u) cur = n;
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
-#if PB_PLAN_STOP == 1
-  return;
-#endif
-  // 2. previous firing of each branch before span n, n in [lo, hi): warp
-  //    max-scan over [0, hi)
-  const int chunk = (hi + 31) / 32;
-  for (int b = warp; b < nb; b += kPlanParThreads / 32) {
-    const int a0 = lane * chunk, a1 = min(hi, a0 + chunk);
-    int last = -1;
-    for (int n = a0; n < a1; ++n)
-      if ((mask[n] >> b) & 1u) last = n;
-    int carry = last;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int o = __shfl_up_sync(0xffffffffu, carry, d);
-      if (lane >= d) carry = max(carry, o);
-    }
-    int cur = __shfl_up_sync(0xffffffffu, carry, 1);
-    if (lane == 0) cur = -1;
-    for (int n = a0; n < a1; ++n) {
-      if (n >= lo) prev[b * kPC + n - lo] = cur;
-      if ((mask[n] >> b) & 1u) cur = n;
-    }
-  }
-  __syncthreads();
 #if PB_PLAN_STOP == 2
   return;
 #endif
