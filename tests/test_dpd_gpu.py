@@ -18,9 +18,13 @@ def dpd_graph(tmp_path, data: bytes, block=256, branches=4, min_active=2):
     return pd.build_description(block, branches, str(p), min_active)
 
 
+@pytest.mark.parametrize("epoch_close", ["1", "0"])
 @pytest.mark.parametrize("fuse", [True, False])
 @pytest.mark.parametrize("epoch", [4096, 7])
-def test_default_app_digest(golden, tmp_path, fuse, epoch):
+def test_default_app_digest(golden, tmp_path, monkeypatch, fuse, epoch, epoch_close):
+    # epoch_close "1": the Eq. 1 recheck and the ring advance in one launch
+    # (pb_epoch_close); "0": pb_eq1_check after resolve, pb_rings_advance at the end
+    monkeypatch.setenv("PB_EPOCH_CLOSE", epoch_close)
     g = golden["dpd"]["default"]
     desc = dpd_graph(tmp_path, pd.make_input(11, 160))
     rep = run(desc, config=RuntimeConfig(source_firings=160, seed=11, fuse=fuse, epoch=epoch))
