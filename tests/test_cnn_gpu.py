@@ -132,3 +132,32 @@ def test_conv_layer2_cta_pair_matches(monkeypatch):
     single = logits()
     monkeypatch.setenv("PB_CONV_PAIR", "1")
     assert logits() == single
+
+
+def test_vision_graph_full_c3_size():
+    """BASELINE config 3 at the bench's size (4 streams x 64 firings x 24
+    frames = 6144 frames, adaptive alternate_policy): every bypassed firing
+    carries the marker exactly, firing counts exact, a sample of processed
+    firings (first and last of each stream) within the logit tolerance and
+    top-1 equal against the oracle, identical digests across two runs."""
+    R, firings, S = 24, 64, 4
+    xs = [vision.make_frames(s, R * firings) for s in range(S)]
+    desc = vision.build_description(R)
+
+    def go():
+        return run_streams(desc, S, RuntimeConfig(source_firings=firings, epoch=firings,
+                                                  capture_sinks=True),
+                           seeds=[5 + s for s in range(S)], sources={"src": [x.tobytes() for x in xs]})
+    reps = go()
+    p = oc.graph_params(desc)
+    for s in range(S):
+        logits = np.frombuffer(reps[s].sink_data["sink"], np.float32).reshape(firings, R, 4)
+        assert (logits[1::2] == np.float32(p["marker"])).all(), s
+        for j in (0, firings - 2):
+            want = oc.forward(xs[s][j * R:j * R + 2], p)["logits"]
+            err = float(np.abs(logits[j, :2] - want).max())
+            assert err <= LOGIT_TOL, (s, j, err)
+            assert (logits[j, :2].argmax(-1) == want.argmax(-1)).all()
+        fc = reps[s].firing_counts
+        assert fc["l1"] == fc["l2"] == fc["l3"] == firings // 2 and fc["sink"] == firings
+    assert [r.sink_digests for r in go()] == [r.sink_digests for r in reps]
