@@ -110,6 +110,11 @@ __global__ void path_merge_kernel(pb_path_merge_actor a, pb_resolved res) {
   }
 }
 
+#ifndef PB_MATMUL_MF
+#define PB_MATMUL_MF 4
+#endif
+constexpr int kMF = PB_MATMUL_MF;   // firings per lane group (matmul_packed_kernel)
+
 // MatMul.fire for N*N/4 <= 32 dividing 32 (the reference's 8x8: 16 lanes
 // per firing, two firings per warp): the group's first lane resolves the
 // firing's spans once; each lane computes 4 consecutive outputs of one row
@@ -123,30 +128,48 @@ matmul_packed_kernel(pb_matmul_actor a, pb_resolved res, int L) {
   __syncthreads();
   const int fpw = 32 / L;
   const int g = lane / L, sub = lane - g * L;
-  const int j = ((int)blockIdx.x * 8 + (threadIdx.x >> 5)) * fpw + g;   // firing index
+  // each lane group takes kMF consecutive firings: the leader resolves all of
+  // them at once (independent load chains), every lane then has kMF x N
+  // row loads in flight
+  const int j0 = (((int)blockIdx.x * 8 + (threadIdx.x >> 5)) * fpw + g) * kMF;
   const int leader = g * L;
   const unsigned grp = (L == 32 ? 0xffffffffu : ((1u << L) - 1u) << leader);
-  if (j >= pb::cond_count(res, a.cond, s)) return;   // whole lane groups leave together
-  const float* x = nullptr;
-  float* out = nullptr;
-  if (sub == 0) {
-    const int n = pb::firing_iter(res, a.cond, s, j);
-    x = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n));
-    out = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
+  const int cnt = pb::cond_count(res, a.cond, s);
+  if (j0 >= cnt) return;   // whole lane groups leave together
+  const float* x[kMF];
+  float* out[kMF];
+#pragma unroll
+  for (int f = 0; f < kMF; ++f) {
+    x[f] = nullptr;
+    out[f] = nullptr;
+    if (sub == 0 && j0 + f < cnt) {
+      const int n = pb::firing_iter(res, a.cond, s, j0 + f);
+      x[f] = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n));
+      out[f] = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
+    }
   }
-  x = reinterpret_cast<const float*>(__shfl_sync(grp, reinterpret_cast<unsigned long long>(x), leader));
-  out = reinterpret_cast<float*>(__shfl_sync(grp, reinterpret_cast<unsigned long long>(out), leader));
+#pragma unroll
+  for (int f = 0; f < kMF; ++f) {
+    x[f] = reinterpret_cast<const float*>(
+        __shfl_sync(grp, reinterpret_cast<unsigned long long>(x[f]), leader));
+    out[f] = reinterpret_cast<float*>(
+        __shfl_sync(grp, reinterpret_cast<unsigned long long>(out[f]), leader));
+  }
   const int e0 = 4 * sub, i = e0 / N, c0 = e0 - i * N;
-  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-  for (int k = 0; k < N; ++k) {
-    const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k * N + c0));
-    const float wk = w[i * N + k];
-    acc[0] = __fadd_rn(acc[0], __fmul_rn(wk, xv.x));
-    acc[1] = __fadd_rn(acc[1], __fmul_rn(wk, xv.y));
-    acc[2] = __fadd_rn(acc[2], __fmul_rn(wk, xv.z));
-    acc[3] = __fadd_rn(acc[3], __fmul_rn(wk, xv.w));
+#pragma unroll
+  for (int f = 0; f < kMF; ++f) {
+    if (x[f] == nullptr) continue;
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int k = 0; k < N; ++k) {
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(x[f] + k * N + c0));
+      const float wk = w[i * N + k];
+      acc[0] = __fadd_rn(acc[0], __fmul_rn(wk, xv.x));
+      acc[1] = __fadd_rn(acc[1], __fmul_rn(wk, xv.y));
+      acc[2] = __fadd_rn(acc[2], __fmul_rn(wk, xv.z));
+      acc[3] = __fadd_rn(acc[3], __fmul_rn(wk, xv.w));
+    }
+    reinterpret_cast<float4*>(out[f])[sub] = make_float4(acc[0], acc[1], acc[2], acc[3]);
   }
-  reinterpret_cast<float4*>(out)[sub] = make_float4(acc[0], acc[1], acc[2], acc[3]);
 }
 
 // Packed form for tokens of 16..512 bytes in 16-byte units (the reference's
@@ -228,7 +251,7 @@ int pb_fire_matmul(pb_matmul_actor actor, pb_resolved res, void* stream) {
   const int NN = actor.n * actor.n;
   if (actor.n < 1 || NN > 1024) return pb::fail(PB_E_UNSUPPORTED, "matmul: N*N must be <= 1024");
   if (actor.n % 4 == 0 && NN <= 128 && 32 % (NN / 4) == 0) {
-    const int L = NN / 4, per_cta = 8 * (32 / L);
+    const int L = NN / 4, per_cta = 8 * (32 / L) * kMF;
     dim3 grid((unsigned)((res.n_iter + per_cta - 1) / per_cta), res.n_streams);
     matmul_packed_kernel<<<grid, 256, 0, pb::as_stream(stream)>>>(actor, res, L);
     PB_LAUNCHED("matmul_packed_kernel");
