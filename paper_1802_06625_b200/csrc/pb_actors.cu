@@ -179,44 +179,63 @@ matmul_packed_kernel(pb_matmul_actor a, pb_resolved res, int L) {
 __global__ void __launch_bounds__(256)
 path_merge_packed_kernel(pb_path_merge_actor a, pb_resolved res, int L) {
   const int s = blockIdx.y, lane = threadIdx.x & 31;
-  const int fpw = 32 / L;                                // firings per warp
+  const int fpw = 32 / L;                                // lane groups per warp
   const int g = lane / L, sub = lane - g * L;
-  const int n = ((int)blockIdx.x * 8 + (threadIdx.x >> 5)) * fpw + g;
+  // kMF consecutive iterations per lane group, resolved together by its leader
+  const int n0 = (((int)blockIdx.x * 8 + (threadIdx.x >> 5)) * fpw + g) * kMF;
   const int leader = g * L;
   const unsigned grp = (L == 32 ? 0xffffffffu : ((1u << L) - 1u) << leader);
-  if (n >= res.n_iter) return;   // whole lane groups leave together
-  int state = 0;                 // 0: idle, 1: forward, 2: forward + marker, 3: error
-  const float4* x = nullptr;
-  float4* out = nullptr;
-  if (sub == 0 && pb::active(res, a.cond, s, n)) {
-    int live = -1, n_live = 0;
-    for (int p = 0; p < a.n_in; ++p)
-      if (pb::active(res, a.in[p].act_cond, s, n)) {
-        live = p;
-        ++n_live;
+  if (n0 >= res.n_iter) return;   // whole lane groups leave together
+  int state[kMF];                 // 0: idle, 1: forward, 2: forward + marker, 3: error
+  const float4* x[kMF];
+  float4* out[kMF];
+#pragma unroll
+  for (int f = 0; f < kMF; ++f) {
+    const int n = n0 + f;
+    state[f] = 0;
+    x[f] = nullptr;
+    out[f] = nullptr;
+    if (sub == 0 && n < res.n_iter && pb::active(res, a.cond, s, n)) {
+      int live = -1, n_live = 0;
+      for (int p = 0; p < a.n_in; ++p)
+        if (pb::active(res, a.in[p].act_cond, s, n)) {
+          live = p;
+          ++n_live;
+        }
+      if (n_live != 1) {
+        state[f] = 3;
+      } else {
+        x[f] = reinterpret_cast<const float4*>(pb::span_ptr(a.in[live], res, s, n));
+        out[f] = reinterpret_cast<float4*>(pb::span_ptr(a.out, res, s, n));
+        state[f] = live == a.bypass_index ? 2 : 1;
       }
-    if (n_live != 1) {
-      state = 3;
-    } else {
-      x = reinterpret_cast<const float4*>(pb::span_ptr(a.in[live], res, s, n));
-      out = reinterpret_cast<float4*>(pb::span_ptr(a.out, res, s, n));
-      state = live == a.bypass_index ? 2 : 1;
     }
   }
-  state = __shfl_sync(grp, state, leader);
-  if (state == 0) return;
-  if (state == 3) {
-    if (sub == 0) atomicExch(a.error_flag, 1);
-    return;
+#pragma unroll
+  for (int f = 0; f < kMF; ++f) {
+    state[f] = __shfl_sync(grp, state[f], leader);
+    x[f] = reinterpret_cast<const float4*>(
+        __shfl_sync(grp, reinterpret_cast<unsigned long long>(x[f]), leader));
+    out[f] = reinterpret_cast<float4*>(
+        __shfl_sync(grp, reinterpret_cast<unsigned long long>(out[f]), leader));
   }
-  x = reinterpret_cast<const float4*>(__shfl_sync(grp, reinterpret_cast<unsigned long long>(x), leader));
-  out = reinterpret_cast<float4*>(__shfl_sync(grp, reinterpret_cast<unsigned long long>(out), leader));
-  float4 v = x[sub];
-  if (state == 2) {
-    v.x = __fadd_rn(v.x, a.marker); v.y = __fadd_rn(v.y, a.marker);
-    v.z = __fadd_rn(v.z, a.marker); v.w = __fadd_rn(v.w, a.marker);
+  float4 v[kMF];
+#pragma unroll
+  for (int f = 0; f < kMF; ++f)
+    if (state[f] == 1 || state[f] == 2) v[f] = x[f][sub];
+#pragma unroll
+  for (int f = 0; f < kMF; ++f) {
+    if (state[f] == 3) {
+      if (sub == 0) atomicExch(a.error_flag, 1);
+    } else if (state[f] != 0) {
+      float4 w = v[f];
+      if (state[f] == 2) {
+        w.x = __fadd_rn(w.x, a.marker); w.y = __fadd_rn(w.y, a.marker);
+        w.z = __fadd_rn(w.z, a.marker); w.w = __fadd_rn(w.w, a.marker);
+      }
+      out[f][sub] = w;
+    }
   }
-  out[sub] = v;
 }
 
 }  // namespace
@@ -270,7 +289,7 @@ int pb_fire_path_merge(pb_path_merge_actor actor, pb_resolved res, void* stream)
   if (actor.n_in > PB_MAX_PORTS) return pb::fail(PB_E_INVALID, "path_merge: too many ports");
   const int64_t sb = actor.out.span_bytes;
   if (sb % 16 == 0 && sb >= 16 && sb <= 512 && 32 % (sb / 16) == 0) {
-    const int L = (int)(sb / 16), per_cta = 8 * (32 / L);
+    const int L = (int)(sb / 16), per_cta = 8 * (32 / L) * kMF;
     dim3 grid((res.n_iter + per_cta - 1) / per_cta, res.n_streams);
     path_merge_packed_kernel<<<grid, 256, 0, pb::as_stream(stream)>>>(actor, res, L);
     PB_LAUNCHED("path_merge_packed_kernel");
