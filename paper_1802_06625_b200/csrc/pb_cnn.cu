@@ -1350,18 +1350,33 @@ __global__ void classify_kernel(pb_classify_actor a, pb_resolved res) {
     return;
   }
   const float* x = reinterpret_cast<const float*>(pb::span_ptr(a.chain, res, s, n));
-  extern __shared__ float hid[];   // [frames][nhid]
+  // the firing's inputs (ReLU applied once) and both weight matrices are
+  // staged in shared memory with coalesced loads; the dot products then run
+  // from shared memory in the same order as before
+  extern __shared__ float csm[];
+  float* hid = csm;                                   // [frames][nhid]
+  float* xs = hid + a.frames * a.nhid;                // [frames][nin], relu(x)
+  const int ws = a.nin | 1;                           // odd row stride: conflict-free rows
+  float* w4 = xs + a.frames * a.nin;                  // [nhid][ws]
+  float* w5 = w4 + a.nhid * ws;                       // [nout][nhid]
+  for (int e = threadIdx.x; e < a.frames * a.nin; e += blockDim.x) xs[e] = fmaxf(x[e], 0.f);
+  for (int e = threadIdx.x; e < a.nhid * a.nin; e += blockDim.x)
+    w4[(e / a.nin) * ws + e % a.nin] = a.w4[e];
+  for (int e = threadIdx.x; e < a.nout * a.nhid; e += blockDim.x) w5[e] = a.w5[e];
+  __syncthreads();
   for (int e = threadIdx.x; e < a.frames * a.nhid; e += blockDim.x) {
     const int f = e / a.nhid, h = e % a.nhid;
     float acc = a.b4[h];
-    for (int k = 0; k < a.nin; ++k) acc = fmaf(a.w4[h * a.nin + k], fmaxf(x[f * a.nin + k], 0.f), acc);
+    const float* wr = w4 + h * ws;
+    const float* xr = xs + f * a.nin;
+    for (int k = 0; k < a.nin; ++k) acc = fmaf(wr[k], xr[k], acc);
     hid[e] = fmaxf(acc, 0.f);
   }
   __syncthreads();
   for (int e = threadIdx.x; e < a.frames * a.nout; e += blockDim.x) {
     const int f = e / a.nout, o = e % a.nout;
     float acc = a.b5[o];
-    for (int k = 0; k < a.nhid; ++k) acc = fmaf(a.w5[o * a.nhid + k], hid[f * a.nhid + k], acc);
+    for (int k = 0; k < a.nhid; ++k) acc = fmaf(w5[o * a.nhid + k], hid[f * a.nhid + k], acc);
     out[e] = acc;
   }
 }
@@ -1440,7 +1455,19 @@ int pb_fire_dense(pb_dense_actor actor, pb_resolved res, void* stream) {
 int pb_fire_classify(pb_classify_actor actor, pb_resolved res, void* stream) {
   if (res.n_iter == 0) return PB_OK;
   dim3 grid(res.n_iter, res.n_streams);
-  const size_t smem = sizeof(float) * actor.frames * actor.nhid;
+  const size_t smem = sizeof(float) * ((size_t)actor.frames * actor.nhid +
+                                       (size_t)actor.frames * actor.nin +
+                                       (size_t)actor.nhid * (actor.nin | 1) +
+                                       (size_t)actor.nout * actor.nhid);
+  if (smem > 200 * 1024) return pb::fail(PB_E_UNSUPPORTED, "classify: layers too large");
+  const int dev = pb::device();
+  if (dev < 0) return PB_E_CUDA;
+  static bool attr[pb::kMaxDevices] = {};
+  if (!attr[dev]) {
+    PB_CUDA(cudaFuncSetAttribute(classify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024));
+    attr[dev] = true;
+  }
   classify_kernel<<<grid, 256, smem, pb::as_stream(stream)>>>(actor, res);
   PB_LAUNCHED("classify_kernel");
   return PB_OK;
