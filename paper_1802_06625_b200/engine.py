@@ -136,6 +136,15 @@ class _Dev:
         self.rings, self.dev, self.host = [], [], []
 
 
+def _default_hashers() -> int:
+    """Hashing threads of the pipelined run: this process's share of the host
+    cores (torchrun's LOCAL_WORLD_SIZE processes per host) minus one for the
+    orchestrating thread, at most 16 (tools/e2e_probe2.py: 15 threads on 16
+    cores beat 16)."""
+    share = (os.cpu_count() or 16) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+    return max(1, min(16, share - 1))
+
+
 @dataclass
 class _Storage:
     """Where a FIFO's spans live (its own ring or an alias of another's)."""
@@ -1019,7 +1028,7 @@ class DeviceRuntime:
         # is balanced dynamically across the hashing threads (a static split
         # stalls the whole pipeline on whichever thread loses its core).
         jobs = [(a, f, s) for a, f in sinks for s in range(S)]
-        n_thr = max(1, min(len(jobs), int(self.config.host_threads or 16)))
+        n_thr = max(1, min(len(jobs), int(self.config.host_threads or _default_hashers())))
         recorded = [threading.Event() for _ in chunks]     # d2h_ev[c] has been recorded
         hashed = [0] * len(chunks)                          # jobs done with chunk c
         hashed_cv = threading.Condition()
