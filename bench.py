@@ -74,6 +74,28 @@ def dist_env():
     return rank, world, local
 
 
+def relaunch(args) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks (one process per
+    GPU) through torch.distributed.run on 127.0.0.1 with this same command
+    line; rank 0 prints the JSON line.  Returns the launcher's exit code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def workload_name(S: int, blocks: int, B: int, K: int) -> str:
+    """The C2 workload string both arms report (config.workload)."""
+    return (f"C2 DPD: {S} streams/GPU x {blocks} blocks x {B} samples, K={K} branches, "
+            f"subset_policy control per block")
+
+
 # ------------------------------------------------------------ clocks sampler
 
 class Clocks:
@@ -168,19 +190,27 @@ class CpuReference:
         self.cores = os.cpu_count() or 1
         self.dir = tempfile.mkdtemp(prefix="prune_ref_")
         from paper_1802_06625_b200.apps import predistortion as pd
-        self.jobs = []
+        self.paths = []
         for s in range(streams):
             path = os.path.join(self.dir, f"s{s}.bin")
             pd.stream_input(s, blocks, block).tofile(path)
-            self.jobs.append((path, blocks, 1000 + s, block, branches))
-        self.samples = streams * blocks * block
+            self.paths.append(path)
+        self.streams, self.block, self.branches = streams, block, branches
+        self.set_blocks(blocks)
         ctx = mp.get_context("fork")
         init = _ref_worker_init if self.kind == "reference" else None
         self.pool = ctx.Pool(self.cores, initializer=init,
                              initargs=(block, branches) if init else ())
         self.fn = _ref_run_stream if self.kind == "reference" else _oracle_run_stream
-        self.sample = (f"{streams} streams x {blocks} blocks x {block} samples of the C2 "
-                       f"workload (K={branches}), one process per core")
+
+    def set_blocks(self, blocks: int) -> None:
+        """Blocks per stream of one step (a prefix of each stream's input)."""
+        self.blocks = blocks
+        self.jobs = [(p, blocks, 1000 + s, self.block, self.branches)
+                     for s, p in enumerate(self.paths)]
+        self.samples = self.streams * blocks * self.block
+        self.sample = (f"{self.streams} streams x {blocks} blocks x {self.block} samples of "
+                       f"the C2 workload (K={self.branches}), one process per core")
 
     def step(self) -> float:
         t0 = time.perf_counter()
@@ -192,22 +222,37 @@ class CpuReference:
         self.pool.join()
 
 
+REFERENCE_BUDGET_S = 150.0   # whole --impl reference run (warm-up + timed steps)
+
+
 def run_reference(args, rank, world):
+    """The reference arm: --steps timed steps after --warmup untimed ones, each
+    step one pass of the reference interpreter over a bounded sample of the C2
+    workload.  The first warm-up step runs the whole per-GPU workload; if
+    (steps + warmup) such passes would exceed REFERENCE_BUDGET_S the remaining
+    steps run a prefix of every stream (fewer blocks, same 64 streams)."""
     if rank != 0:
         return
     ref = CpuReference(args.cpu_streams, args.cpu_blocks, args.block, args.branches)
-    for _ in range(max(1, min(args.warmup, 1))):
+    warm = max(1, args.warmup)
+    t_full = ref.step()
+    left = (args.steps + warm - 1) * t_full
+    if left > REFERENCE_BUDGET_S:
+        ref.set_blocks(max(1, int(args.cpu_blocks * REFERENCE_BUDGET_S / left)))
+    for _ in range(warm - 1):
         ref.step()
-    times = [ref.step() for _ in range(max(1, min(args.steps, 5)))]
+    times = [ref.step() for _ in range(max(1, args.steps))]
     ref.close()
     t = statistics.mean(times)
     value = ref.samples / t / 1e6
+    n_gpus = world if world > 1 else args.gpus
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": len(times), "warmup": 1, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus,
+        "steps": len(times), "warmup": warm, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "C2 DPD: 64 streams x 256 blocks x 4096 samples, K=%d"
-                   % args.branches, "parallelism": f"{ref.cores} host processes"},
+        "config": {"workload": workload_name(args.streams, args.blocks, args.block,
+                                             args.branches),
+                   "parallelism": f"{ref.cores} host processes (rank 0 only)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.cores, "kind": ref.kind,
                          "sample": ref.sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -410,6 +455,11 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; reporting {world} ranks",
+              file=sys.stderr)
     dist = None
     # PB_BENCH_BACKEND=gloo (testing the multi-rank path with several ranks on
     # one GPU, which NCCL refuses): ranks share devices round-robin and the
@@ -678,8 +728,7 @@ def main():
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"C2 DPD: {S} streams/GPU x {blocks} blocks x {B} samples, "
-                                   f"K={K} branches, subset_policy control per block",
+            "config": {"workload": workload_name(S, blocks, B, K),
                        "fused": not args.no_fuse, "streams_per_gpu": S,
                        "fir_math": "exact (bit-exact)" if args.exact else
                        "tolerance (PB_FIR_MERGED, <= 1e-5; the exact mode is in fir_modes)",

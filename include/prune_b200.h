@@ -68,6 +68,12 @@ int pb_malloc(void** dptr, size_t bytes);
 int pb_free(void* dptr);
 int pb_host_alloc(void** hptr, size_t bytes); /* page-locked host memory */
 int pb_host_free(void* hptr);
+/* Page-lock caller-owned host memory in place (cudaHostRegister) so ring
+ * copies DMA straight from the caller's source buffers (FileSource / sources=
+ * data, behavior.py:124-140) without a staging copy.  Returns PB_OK, or 1 when
+ * the range was already registered by someone else (do not unregister it). */
+int pb_host_register(void* hptr, size_t bytes);
+int pb_host_unregister(void* hptr);
 int pb_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
 int pb_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
 int pb_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);

@@ -138,6 +138,8 @@ SIGNATURES = {
     "pb_free": (C.c_int, [vp]),
     "pb_host_alloc": (C.c_int, [C.POINTER(vp), C.c_size_t]),
     "pb_host_free": (C.c_int, [vp]),
+    "pb_host_register": (C.c_int, [vp, C.c_size_t]),
+    "pb_host_unregister": (C.c_int, [vp]),
     "pb_memcpy_h2d": (C.c_int, [vp, vp, C.c_size_t, vp]),
     "pb_memcpy_d2h": (C.c_int, [vp, vp, C.c_size_t, vp]),
     "pb_memcpy_d2d": (C.c_int, [vp, vp, C.c_size_t, vp]),

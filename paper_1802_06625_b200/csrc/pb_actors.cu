@@ -37,18 +37,19 @@ branch_sum_kernel(pb_sum_actor a, pb_resolved res, int64_t B, int tiles) {
 
 // Byte actors: out = (sum of active inputs + offset) mod 256 on every active
 // output span.  Route/passthrough (one input, offset 0) reduce to a copy;
-// merge with one live input is a copy and otherwise the bytewise sum.
+// merge with one live input is a copy and otherwise the bytewise sum.  The
+// engine admits only actors whose every input span is at least as long as
+// every output span (the reference indexes each input over the output span,
+// behavior.py:153-199), so no input is read past its span.
 __global__ void bytes_kernel(pb_bytes_actor a, pb_resolved res) {
   const int s = blockIdx.y;
   const int n = blockIdx.x;
   if (!pb::active(res, a.cond, s, n)) return;
   const uint8_t* ins[PB_MAX_PORTS];
-  int64_t len = 0;
   int n_live = 0;
   for (int p = 0; p < a.n_in; ++p) {
     if (!pb::active(res, a.in[p].act_cond, s, n)) continue;
     ins[n_live++] = pb::span_ptr(a.in[p], res, s, n);
-    len = a.in[p].span_bytes;
   }
   for (int o = 0; o < a.n_out; ++o) {
     const pb_span_ref& r = a.out[o];
@@ -56,7 +57,7 @@ __global__ void bytes_kernel(pb_bytes_actor a, pb_resolved res) {
     uint8_t* dst = pb::span_ptr(r, res, s, n);
     for (int64_t b = threadIdx.x; b < r.span_bytes; b += blockDim.x) {
       unsigned v = (unsigned)a.offset;
-      for (int p = 0; p < n_live; ++p) v += b < len ? ins[p][b] : 0u;
+      for (int p = 0; p < n_live; ++p) v += ins[p][b];
       dst[b] = (uint8_t)(v & 0xFFu);
     }
   }

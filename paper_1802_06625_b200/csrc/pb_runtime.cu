@@ -126,6 +126,28 @@ int pb_host_free(void* hptr) {
   return PB_OK;
 }
 
+int pb_host_register(void* hptr, size_t bytes) {
+  if (!hptr || !bytes) return fail(PB_E_INVALID, "pb_host_register: empty range");
+  cudaError_t e = cudaHostRegister(hptr, bytes, cudaHostRegisterPortable);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    (void)cudaGetLastError();
+    return 1;  /* already page-locked by the caller: nothing to undo later */
+  }
+  PB_CUDA(e);
+  return PB_OK;
+}
+
+int pb_host_unregister(void* hptr) {
+  if (!hptr) return PB_OK;
+  cudaError_t e = cudaHostUnregister(hptr);
+  if (e == cudaErrorHostMemoryNotRegistered) {
+    (void)cudaGetLastError();
+    return PB_OK;
+  }
+  PB_CUDA(e);
+  return PB_OK;
+}
+
 int pb_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
   if (bytes) PB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, pb::as_stream(stream)));
   return PB_OK;

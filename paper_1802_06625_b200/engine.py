@@ -20,7 +20,9 @@ actor (runtime.py:118-193):
        port order (runtime.py:175-180), optional capture
 
 FIFO channels are device rings of C = max(c_factor, epoch) chunks; a
-channel's per-epoch tokens never exceed E <= C, so occupancy stays <= beta.
+channel's per-epoch tokens never exceed E <= C (RunReport.device_slots /
+device_max_occupancy).  slots, beta and max_occupancy keep the reference's
+meaning at the caller's c_factor.
 """
 from __future__ import annotations
 
@@ -37,6 +39,7 @@ from typing import Callable, Mapping, Sequence
 import numpy as np
 
 from . import _lib
+from .admission import layout_slots
 from .behaviors import (ActorBehavior, FileSource, FireContext, actor_seed, native_policy_kind,
                         resolve)
 from .errors import ActorPanic, DeviceUnavailable, Timeout, UnsupportedGraph
@@ -79,6 +82,11 @@ class RunReport:
     eq1_checks: int = 0
     eq1_failures: int = 0
     wall_ms: float = 0.0
+    # device executor: ring capacity (tokens) and the measured peak ring
+    # occupancy per FIFO; an epoch's tokens are in flight at once, so these
+    # scale with the epoch rather than with c_factor
+    device_slots: dict[str, int] = field(default_factory=dict)
+    device_max_occupancy: dict[str, int] = field(default_factory=dict)
 
 
 class _Dev:
@@ -194,7 +202,7 @@ class DeviceRuntime:
         self.n_streams = S = int(n_streams)
         self.epoch = max(1, min(int(config.epoch), max(1, int(config.source_firings))))
         self.C = max(int(config.c_factor), self.epoch, 2)
-        self.plan = admit(self.graph, self.C)
+        self.plan = admit(self.graph, int(config.c_factor))
         self.analysis = self.plan.admission
         self.seeds = list(seeds) if seeds is not None else [config.seed] * S
         if len(self.seeds) != S:
@@ -216,6 +224,8 @@ class DeviceRuntime:
             _lib.check(lib.pb_stream_create(C.byref(st)), "pb_stream_create")
             setattr(self, name, st.value)
         self._events: list[int] = []
+        self._registered: list[int] = []      # caller buffers page-locked in place
+        self._direct: dict[str, tuple | None] = {}
 
         # device behaviours must be device kernels
         for a in g.actors:
@@ -327,6 +337,20 @@ class DeviceRuntime:
                 self.policy_state[ref] = (C.c_uint8 * (_lib.PB_POLICY_STATE_BYTES * S))()
                 for f in fifos:
                     self.counters[f.id] = m.malloc(8 * 4 * S)
+        # configuration actors: (actor, control ports, data ports); staging for
+        # the data ports' tokens
+        self.config_outputs = []
+        self.cfg_host: dict[tuple[str, str], tuple[int, np.ndarray]] = {}
+        for a in g.actors:
+            if plan.roles[a.id] != "config":
+                continue
+            ports = sorted(a.output_ports, key=lambda p: p.id)
+            ctl = [PortRef(a.id, p.id) for p in ports if p.kind == CONTROL_OUT]
+            data = [p for p in ports if p.kind != CONTROL_OUT]
+            self.config_outputs.append((a.id, ctl, data))
+            for p in data:
+                self.cfg_host[(a.id, p.id)] = m.pinned(S * self.epoch *
+                                                       self._port_span(a.id, p.id))
         # ring counters start with max occupancy = delay (0 here) — zeroed above
 
         # host staging for sources and sinks
@@ -419,7 +443,13 @@ class DeviceRuntime:
                 chunks[(lvl, block, c0)] = members[c0:c0 + _lib.PB_MAX_BRANCHES]
         fir_by_level = {(k[0], k[1], k[2]): v for k, v in chunks.items()}
 
-        for aid in plan.order:
+        # launch in level order (longest-path depth, then plan order): every
+        # data edge goes from a lower to a higher level, so a FIR group of one
+        # level is launched after all its members' producers and before all
+        # their consumers (a plain Kahn order can interleave a member's
+        # producer after another member of the same group)
+        pos = {aid: k for k, aid in enumerate(plan.order)}
+        for aid in sorted(plan.order, key=lambda x: (depth[x], pos[x])):
             if aid in done or aid in self.fused_actors:
                 continue
             a = g.actor(aid)
@@ -489,6 +519,13 @@ class DeviceRuntime:
                 f0 = g.fifo(out_f[0])
                 self.launches.append(("sum", act, f0.rate * f0.token_bytes // 8))
             elif kind == "bytes":
+                spans_in = [g.fifo(fid).rate * g.fifo(fid).token_bytes for fid in in_f]
+                spans_out = [g.fifo(fid).rate * g.fifo(fid).token_bytes for fid in out_f]
+                if spans_in and spans_out and min(spans_in) < max(spans_out):
+                    # the reference's byte actors index every input over the
+                    # output span (behavior.py:153-199) and fail on a shorter one
+                    raise UnsupportedGraph(f"{aid}: an input span ({min(spans_in)} B) is shorter "
+                                           f"than an output span ({max(spans_out)} B)")
                 act = _lib.BytesActor()
                 for k, fid in enumerate(in_f):
                     act.in_[k] = self._ref(fid)
@@ -649,6 +686,59 @@ class DeviceRuntime:
         return self.src_host[f"{actor}.{pid}"][1][:self.n_streams * self.epoch * span].reshape(
             self.n_streams, self.epoch, span)
 
+    def _port_span(self, aid: str, pid: str) -> int:
+        f = sorted(self.graph.fifos_from(PortRef(aid, pid)), key=lambda f: f.id)[0]
+        return f.rate * f.token_bytes
+
+    def _source_bytes(self, aid: str, s: int) -> np.ndarray:
+        return np.frombuffer(memoryview(self.sources[aid][s]).cast("B"), dtype=np.uint8)
+
+    def _direct_source(self, aid: str, n_iter: int) -> tuple[int, int] | None:
+        """(address of stream 0's bytes, pitch between streams) when the
+        caller's `sources=` buffers of the single-port source `aid` can feed
+        the rings by DMA in place: one C-contiguous buffer per stream holding
+        at least n_iter spans, at a uniform pitch (the rows of one [S, ...]
+        array, or a single stream).  The range is page-locked on first use
+        (pb_host_register) and stays registered until close(); the runtime
+        keeps the buffers referenced.  None -> copy through pinned staging."""
+        if aid not in self.sources or len(self.graph.actor(aid).output_ports) != 1 or \
+                (aid in self._direct and self._direct[aid] is None):
+            return None
+        span = self._port_span(aid, self.graph.actor(aid).output_ports[0].id)
+        need = n_iter * span
+        bufs = self.sources[aid]
+        ptrs = []
+        for obj in bufs:
+            if obj is None:
+                return None
+            try:
+                mv = memoryview(obj)
+            except TypeError:
+                return None
+            if not mv.c_contiguous or mv.nbytes < need:
+                return None
+            ptrs.append(np.frombuffer(mv.cast("B") if mv.format != "B" or mv.ndim != 1 else mv,
+                                      dtype=np.uint8).__array_interface__["data"][0])
+        if not ptrs:
+            return None
+        full = min(memoryview(o).nbytes for o in bufs)
+        pitch = full if len(ptrs) == 1 else ptrs[1] - ptrs[0]
+        if len(ptrs) > 1 and (pitch < full or
+                              any(q != ptrs[0] + k * pitch for k, q in enumerate(ptrs))):
+            return None
+        key = (ptrs[0], pitch, len(ptrs), full)
+        if self._direct.get(aid) != key:
+            nbytes = (len(ptrs) - 1) * pitch + full
+            rc = self.lib.pb_host_register(ptrs[0], nbytes)
+            if rc < 0:
+                _lib.error_text()       # clear; the staging path still works
+                self._direct[aid] = None
+                return None
+            if rc == 0:
+                self._registered.append(ptrs[0])
+            self._direct[aid] = key
+        return ptrs[0], pitch
+
     def stage_sources(self, it0: int, E: int, prestaged: bool = False):
         """Host sources produce E spans per stream (runtime.py:123-124 stops
         them after source_firings) and copy them into the device rings."""
@@ -670,15 +760,25 @@ class DeviceRuntime:
                 hptr, harr = self.src_host[f"{a.id}.{p.id}"]
                 buf = harr[:S * E * span].reshape(S, E, span)
                 if a.id in self.sources:
+                    direct = self._direct_source(a.id, it0 + E) if len(ports) == 1 else None
+                    if direct is not None:
+                        # DMA from the caller's page-locked buffers in place
+                        st = self.storage[f.id]
+                        self._h2d_chunks(st.data, st.stream_stride, span,
+                                         direct[0] + it0 * span, E, it0, host_pitch=direct[1])
+                        continue
+                    # FileSource order (behavior.py:132-140): per firing, the
+                    # ports in sorted order each take their span's bytes
+                    spans = [self._port_span(a.id, q.id) for q in ports]
+                    T, o = sum(spans), sum(spans[:ports.index(p)])
                     for s in range(S):
-                        data = np.frombuffer(memoryview(self.sources[a.id][s]).cast("B"),
-                                             dtype=np.uint8)
-                        lo = it0 * span * len(ports)
-                        chunk = data[lo:lo + E * span]
-                        if chunk.size < E * span:
+                        data = self._source_bytes(a.id, s)
+                        lo = it0 * T
+                        chunk = data[lo:lo + E * T]
+                        if chunk.size < E * T:
                             raise ActorPanic(a.id, EOFError(
                                 f"{a.id}: input exhausted at byte {lo + chunk.size}"))
-                        buf[s] = chunk.reshape(E, span)
+                        buf[s] = chunk.reshape(E, T)[:, o:o + span]
                 elif len(ports) == 1 and type(self.behaviors[0][a.id]) is FileSource:
                     for s in range(S):
                         b = self.behaviors[s][a.id]
@@ -719,46 +819,86 @@ class DeviceRuntime:
                 self._h2d_chunks(st.data, st.stream_stride, f.rate * f.token_bytes, hp, E, it0)
 
     def stage_control(self, it0: int, E: int):
-        """Configuration actors emit E tokens per stream (behavior.py:212-218)."""
+        """Configuration actors emit E tokens per stream (behavior.py:212-218):
+        each actor fires ONCE per iteration and its token goes to every output
+        port -- every control port (a device token array per port, aliased by
+        the port's control FIFOs) and every data port (the token padded with
+        zeros to the span, written into the port's rings)."""
         g, S = self.graph, self.n_streams
-        for ref in self.ctl_ports:
-            a = g.actor(ref.actor)
-            stride = self.ctl_stride[ref]
-            hptr, harr = self.ctl_host[ref]
-            buf = harr[:S * E * stride]
-            b0 = self.behaviors[0][a.id]
+        for aid, ctl_refs, data_ports in self.config_outputs:
+            a = g.actor(aid)
+            b0 = self.behaviors[0][aid]
             kind = native_policy_kind(b0)
-            min_tb = min(f.token_bytes for f in g.fifos_from(ref))
-            ctl_ports = [p for p in a.output_ports if p.kind == CONTROL_OUT]
-            if kind is not None and len(ctl_ports) == 1:
+            lead = ctl_refs[0]
+            stride0 = self.ctl_stride[lead]
+            tok = self.ctl_host[lead][1][:S * E * stride0].reshape(S, E, stride0)
+            min_tb = min(f.token_bytes for r in ctl_refs for f in g.fifos_from(r))
+            if kind is not None:
                 try:
                     length = int(a.params["length"])
                     param = b0.native_param(a.params)
                     if length > min_tb:
                         raise ValueError(f"{length} control elements exceed {min_tb} bytes")
                 except Exception as e:  # noqa: BLE001
-                    raise ActorPanic(a.id, e) from e
+                    raise ActorPanic(aid, e) from e
                 rc = self.lib.pb_policy_tokens_streams(
-                    C.addressof(self.policy_state[ref]), S, kind, length, param, it0, E, hptr, stride,
-                    int(self.config.host_threads))
+                    C.addressof(self.policy_state[lead]), S, kind, length, param, it0, E,
+                    self.ctl_host[lead][0], stride0, int(self.config.host_threads))
                 if rc != _lib.PB_OK:
-                    raise ActorPanic(a.id, ValueError(_lib.error_text()))
+                    raise ActorPanic(aid, ValueError(_lib.error_text()))
+                ports_out = None
             else:
+                # the plugin API: one fire per iteration with a distinct span per
+                # output port (inactive bytes beyond min_tb stay zero)
+                ports_out = {}
+                for p in a.output_ports:
+                    ref = PortRef(aid, p.id)
+                    if p.kind == CONTROL_OUT:
+                        st = self.ctl_stride[ref]
+                        ports_out[p.id] = (min(f.token_bytes for f in g.fifos_from(ref)),
+                                           self.ctl_host[ref][1][:S * E * st].reshape(S, E, st))
+                    else:
+                        sp = self._port_span(aid, p.id)
+                        ports_out[p.id] = (sp, self.cfg_host[(aid, p.id)][1][:S * E * sp]
+                                           .reshape(S, E, sp))
+                for _, arr in ports_out.values():
+                    arr[:] = 0
                 for s in range(S):
-                    b = self.behaviors[s][a.id]
-                    seed = actor_seed(self.seeds[s], a.id)
+                    b = self.behaviors[s][aid]
+                    seed = actor_seed(self.seeds[s], aid)
                     for n in range(E):
-                        off = (s * E + n) * stride
-                        span = memoryview(buf[off:off + min_tb])
-                        outs = {p.id: span for p in ctl_ports}
-                        ctx = FireContext(a.id, it0 + n, {p.id: p.rate for p in a.ports}, {},
+                        outs = {pid: memoryview(arr[s, n, :w]) for pid, (w, arr) in
+                                ports_out.items()}
+                        ctx = FireContext(aid, it0 + n, {p.id: p.rate for p in a.ports}, {},
                                           outs, a.params, seed, None)
                         try:
                             b.fire(ctx)
                         except Exception as e:  # noqa: BLE001
-                            raise ActorPanic(a.id, e) from e
-                        buf[off + min_tb:off + stride] = 0
-            self._h2d_chunks(self.ctl_dev[ref], self.C * stride, stride, hptr, E, it0)
+                            raise ActorPanic(aid, e) from e
+            if ports_out is None:
+                # native generator: the lead port's tokens, copied to the other ports
+                for ref in ctl_refs[1:]:
+                    st = self.ctl_stride[ref]
+                    arr = self.ctl_host[ref][1][:S * E * st].reshape(S, E, st)
+                    w = min(st, stride0)
+                    arr[:, :, :w] = tok[:, :, :w]
+                    arr[:, :, w:] = 0
+                for p in data_ports:
+                    sp = self._port_span(aid, p.id)
+                    arr = self.cfg_host[(aid, p.id)][1][:S * E * sp].reshape(S, E, sp)
+                    w = min(sp, stride0)
+                    arr[:, :, :w] = tok[:, :, :w]
+                    arr[:, :, w:] = 0
+            for ref in ctl_refs:
+                st = self.ctl_stride[ref]
+                self._h2d_chunks(self.ctl_dev[ref], self.C * st, st, self.ctl_host[ref][0], E,
+                                 it0)
+            for p in data_ports:
+                sp = self._port_span(aid, p.id)
+                for fid in self._port_targets(aid, p.id):
+                    st = self.storage[fid]
+                    self._h2d_chunks(st.data, st.stream_stride, sp, self.cfg_host[(aid, p.id)][0],
+                                     E, it0 + self.delay_chunks.get(fid, 0))
 
     def fire_epoch(self, it0: int, E: int, hook=None) -> int:
         """Device work of one epoch (inputs already resident); returns launches.
@@ -1116,6 +1256,13 @@ class DeviceRuntime:
                 for a, f in src:
                     span = f.rate * f.token_bytes
                     hptr, harr = self.src_host[f"{a.id}.{a.output_ports[0].id}"]
+                    direct = None if prestaged else self._direct_source(a.id, N)
+                    if direct is not None:
+                        st = self.storage[f.id]
+                        self._h2d_chunks(st.data, st.stream_stride, span,
+                                         direct[0] + it0 * span, n, it0,
+                                         host_pitch=direct[1], stream=self.copy_in)
+                        continue
                     if not prestaged:
                         buf = harr[:S * E * span].reshape(S, E, span)
                         for s in range(S):
@@ -1288,8 +1435,17 @@ class DeviceRuntime:
                 if self.captured is not None:
                     r.sink_data[aid] = bytes(self.captured[aid][s])
             for f in g.fifos:
-                r.max_occupancy[f.id] = int(ctrs[f.id][2, s])
-                r.slots[f.id] = max(f.rate * self.C, f.delay)
+                # slots / beta / max_occupancy with the reference's meaning at
+                # the caller's c_factor: the channel plan (fifos.py:87-98), the
+                # analysis bound (analysis.py:398-411) and the peak of the
+                # firing sequence the executor realises -- iteration by
+                # iteration, a producer before its consumer, so a channel holds
+                # its delay tokens plus one firing's rate once it carried data
+                r.slots[f.id] = layout_slots(f.rate, f.delay, self.config.c_factor)
+                r.max_occupancy[f.id] = f.delay + (f.rate if ctrs[f.id][0, s] > 0 else 0)
+                st = self.storage.get(f.id)
+                r.device_slots[f.id] = f.rate * (st.slots if st is not None else self.C)
+                r.device_max_occupancy[f.id] = int(ctrs[f.id][2, s])
             r.beta = dict(self.analysis.beta)
             reports.append(r)
         # Eq. 1 counters are device-wide; attribute them evenly per stream
@@ -1299,6 +1455,11 @@ class DeviceRuntime:
         return reports
 
     def close(self):
+        if getattr(self, "_registered", None):
+            self.lib.pb_device_sync()
+            for p in self._registered:
+                self.lib.pb_host_unregister(p)
+            self._registered = []
         if getattr(self, "mem", None) is not None:
             self.mem.close()
             self.mem = None

@@ -12,45 +12,36 @@ exactly one condition or by none ("always").  Propagation goes
     FIFO                    =   condition of its producer port
                             =   condition of its consumer port   (Eq. 1)
 
-A FIFO whose two ends disagree is exactly a graph whose token counts cannot
-balance per iteration (analysis.py:264-319 rejects those too), so admission
-raises InconsistentGraph.  The executor covers acyclic graphs whose dynamic
-regions are not nested, with configuration actors that have no data inputs
-and initial delay tokens only on aligned, always-active channels between
-device actors (every shipped app: the motion app's one-frame delay is such a
+Admission first runs the reference's decidability analysis (admission.py:
+the five design rules, DPG identification and validation, period schedules
+and bounds, analysis.py:414-460) and raises InconsistentGraph exactly when the
+reference does.  A graph the analysis accepts but whose FIFO ends carry
+different conditions (an always-active actor feeding a gated subchain, as in
+fixtures.encapsulated_pass) is outside the executor's class and raises
+UnsupportedGraph.  The executor covers acyclic graphs whose dynamic regions
+are not nested, with configuration actors that have no data inputs and
+initial delay tokens only on aligned, always-active channels between device
+actors (every shipped app: the motion app's one-frame delay is such a
 channel); anything else raises UnsupportedGraph rather than running
 incorrectly.
 
 Per iteration n every "always" actor fires once and every gated actor fires
 iff its condition is true at n, which is the firing sequence both reference
 engines produce (interp.py:126-148 is the oracle's version of the rule).
-Buffer bounds follow compute_bounds (analysis.py:398-411): beta = delay + r +
-(C-1)*r for a rate-r FIFO.
+Buffer bounds are the analysis' beta = delay + r + (C-1)*r for a rate-r FIFO
+at the caller's c_factor (compute_bounds, analysis.py:398-411).
 """
 from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+from . import admission
+from .admission import AnalysisReport
 from .behaviors import ActorBehavior, DeviceBehavior
-from .errors import InconsistentGraph, UnsupportedGraph
+from .errors import InconsistentGraph, InvalidParams, UnsupportedGraph
 from .graph import (CONFIG, CONTROL_IN, CONTROL_OUT, DRP, DYNAMIC, Graph, PortRef)
 
 ALWAYS = -1
-
-
-@dataclass
-class AdmissionReport:
-    """Stand-in for analysis.ConsistencyReport: verdict, problems and the
-    per-FIFO bound beta(f) for the chosen buffering factor."""
-
-    verdict: str = "consistent"
-    problems: list[str] = field(default_factory=list)
-    beta: dict[str, int] = field(default_factory=dict)
-    c_factor: int = 3
-
-    @property
-    def consistent(self) -> bool:
-        return self.verdict == "consistent"
 
 
 @dataclass(frozen=True)
@@ -80,17 +71,18 @@ class ExecPlan:
     control_fifos: list[str]
     data_fifos: list[str]
     eq1_ports: list[tuple[str, str, int, int]]   # (actor, port, own_cond, moved_cond)
-    admission: AdmissionReport
-
-
-def _problem(report: AdmissionReport, msg: str) -> None:
-    report.verdict = "inconsistent"
-    report.problems.append(msg)
+    admission: AnalysisReport
 
 
 def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
-    """Build the condition plan or raise InconsistentGraph/UnsupportedGraph."""
-    report = AdmissionReport(c_factor=c_factor)
+    """Build the condition plan or raise InconsistentGraph (the reference's
+    analysis rejects the graph) / UnsupportedGraph (consistent, but outside
+    the executor's class) / InvalidParams (c_factor < 2, fifos.py:80-81)."""
+    if c_factor < 2:
+        raise InvalidParams(f"buffering factor must be >= 2, got {c_factor}")
+    report = admission.analyze(g, c_factor)
+    if not report.consistent:
+        raise InconsistentGraph(report)
     unsupported: list[str] = []
 
     # every dynamic port needs a table entry (analysis.py:420-427)
@@ -109,14 +101,7 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
         if a.kind == DYNAMIC:
             for p in a.drps:
                 ref = PortRef(a.id, p.id)
-                try:
-                    ctl, el = g.control_lookup(ref)
-                except Exception as e:  # noqa: BLE001
-                    _problem(report, f"Uncontrolled: {e}")
-                    continue
-                port_cond[ref] = cond_of(ctl, el)
-    if not report.consistent:
-        raise InconsistentGraph(report)
+                port_cond[ref] = cond_of(*g.control_lookup(ref))
 
     roles: dict[str, str] = {}
     actor_cond: dict[str, int | None] = {}
@@ -146,18 +131,12 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
                      == CONTROL_OUT]
     data_fifos = [f.id for f in g.fifos if f.id not in set(control_fifos)]
 
-    # control channels: the two dynamic actors of a pair must see the same
-    # token (rule 2 of the paper; analysis rejects skewed delays)
-    by_ctl: dict[PortRef, set[int]] = {}
+    # control channels: rule 2 (checked by the analysis) leaves one delay per
+    # control port; initial control tokens are outside the executor's class
     for fid in control_fifos:
         f = g.fifo(fid)
-        by_ctl.setdefault(f.src, set()).add(f.delay)
-    for ctl, delays in by_ctl.items():
-        if len(delays) > 1:
-            _problem(report, f"rule 2: control tokens of {ctl} reach its dynamic actors with "
-                             f"different delays {sorted(delays)}")
-        elif delays != {0}:
-            unsupported.append(f"control channels of {ctl} carry initial delay tokens")
+        if f.delay:
+            unsupported.append(f"control channel {fid} carries initial delay tokens")
 
     # propagate conditions through static actors
     def pc(ref: PortRef) -> int | None:
@@ -190,14 +169,11 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
                 if c == ALWAYS:
                     return "always"
                 return f"{conds[c].ctl}[{conds[c].element}]"
-            nested = (roles[f.src.actor] == "dynamic" and f.src not in port_cond) or \
-                     (roles[f.dst.actor] == "dynamic" and f.dst not in port_cond)
-            msg = (f"fifo {fid}: producer {f.src} is gated by {name(cs)} but consumer "
-                   f"{f.dst} by {name(cd)}")
-            if nested and cs != ALWAYS and cd != ALWAYS:
-                unsupported.append("nested dynamic region: " + msg)
-            else:
-                _problem(report, "Eq. 1: " + msg)
+            # the analysis accepted the graph, so this is a layout the
+            # per-iteration condition schedule does not cover (a nested
+            # region, or an always-active actor feeding a gated subchain)
+            unsupported.append(f"fifo {fid}: producer {f.src} is gated by {name(cs)} but "
+                               f"consumer {f.dst} by {name(cd)}")
         fifo_cond[fid] = cs
     for fid in control_fifos:
         fifo_cond[fid] = ALWAYS
@@ -235,11 +211,7 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
         ready.sort()
     if len(order) != len(g.actors):
         stuck = sorted(a for a, d in indeg.items() if d > 0)
-        delayed = any(g.fifo(fid).delay for fid in data_fifos)
-        if delayed:
-            unsupported.append(f"cycle through {stuck} (delay tokens)")
-        else:
-            _problem(report, f"DeadlockError: zero-delay cycle through {stuck}")
+        unsupported.append(f"cycle through {stuck} (delay tokens)")
 
     # every actor must fire exactly once per source firing: a consumer whose
     # inputs all carry delay tokens would keep firing on them after the sources
@@ -255,8 +227,6 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
                                    "sources on its inputs' delay tokens (drain phase)")
                 break
 
-    if not report.consistent:
-        raise InconsistentGraph(report)
     if unsupported:
         raise UnsupportedGraph("; ".join(unsupported))
 
@@ -269,9 +239,6 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
             fid = g.fifo_into(ref).id if p.direction == "in" else g.fifos_from(ref)[0].id
             eq1.append((a.id, p.id, port_cond[ref], fifo_cond[fid]))
 
-    for fid in control_fifos + data_fifos:
-        f = g.fifo(fid)
-        report.beta[fid] = f.delay + f.rate + (c_factor - 1) * f.rate
     return ExecPlan(g, conds, {k: v for k, v in actor_cond.items()}, fifo_cond, order, roles,
                     control_fifos, data_fifos, eq1, report)
 

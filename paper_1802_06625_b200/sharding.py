@@ -6,7 +6,9 @@ a contiguous range of streams on its own GPU (one process per GPU, launched
 by torchrun).  The only exchange is the final gather of the per-stream
 reports to rank 0: captured sink bytes as uint8 tensors through the process
 group's backend (NCCL over NVLink on the GPU box), the small digest/count
-records as pickled objects.
+records as pickled objects.  `gather_sink_rings` moves the sink bytes
+straight out of the device rings (a zero-copy torch view of the ring storage,
+NCCL gather device to device), so no rank round-trips them through the host.
 """
 from __future__ import annotations
 
@@ -82,6 +84,50 @@ def gather_reports(local: Sequence[RunReport], streams: range, total: int,
                 off += ln
             out[sid] = RunReport(**rec, sink_data=sinks)
     return out  # type: ignore[return-value]
+
+
+class _DeviceBytes:
+    """__cuda_array_interface__ over library-owned device memory, so torch can
+    view a ring's storage without a copy (torch.as_tensor)."""
+
+    def __init__(self, ptr: int, shape: tuple[int, ...], strides: tuple[int, ...]):
+        self.__cuda_array_interface__ = {"shape": shape, "strides": strides, "typestr": "|u1",
+                                         "data": (int(ptr), False), "version": 3}
+
+
+def ring_view(rt, fid: str, n_iter: int):
+    """uint8 torch view [S, n_iter * span] of FIFO `fid`'s ring on the
+    runtime's device, valid for a run that started from reset (write counter
+    0) and fired n_iter <= slots iterations: chunk n of stream s is iteration
+    n (fifos.py:87-98 aligned ring, no wrap)."""
+    import torch
+    st = rt.storage[fid]
+    if n_iter > st.slots:
+        raise ValueError(f"{fid}: {n_iter} iterations wrap a ring of {st.slots} chunks")
+    cai = _DeviceBytes(st.data, (rt.n_streams, n_iter * st.span), (st.stream_stride, 1))
+    return torch.as_tensor(cai, device=torch.device("cuda", int(rt.config.device)))
+
+
+def gather_sink_rings(rt, sink: str, n_iter: int, dst: int = 0):
+    """Gather the last run's sink-channel bytes of every rank to `dst`
+    directly from the device rings (NCCL gather over NVLink; gloo falls back
+    to host tensors).  Returns the [world * S, n_iter * span] uint8 tensor
+    (stream-major, rank-contiguous) on dst, None elsewhere.  Without a process
+    group the local view is returned."""
+    from .graph import PortRef
+    a = rt.graph.actor(sink)
+    (p,) = a.input_ports
+    fid = rt.graph.fifo_into(PortRef(sink, p.id)).id
+    view = ring_view(rt, fid, n_iter)
+    dist = _dist()
+    if dist is None:
+        return view
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    t = view.contiguous() if dist.get_backend() == "nccl" else view.cpu()
+    parts = [torch.empty_like(t) for _ in range(world)] if rank == dst else None
+    dist.gather(t, parts, dst=dst)
+    return torch.cat(parts, 0) if rank == dst else None
 
 
 def run_sharded(graph, total_streams: int, config: RuntimeConfig | None = None,

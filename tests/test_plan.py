@@ -38,7 +38,8 @@ def test_eq1_mismatch_rejected():
             f["src"] = "split.d1"
         if f["id"] == "f_in1":
             f["src"] = "split.d2"
-    with pytest.raises(InconsistentGraph, match="Eq. 1"):
+    # the reference's rule 1 catches it (rules.py:162-175)
+    with pytest.raises(InconsistentGraph, match="rule 1"):
         admit(as_graph(desc))
 
 
