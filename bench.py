@@ -58,7 +58,12 @@ def parse():
     ap.add_argument("--cpu-blocks", type=int, default=256,
                     help="blocks per stream of the CPU reference sample (256: the whole C2 "
                          "workload, about 9 s of CPU work per step on 16 cores)")
+    ap.add_argument("--plumbing", action="store_true",
+                    help="launcher check only: ranks, process group, barrier and the "
+                         "max-over-ranks reduction, no device work and no measurement")
     ap.add_argument("--skip-cnn", action="store_true")
+    ap.add_argument("--skip-k10", action="store_true",
+                    help="skip the K=10 paper-scale leg (PAPER.md:658)")
     ap.add_argument("--cnn-streams", type=int, default=4, help="CNN streams per GPU")
     ap.add_argument("--cnn-firings", type=int, default=64, help="24-frame firings per stream")
     ap.add_argument("--cnn-steps", type=int, default=20)
@@ -260,6 +265,126 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def device_steps(rt, blocks, math_mode, n_steps, warmup, barrier, max_over_ranks, clocks=None):
+    """n_steps device-resident DPD steps of runtime `rt` in one FIR mode,
+    timed with CUDA events on the launching stream: (ms/step max over ranks,
+    mean bank/FIR launch ms, launches in the timed region)."""
+    import ctypes as C
+
+    from paper_1802_06625_b200 import _lib
+    lib = rt.lib
+    ms = C.c_float()
+
+    def new_event():
+        e = C.c_void_p()
+        _lib.check(lib.pb_event_create(C.byref(e)))
+        return e.value
+    rt.set_fir_math(math_mode)
+    for _ in range(max(3, warmup)):
+        rt.fire_epoch(0, blocks)
+    _lib.check(lib.pb_stream_sync(rt.stream))
+    kev = []
+
+    def hook(kind, phase):
+        if kind in ("bank", "fir"):
+            e = new_event()
+            lib.pb_event_record(e, rt.stream)
+            kev.append(e)
+    if clocks is not None:
+        time.sleep(0.3)
+    barrier()
+    _lib.check(lib.pb_stream_sync(rt.stream))
+    e0, e1 = new_event(), new_event()
+    n0 = lib.pb_launch_count()
+    t_wall0 = time.time()
+    lib.pb_event_record(e0, rt.stream)
+    for _ in range(n_steps):
+        rt.fire_epoch(0, blocks, hook=hook)
+    lib.pb_event_record(e1, rt.stream)
+    _lib.check(lib.pb_stream_sync(rt.stream))
+    if clocks is not None:
+        clocks.mark(t_wall0, time.time())
+    n_l = lib.pb_launch_count() - n0
+    barrier()
+    _lib.check(lib.pb_event_elapsed_ms(e0, e1, C.byref(ms)))
+    step = max_over_ranks(ms.value / n_steps)
+    kt = []
+    for i in range(0, len(kev) - 1, 2):
+        lib.pb_event_elapsed_ms(kev[i], kev[i + 1], C.byref(ms))
+        kt.append(ms.value)
+    for e in kev + [e0, e1]:
+        lib.pb_event_destroy(e)
+    return step, (statistics.mean(kt) if kt else float("nan")), n_l
+
+
+def k10_leg(args, rank, world, local, barrier, max_over_ranks, hbm_peak, fp32_peak):
+    """BASELINE config 2 at the paper's branch count (K = 10):
+    the same 64 streams x 256 blocks x 4096 samples per GPU, both FIR modes
+    device-resident, with the bank kernels' HBM roofline and the exact mode's
+    FP32 fraction; parity of stream 0 against the oracle in both modes."""
+    from paper_1802_06625_b200 import RuntimeConfig, _lib, run_streams
+    from paper_1802_06625_b200.apps import predistortion as pd
+    from paper_1802_06625_b200.engine import DeviceRuntime
+    S, blocks, B, K = args.streams, args.blocks, args.block, 10
+    streams = [rank * S + s for s in range(S)]
+    desc = pd.build_description(B, K)
+    rt = DeviceRuntime(desc, config=RuntimeConfig(source_firings=blocks, epoch=blocks,
+                                                  device=local),
+                       n_streams=S, seeds=[pd.stream_seed(s) for s in streams],
+                       sources={"src": [None] * S})
+    stage = rt.source_staging("src")
+    for i, s in enumerate(streams):
+        stage[i] = pd.stream_input(s, blocks, B).reshape(blocks, -1).view(np.uint8)
+    rt.reset()
+    rt.stage_sources(0, blocks, prestaged=True)
+    rt.stage_control(0, blocks)
+    _lib.check(rt.lib.pb_stream_sync(rt.stream))
+    n_steps = max(10, args.steps // 2)
+    out = {"workload": workload_name(S, blocks, B, K), "unit": UNIT}
+    counts = None
+    for name, math in (("tolerance", _lib.PB_FIR_MERGED), ("exact", _lib.PB_FIR_EXACT)):
+        step, kern, _ = device_steps(rt, blocks, math, n_steps, args.warmup, barrier,
+                                     max_over_ranks)
+        if counts is None:
+            counts = np.zeros((len(rt.plan.conds), S), dtype=np.int32)
+            rt.lib.pb_memcpy_d2h(counts.ctypes.data, rt.res_count, counts.nbytes, rt.stream)
+            rt.lib.pb_stream_sync(rt.stream)
+        alg = 16 * S * blocks * B
+        leg = {"value": S * blocks * B * world / (step / 1e3) / 1e6, "ms_per_step": step,
+               "roofline": {"bound": "hbm", "achieved": alg / (kern / 1e3) / 1e9,
+                            "peak": hbm_peak, "unit": "GB/s",
+                            "frac": alg / (kern / 1e3) / 1e9 / hbm_peak, "kernel_ms": kern,
+                            "algorithmic_bytes_per_launch": alg}}
+        if name == "exact":
+            ops = 82 * int(counts.sum()) * B
+            leg["fp32"] = {"achieved": ops / (kern / 1e3) / 1e12, "unit": "TFLOP/s",
+                           "peak": fp32_peak / 1e12, "frac": ops / (kern / 1e3) / fp32_peak,
+                           "mean_active_branches": int(counts.sum()) / (S * blocks)}
+        out[name] = leg
+    out["value"] = out["tolerance"]["value"]
+    out["roofline"] = out["tolerance"]["roofline"]
+    rt.close()
+    if rank == 0:
+        from oracle import dpd as od
+        x0 = pd.stream_input(streams[0], blocks, B)
+        sets = od.subset_schedule(pd.stream_seed(streams[0]), blocks, length=K)
+        want = od.dpd_stream(x0, sets, K)
+        par = {}
+        for name, exact in (("tolerance", False), ("exact", True)):
+            (rep0,) = run_streams(desc, 1, RuntimeConfig(source_firings=blocks, epoch=blocks,
+                                                         device=local, capture_sinks=True,
+                                                         exact=exact),
+                                  seeds=[pd.stream_seed(streams[0])],
+                                  sources={"src": [x0.tobytes()]})
+            got = np.frombuffer(rep0.sink_data["sink"], np.float32).reshape(want.shape)
+            err = float((np.abs(got.astype(np.float64) - want) /
+                         np.maximum(1.0, np.abs(want.astype(np.float64)))).max())
+            par[name] = {"bit_exact": bool(got.tobytes() == want.tobytes()), "max_rel_err": err,
+                         "firing_counts_exact": rep0.firing_counts == od.firing_counts(sets, K)}
+        out["parity_stream0"] = par
+    return out
+
+
 # ------------------------------------------------------------------ CNN leg
 
 CNN_FRAMES_PER_FIRING = 24   # PAPER.md:680 (atr = 24 frames per token)
@@ -449,6 +574,23 @@ def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
 
 # ------------------------------------------------------------------ our arm
 
+def plumbing(args, rank, world, local, dist):
+    """--plumbing: exercise the multi-rank launch path without a GPU (gloo):
+    every rank reports its (rank, local rank, pid); rank 0 prints one line.
+    Not a measurement (no metric value)."""
+    info = {"rank": rank, "local_rank": local, "pid": os.getpid()}
+    seen = [info]
+    if dist is not None:
+        seen = [None] * world
+        dist.all_gather_object(seen, info)
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        backend = os.environ.get("PB_BENCH_BACKEND", "nccl") if dist is not None else "none"
+        print(json.dumps({"plumbing": True, "n_gpus": world, "ranks": seen,
+                          "backend": backend}), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -468,12 +610,20 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        local = local % max(1, torch.cuda.device_count())
-        torch.cuda.set_device(local)
+        n_dev = torch.cuda.device_count()
+        if backend == "nccl" and n_dev < world:
+            raise SystemExit(f"bench.py: {world} ranks need {world} GPUs (one per rank, NCCL); "
+                             f"{n_dev} visible")
+        if n_dev:
+            local = local % n_dev
+            torch.cuda.set_device(local)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+    if args.plumbing:
+        plumbing(args, rank, world, local, dist)
+        return
 
     import ctypes as C
 
@@ -485,13 +635,18 @@ def main():
     streams = [rank * S + s for s in range(S)]
     cfg = RuntimeConfig(source_firings=blocks, epoch=blocks, fuse=not args.no_fuse,
                         device=local)
+    # the caller's inputs: one ordinary (pageable) numpy array [S][blocks][2][B]
+    # whose rows are the streams' sources; the runtime page-locks it in place
+    # on first use and DMAs the rings straight from it
+    X = np.empty((S, blocks, 2, B), np.float32)
+    for i, s in enumerate(streams):
+        X[i] = pd.stream_input(s, blocks, B)
     rt = DeviceRuntime(pd.build_description(B, K), config=cfg, n_streams=S,
                        seeds=[pd.stream_seed(s) for s in streams],
-                       sources={"src": [None] * S})
-    # inputs live in pinned host memory (the runtime's staging buffer)
+                       sources={"src": list(X)})
+    # the same inputs in the runtime's own pinned staging buffer (prestaged)
     stage = rt.source_staging("src")
-    for i, s in enumerate(streams):
-        stage[i] = pd.stream_input(s, blocks, B).reshape(blocks, -1).view(np.uint8)
+    stage[:] = X.reshape(S, blocks, -1).view(np.uint8)
     lib = rt.lib
 
     def barrier():
@@ -509,7 +664,11 @@ def main():
 
     # ---- device-resident measurement
     rt.reset()
-    rt.stage_sources(0, blocks, prestaged=True)
+    t_reg = time.perf_counter()
+    rt.stage_sources(0, blocks)          # first use: page-locks X in place, then DMA
+    _lib.check(lib.pb_stream_sync(rt.stream))
+    register_s = time.perf_counter() - t_reg
+    direct = rt._direct.get("src") is not None
     rt.stage_control(0, blocks)
     _lib.check(lib.pb_stream_sync(rt.stream))
     ms = C.c_float()
@@ -520,42 +679,8 @@ def main():
         return e.value
 
     def timed(math_mode, n_steps, clocks=None):
-        """n_steps device-resident steps in one FIR mode: (ms/step max over
-        ranks, mean bank/FIR launch ms on the launching stream, launches)."""
-        rt.set_fir_math(math_mode)
-        for _ in range(max(3, args.warmup)):
-            rt.fire_epoch(0, blocks)
-        _lib.check(lib.pb_stream_sync(rt.stream))
-        kev = []
-
-        def hook(kind, phase):
-            if kind in ("bank", "fir"):
-                e = new_event()
-                lib.pb_event_record(e, rt.stream)
-                kev.append(e)
-        if clocks is not None:
-            time.sleep(0.3)
-        barrier()
-        _lib.check(lib.pb_stream_sync(rt.stream))
-        e0, e1 = new_event(), new_event()
-        n0 = lib.pb_launch_count()
-        t_wall0 = time.time()
-        lib.pb_event_record(e0, rt.stream)
-        for _ in range(n_steps):
-            rt.fire_epoch(0, blocks, hook=hook)
-        lib.pb_event_record(e1, rt.stream)
-        _lib.check(lib.pb_stream_sync(rt.stream))
-        if clocks is not None:
-            clocks.mark(t_wall0, time.time())
-        n_l = lib.pb_launch_count() - n0
-        barrier()
-        _lib.check(lib.pb_event_elapsed_ms(e0, e1, C.byref(ms)))
-        step = max_over_ranks(ms.value / n_steps)
-        kt = []
-        for i in range(0, len(kev) - 1, 2):
-            lib.pb_event_elapsed_ms(kev[i], kev[i + 1], C.byref(ms))
-            kt.append(ms.value)
-        return step, (statistics.mean(kt) if kt else float("nan")), n_l
+        return device_steps(rt, blocks, math_mode, n_steps, args.warmup, barrier,
+                            max_over_ranks, clocks)
 
     fused = not args.no_fuse
     exact_math = _lib.PB_FIR_EXACT
@@ -574,18 +699,23 @@ def main():
     lib.pb_memcpy_d2h(counts.ctypes.data, rt.res_count, counts.nbytes, rt.stream)
     lib.pb_stream_sync(rt.stream)
 
-    # ---- end to end through the public runtime API (headline FIR mode)
+    # ---- end to end through the public runtime API (headline FIR mode):
+    # run_all() from the caller's array X (headline), and from the runtime's
+    # pinned staging buffer (prestaged=True)
     rt.set_fir_math(head_math)
-    e2e_times = []
-    reps = None
-    for k in range(args.e2e_steps + 1 if args.e2e_steps > 0 else 0):
-        barrier()
-        t0 = time.perf_counter()
-        reps = rt.run_all(prestaged=True)
-        t1 = time.perf_counter()
-        if k:
-            e2e_times.append(max_over_ranks(t1 - t0))
-    e2e_s = statistics.median(e2e_times) if e2e_times else float("nan")
+
+    def e2e(prestaged):
+        times, out = [], None
+        for k in range(args.e2e_steps + 1 if args.e2e_steps > 0 else 0):
+            barrier()
+            t0 = time.perf_counter()
+            out = rt.run_all(prestaged=prestaged)
+            t1 = time.perf_counter()
+            if k:
+                times.append(max_over_ranks(t1 - t0))
+        return (statistics.median(times) if times else float("nan")), out
+    e2e_pre_s, _ = e2e(True)
+    e2e_s, reps = e2e(False)
     span = 8 * B
     h2d = S * blocks * span + S * blocks * rt.ctl_stride[next(iter(rt.ctl_ports))]
     d2h = S * blocks * span + 4 * len(rt.plan.conds) * S
@@ -701,25 +831,46 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {e!r}"}
 
-    # output gather (outside the timed region): every rank's per-stream reports
-    # of the last e2e run to rank 0 through the process group -- NCCL over
-    # NVLink on a multi-GPU box -- the only exchange the sharded path has
+    # output gather (outside the timed region): the last e2e run's sink bytes
+    # of every rank straight out of the device rings to rank 0 (NCCL gather
+    # over NVLink, device to device), the only exchange the sharded path has;
+    # rank 0 checks one stream per rank against that rank's SHA-256 digest
     gather = None if dist is not None else {"streams": S, "backend": "none (one rank)"}
     if reps is not None and dist is not None:
-        from paper_1802_06625_b200.sharding import gather_reports
+        import hashlib
+
+        import torch
+
+        from paper_1802_06625_b200.sharding import gather_sink_rings
+        digests = [None] * world
+        dist.all_gather_object(digests, [r.sink_digests["sink"] for r in reps])
         barrier()
         t0 = time.perf_counter()
         try:
-            allr = gather_reports(reps, range(rank * S, rank * S + S), S * world)
-            gather = {"streams": len(allr) if allr is not None else None,
-                      "backend": dist.get_backend(), "seconds": time.perf_counter() - t0}
+            allb = gather_sink_rings(rt, "sink", blocks)
+            if backend == "nccl":
+                torch.cuda.synchronize()
+            secs = time.perf_counter() - t0
+            gather = {"backend": dist.get_backend(), "seconds": secs,
+                      "bytes": world * S * blocks * 8 * B, "from": "device rings"}
+            if rank == 0:
+                ok = all(hashlib.sha256(allb[r * S].cpu().numpy().tobytes()).hexdigest() ==
+                         digests[r][0] for r in range(world))
+                gather.update({"streams": int(allb.shape[0]),
+                               "digests_match": ok, "GB_per_s": gather["bytes"] / secs / 1e9})
         except Exception as e:  # noqa: BLE001
             gather = {"error": f"{type(e).__name__}: {e}"}
 
-    cnn = None
-    if not args.skip_cnn:
+    k10 = None
+    if not args.skip_k10:
         rt.close()
         rt = None
+        k10 = k10_leg(args, rank, world, local, barrier, max_over_ranks, hbm_peak, fp32_peak)
+    cnn = None
+    if not args.skip_cnn:
+        if rt is not None:
+            rt.close()
+            rt = None
         cnn = cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks)
 
     if rank == 0:
@@ -736,11 +887,25 @@ def main():
                        "parallelism": f"{world} GPU(s), streams sharded, no collectives"},
             "roofline": roofline(head_math, kern_ms),
             "fir_modes": modes,
+            "exact": {"value": modes["exact"]["value"], "unit": UNIT,
+                      "ms_per_step": modes["exact"]["ms_per_step"],
+                      "roofline": modes["exact"]["roofline"], "fp32": modes["exact"]["fp32"],
+                      "what": "the bit-exact FIR mode (FirBranch.fire rounding, no FMA) on "
+                              "the same workload; FP32-issue bound"},
+            "k10": k10,
             "clocks": clk,
             "e2e": {"value": samples / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s,
-                    "includes": "H2D pinned inputs, native control actors, device firings, "
-                                "sink D2H, SHA-256 per stream"},
+                    "includes": "DeviceRuntime.run_all() with sources = rows of the caller's "
+                                "numpy array (page-locked in place on first use, DMA straight "
+                                "into the rings), native control actors, device firings, sink "
+                                "D2H, SHA-256 per stream",
+                    "caller_buffers_registered": direct,
+                    "register_seconds_once": register_s,
+                    "prestaged": {"value": samples / e2e_pre_s / 1e6, "unit": UNIT,
+                                  "seconds_per_step": e2e_pre_s,
+                                  "what": "run_all(prestaged=True): inputs already in the "
+                                          "runtime's pinned staging buffer"}},
             "gpu_launches": launches,
             "parity_stream0": parity,
             "output_gather": gather,

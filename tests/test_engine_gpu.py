@@ -5,7 +5,8 @@ import numpy as np
 import pytest
 
 from paper_1802_06625_b200 import (ActorBehavior, ActorPanic, EndOfStream, InvalidParams,
-                                   ProtocolError, RuntimeConfig, UnsupportedGraph, run)
+                                   ProtocolError, RuntimeConfig, UnsupportedGraph, run,
+                                   run_streams)
 from paper_1802_06625_b200 import _lib
 
 pytestmark = pytest.mark.gpu
