@@ -1406,6 +1406,11 @@ int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream) {
   int& sms = sms_d[dev];
   if (sms == 0) PB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   cudaStream_t st = pb::as_stream(stream);
+  // default: the row-streaming kernel with A in TMEM (pb_conv_rows.cu);
+  // PB_CONV_IMPL=tiles selects the round-1 tile kernel below
+  const char* impl = getenv("PB_CONV_IMPL");
+  if ((actor.cin == 3 || actor.cin == 32) && !(impl && impl[0] == 't'))
+    return pb::fire_conv_rows(actor, res, st, sms);
   switch (actor.cin) {
     case 3: return launch_conv<0, 3>(actor, res, st, sms);
     case 16: return launch_conv<1, 16>(actor, res, st, sms);

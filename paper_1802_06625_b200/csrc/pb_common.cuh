@@ -24,12 +24,15 @@ void count_launch(int n = 1);
 constexpr int kMaxDevices = 16;
 int device();   // current device ordinal, < kMaxDevices, or -1 on error (pb_last_error set)
 enum ScratchSlot { kScratchBankPlan = 0, kScratchConvUnits, kScratchDensePartial,
-                   kScratchDenseCounters, kScratchSlots };
+                   kScratchDenseCounters, kScratchConvRows, kScratchSlots };
 // at least `bytes` of device memory for `slot` on the current device; newly
 // allocated memory is zeroed on `st` when zero_new
 int scratch(int slot, size_t bytes, void** out, bool zero_new = false, cudaStream_t st = 0);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// the row-streaming conv kernel with A in TMEM (pb_conv_rows.cu); Cin 3 / 32
+int fire_conv_rows(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t st, int sms);
 
 }  // namespace pb
 
