@@ -513,7 +513,7 @@ def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
     try:   # per-launch DRAM bytes of the two conv kernels (same 6144-frame launch, ncu)
         tr = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
         if frames == 6144:
-            conv_traffic = tr["conv_pool_kernel<0, 3>"] + tr["conv_pool_kernel<1, 32>"]
+            conv_traffic = tr["conv_rows_kernel<3>"] + tr["conv_rows_kernel<32>"]
     except Exception:  # noqa: BLE001
         conv_traffic = None
     achieved = frames * conv_flops / (conv_ms / 1e3) / 1e12 if conv_ms else None
@@ -547,15 +547,15 @@ def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
         "kernel_ms": kern,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if achieved else None, "traffic": conv_traffic,
-                     "kernel": "conv_pool_kernel (layers 1+2)", "kernel_ms": conv_ms,
+                     "kernel": "conv_rows_kernel (layers 1+2)", "kernel_ms": conv_ms,
                      "algorithmic_flops_per_frame": conv_flops, "peak_source": peak_src,
                      "issued_tflops": 3 * achieved if achieved else None,
                      "issued_frac": 3 * achieved / peak if achieved else None,
                      "note": "useful FLOPs; bf16x3 issues 3 MMA products per useful one "
-                             "(issued_*: the tensor pipe's bf16 work); N=32/64 MMAs are "
-                             "shared-memory-read bound (tools/conv_probe); layer 2 runs on CTA "
-                             "pairs (cta_group::2, half the B reads per SM); traffic: DRAM "
-                             "bytes of both conv launches from profiles/ncu_traffic.json"},
+                             "(issued_*: the tensor pipe's bf16 work); both layers stream "
+                             "input rows through N=32 MMAs whose A operand is in tensor memory "
+                             "(pb_conv_rows.cu); traffic: DRAM bytes of both conv launches "
+                             "from profiles/ncu_traffic.json"},
         "e2e": {"value": frames * world / e2e_s, "unit": "frames/s",
                 "h2d_bytes_per_step": frames * vision.FRAME_BYTES,
                 "d2h_bytes_per_step": frames * vision.N_CLASSES * 4,

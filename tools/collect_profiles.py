@@ -58,9 +58,9 @@ if m and p:
 e = last("fir_persistent<1, 0>")
 if e:
     traffic["fir_persistent<bank, EXACT>"] = e["dram_read"] + e["dram_write"]
-# (layer 2 runs as conv_pool_kernel<1, 32, true> on CTA pairs; same key)
-for nm, pat in (("conv_pool_kernel<0, 3>", "conv_pool_kernel<0, 3"),
-                ("conv_pool_kernel<1, 32>", "conv_pool_kernel<1, 32"), ("dense_kernel", "dense_kernel")):
+# both conv layers run as the row-streaming kernel (pb_conv_rows.cu)
+for nm, pat in (("conv_rows_kernel<3>", "conv_rows_kernel<3>"),
+                ("conv_rows_kernel<32>", "conv_rows_kernel<32>"), ("dense_kernel", "dense_kernel")):
     x = last(pat)
     if x:
         traffic[nm] = x["dram_read"] + x["dram_write"]

@@ -15,8 +15,8 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:bank
   -o gpurun_out/${R}_merged $B --skip-cnn > /dev/null 2>&1; echo "merged: $?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fir_persistent -c 1 \
   -o gpurun_out/${R}_exact python bench.py --steps 2 --warmup 3 --skip-cpu --e2e-steps 0 --skip-cnn --exact > /dev/null 2>&1; echo "exact: $?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"conv_pool|dense_kernel" -c 3 \
-  -o gpurun_out/${R}_cnn python tools/cnn_bench.py 2 32 24 1 > /dev/null 2>&1; echo "cnn: $?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"conv_rows_kernel|dense_kernel" -c 3 \
+  -o gpurun_out/${R}_cnn python tools/cnn_bench.py 4 64 24 1 > /dev/null 2>&1; echo "cnn: $?"
 for r in merged exact cnn; do
   python tools/ncu_summary.py gpurun_out/${R}_$r.ncu-rep > gpurun_out/${R}_ncu_$r.json 2>/dev/null
 done
