@@ -1409,8 +1409,10 @@ int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream) {
   // default: the row-streaming kernel with A in TMEM (pb_conv_rows.cu);
   // PB_CONV_IMPL=tiles selects the round-1 tile kernel below
   const char* impl = getenv("PB_CONV_IMPL");
-  if ((actor.cin == 3 || actor.cin == 32) && !(impl && impl[0] == 't'))
-    return pb::fire_conv_rows(actor, res, st, sms);
+  if ((actor.cin == 3 || actor.cin == 32) && !(impl && impl[0] == 't')) {
+    const int rc = pb::fire_conv_rows(actor, res, st, sms);
+    if (rc != 1) return rc;   // 1: shape declined by the row kernel, use the tile kernel
+  }
   switch (actor.cin) {
     case 3: return launch_conv<0, 3>(actor, res, st, sms);
     case 16: return launch_conv<1, 16>(actor, res, st, sms);

@@ -31,7 +31,8 @@ int scratch(int slot, size_t bytes, void** out, bool zero_new = false, cudaStrea
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// the row-streaming conv kernel with A in TMEM (pb_conv_rows.cu); Cin 3 / 32
+// the row-streaming conv kernel with A in TMEM (pb_conv_rows.cu); Cin 3 / 32;
+// returns 1 without launching when it does not handle the shape
 int fire_conv_rows(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t st, int sms);
 
 }  // namespace pb

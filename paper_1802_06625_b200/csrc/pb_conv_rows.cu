@@ -56,11 +56,12 @@
 namespace {
 
 constexpr int kMaxPairSlots = 8;
+constexpr int kMaxPairsPerTile = 256;
+constexpr int kMaxStepsPerTile = 512;
 constexpr int kPairCols = 64;                    // accumulator columns of a pair of rows
 constexpr int kCoutR = 32;
-constexpr int kEpiGroups = 1;                   // epilogue groups of 4 warps (alternate pairs)
-constexpr int kCvtWarp0 = 1 + 4 * kEpiGroups;
 constexpr int kUnitsThreads = 1024;
+constexpr int kDeclined = 1;   // fire_conv_rows: shape not handled here (nothing launched)
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -172,18 +173,51 @@ struct RowCfg {
   static constexpr int STEP_COLS = STEP_CHUNKS * 16;       // hi 8 + lo 8 columns per chunk
   // TMEM: PAIRS accumulator slots, then a ring of RING A steps.  Layer 1
   // (a step feeds 4 pairs) keeps two pairs of slack for the epilogue.
-  static constexpr int PAIRS = CIN == 3 ? 6 : 4;
+#ifndef PB_ROWS_PAIRS1
+#define PB_ROWS_PAIRS1 6
+#endif
+  static constexpr int PAIRS = CIN == 3 ? PB_ROWS_PAIRS1 : 4;
   static constexpr int A0 = PAIRS * kPairCols;             // first A-ring column
   static constexpr int RING = (512 - A0) / STEP_COLS;     // A steps in flight
   static constexpr int GROUPS = 2;                         // converter groups of 4 warps
-  static constexpr int THREADS = (kCvtWarp0 + 4 * GROUPS) * 32;
   // layer 2: each converter warp stages its lanes' row-half pixels in shared
   // memory (coalesced loads; 80-byte pixel pitch makes the per-lane 16-byte
   // reads conflict-free): up to 32 + 2 x 4 pixels, double-buffered
   static constexpr int STAGE_PIX = 40, STAGE_PITCH = 80;
   static constexpr int STAGE_BYTES = CIN == 3 ? 0 : 2 * STAGE_PIX * STAGE_PITCH * 4 * GROUPS;
+  // layer 1: a loader warp (the last) streams each step's raw input rows into
+  // a shared-memory ring by bulk copies; the converters split from there
+  static constexpr int LOADER = CIN == 3 ? 1 : 0;
+  static constexpr int RAW = 4;                            // raw steps in flight
+  // epilogue groups of 4 warps taking alternate pairs: layer 1 has 2.2 pairs
+  // per step to drain (its epilogue chain per pair is latency-bound)
+#ifndef PB_ROWS_EPI1
+#define PB_ROWS_EPI1 1
+#endif
+  static constexpr int EPI = CIN == 3 ? PB_ROWS_EPI1 : 1;
+  static constexpr int CVT0 = 1 + 4 * EPI;                 // first converter warp
+  static constexpr int THREADS = (CVT0 + 4 * GROUPS + LOADER) * 32;
   static_assert(RING >= 2, "TMEM budget");
 };
+
+// Layer-1 raw ring geometry: a step's STEP_ROWS input rows, each as up to
+// `segs` frame segments (the frames a 128-column tile touches); a segment is
+// one frame row with zero margins (lm pixels left -- the padding rounded up
+// so the bulk copy's destination is 16-byte aligned -- and >= pad right), so
+// the converters read every entry without bounds checks.
+struct RawGeom {
+  int lm, seg_px, segs;
+  int64_t seg_bytes, slot_bytes;
+};
+__host__ __device__ inline RawGeom raw_geom(int w, int pad, int wo, int rows) {
+  RawGeom r;
+  r.lm = (pad + 3) & ~3;
+  r.seg_px = (r.lm + w + pad + 3) & ~3;
+  r.segs = (127 + wo - 1) / wo + 1;
+  r.seg_bytes = (int64_t)r.seg_px * 12;
+  r.slot_bytes = r.seg_bytes * r.segs * rows;
+  return r;
+}
 
 // One live firing of the launch: its input and output spans.
 struct LiveSpan {
@@ -221,6 +255,18 @@ conv_rows_units_kernel(pb_conv_actor a, pb_resolved res, LiveSpan* list, int* n_
 
 struct RowBars {
   uint64_t a_full[8], a_empty[8], acc_full[kMaxPairSlots], acc_empty[kMaxPairSlots], w_full;
+  uint64_t raw_full[8], raw_empty[8];
+  // commit batches: every pair completed by the same input step is signalled
+  // by ONE tcgen05.commit (the MMA warp feeds the tensor pipe and every
+  // instruction it spends elsewhere is a bubble); batch_of[p] = the batch of
+  // pair p within a tile, n_batches per tile (same for every tile)
+  uint8_t batch_of[kMaxPairsPerTile];
+  int n_batches;
+  // per input step of a tile: bits 0-14 the last pair to acquire before its
+  // MMAs, bit 15 set if a commit batch follows it; pre_sig = pairs committed
+  // before the first step (above the first input row)
+  uint16_t step_info[kMaxStepsPerTile];
+  int pre_sig;
   uint32_t tmem_base;
   float bias[kCoutR];
 };
@@ -311,16 +357,53 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
       bar_init(&B.acc_empty[i], 4);
     }
     bar_init(&B.w_full, 1);
+    for (int i = 0; i < Cfg::RAW; ++i) {
+      bar_init(&B.raw_full[i], 1);
+      bar_init(&B.raw_empty[i], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (threadIdx.x < kCoutR) B.bias[threadIdx.x] = a.bias[threadIdx.x];
+  if (threadIdx.x == 32) {
+    // the MMA warp's commit points: before the first row, after every step
+    // (layer 2: every row), after the last row
+    int sig = 0, nb = 0;
+    auto batch = [&](int rp_done) {
+      bool any = false;
+      for (; sig < n_pairs && min(2 * sig + 5, g.pad + g.H - 1) <= rp_done; ++sig) {
+        B.batch_of[sig] = (uint8_t)nb;
+        any = true;
+      }
+      nb += any;
+      return any;
+    };
+    batch(g.pad - 1);
+    B.pre_sig = sig;
+    for (int st = 0; st < n_steps; ++st) {
+      const int rp_hi = step_row<CIN>(st, Cfg::STEP_ROWS - 1) + g.pad;
+      const bool cm = (CIN == 3 || (st & 1)) && batch(rp_hi);
+      const int acq = max(min(rp_hi, g.Ho - 1) >> 1, sig - 1);
+      B.step_info[st] = (uint16_t)(acq | (cm ? 0x8000 : 0));
+    }
+    batch(1 << 30);
+    B.n_batches = nb;
+  }
+  uint8_t* raw = smem + Cfg::WBYTES + ((sizeof(RowBars) + 127) & ~size_t(127));
+  const RawGeom rg = raw_geom(g.W, g.pad, g.Wo, Cfg::STEP_ROWS);
+  if constexpr (CIN == 3) {
+    // zero margins: the bulk copies only ever write segment interiors
+    const int64_t n16 = rg.slot_bytes * Cfg::RAW / 16;
+    for (int64_t i = threadIdx.x; i < n16; i += blockDim.x)
+      reinterpret_cast<float4*>(raw)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = B.tmem_base;
   const bool prof = (a.debug & 16) && blockIdx.x == 0;
   const long long t_begin = clock64();
-  WaitClock w1{prof, 0, 0}, w2{prof, 0, 0}, w3{prof, 0, 0};
+  WaitClock w1{prof, 0, 0}, w2{prof, 0, 0}, w3{prof, 0, 0}, w4{prof, 0, 0};
   const int y_last = g.pad + g.H - 1;                      // last padded input row with data
   // output row o has data iff some input row feeds it; pair p is complete
   // once the last input row feeding row 2p + 1 is in
@@ -345,10 +428,12 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
     const bool run_mma = !(a.debug & 4);
     uint32_t c = 0;           // step counter (A ring)
     uint32_t pbase = 0;       // pair counter of this tile's pair 0
+    uint32_t kbase = 0;       // commit batch counter (acc_full[k % slots])
     // Pair q owns accumulator slot q % 4.  Pairs are ACQUIRED in order (wait
     // until the epilogue drained pair q - 4 of the slot) and COMMITTED in order
     // (acc_full once complete), never committed before acquired: no mbarrier
     // phase of a slot runs more than one ahead of the epilogue.
+    const int pre_sig = B.pre_sig;
     for (int t = blockIdx.x; t < g.tiles; t += gridDim.x, pbase += n_pairs) {
       int acq = 0, sig = 0;   // next pair to acquire / to commit
       auto acquire_to = [&](int p_last) {
@@ -359,17 +444,23 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
           w1.stop();
         }
       };
-      auto commit_to = [&](int rp_done) {   // every pair complete once rp_done is in
-        for (; sig < n_pairs && pair_done_after(sig) <= rp_done; ++sig) {
-          acquire_to(sig);
-          if (elect_one()) commit(&B.acc_full[(pbase + sig) % kPairSlots]);
-          __syncwarp();
-        }
+      // pairs with no input rows above / below the frame: one batch each
+      auto commit_rest = [&](int upto) {
+        if (upto <= sig) return;
+        acquire_to(upto - 1);
+        if (elect_one()) commit(&B.acc_full[kbase % kPairSlots]);
+        __syncwarp();
+        ++kbase;
+        sig = upto;
       };
-      commit_to(g.pad - 1);   // pairs above the first input row get no data
+      commit_rest(pre_sig);
+      uint32_t info = B.step_info[0];
       for (int st = 0; st < n_steps; ++st, ++c) {
         const int rp_hi = step_row<CIN>(st, Cfg::STEP_ROWS - 1) + g.pad;
-        acquire_to(min(rp_hi, g.Ho - 1) >> 1);   // pairs first written by this step
+        const bool batch_after = info & 0x8000;
+        acquire_to((int)(info & 0x7FFF));   // pairs this step writes or completes
+        const uint32_t next_info = B.step_info[min(st + 1, n_steps - 1)];
+        const uint32_t kb = kbase % kPairSlots;
         const uint32_t slot = c % RING;
         w2.start();
         bar_wait(&B.a_full[slot], (c / RING) & 1);
@@ -425,6 +516,7 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
               }
             }
             commit(&B.a_empty[slot]);
+            if (batch_after) commit(&B.acc_full[kb]);
           }
         } else if (elect_one()) {
 #pragma unroll
@@ -447,15 +539,20 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
             }
           }
           commit(&B.a_empty[slot]);
+          if (batch_after) commit(&B.acc_full[kb]);
         }
         __syncwarp();
         w3.stop();
-        // pairs complete after this step (its last input row is in)
-        if (CIN == 3 || (st & 1)) commit_to(rp_hi);
+        // the batch of pairs this step completed (its last input row is in)
+        if (batch_after) {
+          ++kbase;
+          while (sig < n_pairs && pair_done_after(sig) <= rp_hi) ++sig;
+        }
+        info = next_info;
       }
-      commit_to(1 << 30);     // pairs below the last input row
+      commit_rest(n_pairs);   // pairs below the last input row
     }
-  } else if (warp < kCvtWarp0) {
+  } else if (warp < Cfg::CVT0) {
     // ------------------------------------------------------------- epilogue
     // group e drains pairs e, e + 2, ... (each pair's 4 warps cover the lanes)
     const int egroup = (warp - 1) >> 2;
@@ -466,17 +563,20 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
     float bias[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) bias[i] = B.bias[(odd ? 16 : 0) + i];
-    uint32_t pbase = 0;
-    for (int t = blockIdx.x; t < g.tiles; t += gridDim.x, pbase += n_pairs) {
+    uint32_t pbase = 0, tnum = 0;
+    for (int t = blockIdx.x; t < g.tiles; t += gridDim.x, pbase += n_pairs, ++tnum) {
       const LaneFrame f = lane_frame(g, list, t, m);
       for (int pr = 0; pr < n_pairs; ++pr) {
         const uint32_t q = pbase + pr;
-        if ((int)(q % kEpiGroups) != egroup) continue;
+        if ((int)(q % Cfg::EPI) != egroup) continue;
         const uint32_t sl = q % kPairSlots;
         const bool h0 = has_data(2 * pr), h1 = has_data(2 * pr + 1);
         w2.start();
         w1.start();
-        bar_wait(&B.acc_full[sl], (q / kPairSlots) & 1);
+        {
+          const uint32_t k = tnum * (uint32_t)B.n_batches + B.batch_of[pr];
+          bar_wait(&B.acc_full[k % kPairSlots], (k / kPairSlots) & 1);
+        }
         w1.stop();
         asm volatile("tcgen05.fence::after_thread_sync;");
         float r0[32], r1[32];
@@ -517,6 +617,39 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
         }
       }
     }
+  } else if (Cfg::LOADER && warp == Cfg::CVT0 + 4 * Cfg::GROUPS) {
+    // ------------------------------------------------- layer-1 row loader
+    // step c: rows 4s .. 4s+3 of every frame the tile touches, one bulk copy
+    // per (row, frame) issued by one lane each, into raw slot c % RAW
+    uint32_t c = 0;
+    const uint32_t row_bytes = (uint32_t)g.W * 12;
+    for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      const int64_t v0 = (int64_t)t * 128;
+      const int fr0 = (int)(v0 / g.Wo);
+      const int fr1 = min((int)((v0 + 127) / g.Wo), g.frames - 1);
+      const int nseg = fr1 - fr0 + 1;
+      const float* fin = nullptr;     // lane's frame (segment lane % segs)
+      const int j = lane % rg.segs, i = lane / rg.segs;
+      if (j < nseg) {
+        const int fr = fr0 + j, u = fr / g.R;
+        fin = list[u].in + (fr - u * g.R) * g.in_frame;
+      }
+      const bool mine = j < nseg && i < Cfg::STEP_ROWS && !(a.debug & 1);
+      for (int st = 0; st < n_steps; ++st, ++c) {
+        const uint32_t rslot = c % Cfg::RAW;
+        bar_wait(&B.raw_empty[rslot], ((c / Cfg::RAW) & 1) ^ 1);
+        if (lane == 0)
+          bar_expect_tx(&B.raw_full[rslot],
+                        (a.debug & 1) ? 0u : row_bytes * nseg * Cfg::STEP_ROWS);
+        __syncwarp();
+        if (mine) {
+          const int y = step_row<CIN>(st, i);
+          bulk_load(raw + rslot * rg.slot_bytes + (i * rg.segs + j) * rg.seg_bytes + rg.lm * 12,
+                    fin + (int64_t)y * g.W * 3, row_bytes, &B.raw_full[rslot]);
+        }
+        __syncwarp();
+      }
+    }
   } else {
     // ----------------------------------------------------------- converters
     // This group's steps s = group, group + 2, ... of the row stream; within
@@ -527,7 +660,7 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
     const int quarter = warp & 3;
     const int m = quarter * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16) + kA0;
-    const int group = (warp - kCvtWarp0) >> 2;
+    const int group = (warp - Cfg::CVT0) >> 2;
     auto load = [&](const LaneFrame& lf, int yy, int k, float (&v)[16]) {
       const float* row = lf.in + (int64_t)yy * g.W * CIN;
       if constexpr (CIN == 3) {
@@ -558,36 +691,42 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
       }
     };
     if constexpr (CIN == 3) {
+      // entry of lane m at chunk (row) i: 15 consecutive floats of its frame's
+      // segment, x = xo - pad .. xo - pad + 4 (margins are zero)
       uint32_t c = 0;
       for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
         const LaneFrame f = lane_frame(g, list, t, m);
+        const int fr0 = (int)((int64_t)t * 128 / g.Wo);
+        const int64_t v = (int64_t)t * 128 + m;
+        const int seg = (int)(v / g.Wo) - fr0;
+        const int64_t lane_off =
+            f.valid ? seg * rg.seg_bytes + (int64_t)(rg.lm - g.pad + f.xo) * 12 : 0;
         for (int st = 0; st < n_steps; ++st, ++c) {
           if ((int)(c % Cfg::GROUPS) != group) continue;
           const uint32_t slot = c % RING;
-          float cur[16], nxt[16];
-          load(f, step_row<CIN>(st, 0), step_wk<CIN>(st, 0), cur);
-          const int y1 = step_row<CIN>(st, Cfg::STEP_ROWS - 1) + 1;
-          if (y1 < g.H && f.valid) {
-            const int xp = min(max(f.xo - g.pad, 0), g.W - 1);
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(f.in + ((int64_t)y1 * g.W + xp) * CIN));
-          }
+          const uint32_t rslot = c % Cfg::RAW;
           w1.start();
+          bar_wait(&B.raw_full[rslot], (c / Cfg::RAW) & 1);
           bar_wait(&B.a_empty[slot], ((c / RING) & 1) ^ 1);
           w1.stop();
           asm volatile("tcgen05.fence::after_thread_sync;");
+          const float* src = reinterpret_cast<const float*>(raw + rslot * rg.slot_bytes + lane_off);
 #pragma unroll
           for (int i = 0; i < Cfg::STEP_CHUNKS; ++i) {
-            if (i + 1 < Cfg::STEP_CHUNKS)
-              load(f, step_row<CIN>(st, i + 1), step_wk<CIN>(st, i + 1), nxt);
+            float e[16];
+            const float* r = src + i * rg.segs * rg.seg_bytes / 4;
+#pragma unroll
+            for (int k = 0; k < 15; ++k) e[k] = (f.valid && !(a.debug & 1)) ? r[k] : 0.f;
+            e[15] = 0.f;
             uint32_t hi[8], lo[8];
-            split16(cur, hi, lo);
+            split16(e, hi, lo);
             if (!(a.debug & 8)) {
               tmem_st8(tl + slot * Cfg::STEP_COLS + i * 16, hi);
               tmem_st8(tl + slot * Cfg::STEP_COLS + i * 16 + 8, lo);
             }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) cur[j] = nxt[j];
           }
+          __syncwarp();
+          if (lane == 0) bar_arrive(&B.raw_empty[rslot]);
           w2.start();
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           asm volatile("tcgen05.fence::before_thread_sync;");
@@ -606,7 +745,7 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
       // every chunk dx reads lane-private 16-byte pieces from there.
       const int h = group;
       uint8_t* stage = smem + Cfg::WBYTES + ((sizeof(RowBars) + 127) & ~size_t(127)) +
-                       (size_t)(warp - kCvtWarp0) * 2 * Cfg::STAGE_PIX * Cfg::STAGE_PITCH;
+                       (size_t)(warp - Cfg::CVT0) * 2 * Cfg::STAGE_PIX * Cfg::STAGE_PITCH;
       struct Seg {   // this warp's lanes in one tile
         const float* in1;
         const float* in2;
@@ -720,9 +859,9 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
     }
   }
 
-  if (prof && lane == 0 && (warp == 0 || warp == 1 || warp == 5 || warp == kCvtWarp0 || warp == kCvtWarp0 + 4))
-    printf("{\"conv_rows_prof\": %d, \"warp\": %d, \"total\": %lld, \"wait1\": %lld, \"wait2\": %lld, \"w3\": %lld}\n",
-           CIN, warp, clock64() - t_begin, w1.acc, w2.acc, w3.acc);
+  if (prof && lane == 0 && (warp == 0 || warp == 1 || warp == Cfg::CVT0 || warp == Cfg::CVT0 + 4))
+    printf("{\"conv_rows_prof\": %d, \"warp\": %d, \"total\": %lld, \"wait1\": %lld, \"wait2\": %lld, \"w3\": %lld, \"w4\": %lld}\n",
+           CIN, warp, clock64() - t_begin, w1.acc, w2.acc, w3.acc, w4.acc);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0)
@@ -733,15 +872,23 @@ template <int CIN>
 int launch_rows(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t st, int sms) {
   using Cfg = RowCfg<CIN>;
   // one CTA per SM: the kernel allocates all 512 TMEM columns
-  const size_t smem =
-      std::max<size_t>(1024 + Cfg::WBYTES + sizeof(RowBars) + 128 + Cfg::STAGE_BYTES, 120 * 1024);
+  const int Wo_ = actor.w + 2 * actor.pad - 4, Ho_ = actor.h + 2 * actor.pad - 4;
+  const RawGeom rg = raw_geom(actor.w, actor.pad, Wo_, Cfg::STEP_ROWS);
+  const size_t raw_bytes = CIN == 3 ? (size_t)rg.slot_bytes * Cfg::RAW : 0;
+  const int steps_ = CIN == 3 ? actor.h / 4 : 2 * actor.h;
+  if (Ho_ / 2 > kMaxPairsPerTile || steps_ > kMaxStepsPerTile || (CIN == 3 && (actor.w % 4 || rg.segs * Cfg::STEP_ROWS > 32)))
+    return kDeclined;   // not for this kernel: the caller uses the tile kernel
+  const size_t smem = std::max<size_t>(
+      1024 + Cfg::WBYTES + ((sizeof(RowBars) + 127) & ~size_t(127)) + Cfg::STAGE_BYTES + raw_bytes,
+      120 * 1024);
+  if (smem > 227 * 1024) return kDeclined;
   const int dev = pb::device();
   if (dev < 0) return PB_E_CUDA;
-  static bool configured[pb::kMaxDevices] = {};
-  if (!configured[dev]) {
+  static size_t configured[pb::kMaxDevices] = {};
+  if (configured[dev] < smem) {
     PB_CUDA(cudaFuncSetAttribute(conv_rows_kernel<CIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    configured[dev] = true;
+    configured[dev] = smem;
   }
   if (res.n_streams > kUnitsThreads)
     return pb::fail(PB_E_UNSUPPORTED, "conv: more than 1024 streams per launch");
