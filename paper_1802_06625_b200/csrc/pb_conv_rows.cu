@@ -179,7 +179,10 @@ struct RowCfg {
   static constexpr int PAIRS = CIN == 3 ? PB_ROWS_PAIRS1 : 4;
   static constexpr int A0 = PAIRS * kPairCols;             // first A-ring column
   static constexpr int RING = (512 - A0) / STEP_COLS;     // A steps in flight
-  static constexpr int GROUPS = 2;                         // converter groups of 4 warps
+#ifndef PB_ROWS_GROUPS1
+#define PB_ROWS_GROUPS1 2
+#endif
+  static constexpr int GROUPS = CIN == 3 ? PB_ROWS_GROUPS1 : 2;   // converter groups of 4 warps
   // layer 2: each converter warp stages its lanes' row-half pixels in shared
   // memory (coalesced loads; 80-byte pixel pitch makes the per-lane 16-byte
   // reads conflict-free): up to 32 + 2 x 4 pixels, double-buffered
@@ -711,15 +714,18 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
           w1.stop();
           asm volatile("tcgen05.fence::after_thread_sync;");
           const float* src = reinterpret_cast<const float*>(raw + rslot * rg.slot_bytes + lane_off);
+          float ev[Cfg::STEP_CHUNKS][16];
 #pragma unroll
           for (int i = 0; i < Cfg::STEP_CHUNKS; ++i) {
-            float e[16];
             const float* r = src + i * rg.segs * rg.seg_bytes / 4;
 #pragma unroll
-            for (int k = 0; k < 15; ++k) e[k] = (f.valid && !(a.debug & 1)) ? r[k] : 0.f;
-            e[15] = 0.f;
+            for (int k = 0; k < 15; ++k) ev[i][k] = (f.valid && !(a.debug & 1)) ? r[k] : 0.f;
+            ev[i][15] = 0.f;
+          }
+#pragma unroll
+          for (int i = 0; i < Cfg::STEP_CHUNKS; ++i) {
             uint32_t hi[8], lo[8];
-            split16(e, hi, lo);
+            split16(ev[i], hi, lo);
             if (!(a.debug & 8)) {
               tmem_st8(tl + slot * Cfg::STEP_COLS + i * 16, hi);
               tmem_st8(tl + slot * Cfg::STEP_COLS + i * 16 + 8, lo);
