@@ -40,10 +40,10 @@ import numpy as np
 
 from . import _lib
 from .admission import layout_slots
-from .behaviors import (ActorBehavior, FileSource, FireContext, actor_seed, native_policy_kind,
-                        resolve)
+from .behaviors import (ActorBehavior, DeviceBehavior, FileSource, FireContext, actor_seed,
+                        decode_control, native_policy_kind, resolve)
 from .errors import ActorPanic, DeviceUnavailable, Timeout, UnsupportedGraph
-from .graph import CONTROL_OUT, DRP, Graph, PortRef, as_graph
+from .graph import CONTROL_IN, CONTROL_OUT, DRP, Graph, PortRef, as_graph
 from .plan import ALWAYS, ExecPlan, admit, find_filter_banks, is_device
 
 
@@ -227,14 +227,26 @@ class DeviceRuntime:
         self._registered: list[int] = []      # caller buffers page-locked in place
         self._direct: dict[str, tuple | None] = {}
 
-        # device behaviours must be device kernels
+        # Actors between sources and sinks whose behaviour is Python code run
+        # that code on the host, per firing, through the plugin API
+        # (runtime.py:336-341 overrides): "host" -- a behaviour with no device
+        # kernel (a user-registered behaviour, or an override of a built-in
+        # one), whose firings read their input spans from the device rings and
+        # write their outputs back; "observe" -- a subclass of a device
+        # behaviour that overrides fire (the FirBranch-recorder pattern of
+        # SURVEY 8(c3b)): the device kernel computes the firing and the Python
+        # fire then sees the inputs and the computed outputs (its writes to
+        # ctx.outputs are copied back).  The device math itself never runs on
+        # the host.
+        self.host_fired: dict[str, str] = {}
         for a in g.actors:
             role = plan.roles[a.id]
             b = self.behaviors[0][a.id]
-            if role in ("device", "dynamic") and not is_device(b):
-                raise UnsupportedGraph(
-                    f"actor {a.id} ({role}) has host behaviour {type(b).__name__}; the device "
-                    "executor fires only device behaviours between sources and sinks")
+            if role in ("device", "dynamic"):
+                if not is_device(b):
+                    self.host_fired[a.id] = "host"
+                elif type(b).fire is not DeviceBehavior.fire:
+                    self.host_fired[a.id] = "observe"
             if role in ("source", "config", "sink") and is_device(b):
                 raise UnsupportedGraph(f"actor {a.id} ({role}) needs a host behaviour")
 
@@ -242,6 +254,9 @@ class DeviceRuntime:
         if config.exact and os.environ.get("PB_FIR_MATH") == "paired":
             self.fir_math = _lib.PB_FIR_EXACT_PAIRED
         self.banks = find_filter_banks(plan, self.behaviors[0]) if config.fuse else []
+        # a region with a host-fired member keeps its channels materialised
+        self.banks = [grp for grp in self.banks
+                      if not ({grp.router, grp.combiner, *grp.branches} & set(self.host_fired))]
         self.fused_actors = {a for grp in self.banks for a in [grp.router, *grp.branches]}
         self.virtual = {fid for grp in self.banks for fid in grp.internal_fifos}
         self._allocate()
@@ -269,7 +284,8 @@ class DeviceRuntime:
         route_alias: dict[str, str] = {}
         for a in g.actors:
             b = self.behaviors[0][a.id]
-            if getattr(b, "kernel", "") == "route" and a.id not in self.fused_actors:
+            if getattr(b, "kernel", "") == "route" and a.id not in self.fused_actors and \
+                    a.id not in self.host_fired:
                 (pin,) = a.data_inputs
                 src = g.fifo_into(PortRef(a.id, pin.id))
                 span = src.rate * src.token_bytes
@@ -380,6 +396,21 @@ class DeviceRuntime:
                 self.fir_state[a.id] = m.malloc(S * 2 * 9 * 4)
             elif getattr(b, "kernel", "") == "matmul":
                 b.init(a.id, a.params, None)
+        # host-fired actors: per data port a device gather/scatter buffer and
+        # its pinned host copy, [S][epoch][span]
+        self.host_stage: dict[tuple[str, str], tuple[int, int, np.ndarray, int, str]] = {}
+        for aid in self.host_fired:
+            a = g.actor(aid)
+            for p in a.ports:
+                if p.kind in (CONTROL_IN, CONTROL_OUT):
+                    continue
+                ref = PortRef(aid, p.id)
+                f = g.fifo_into(ref) if p.direction == "in" else \
+                    sorted(g.fifos_from(ref), key=lambda f: f.id)[0]
+                span = f.rate * f.token_bytes
+                dev = m.malloc(S * self.epoch * span)
+                hptr, harr = m.pinned(S * self.epoch * span)
+                self.host_stage[(aid, p.id)] = (dev, hptr, harr, span, f.id)
         _lib.check(self.lib.pb_device_sync(), "allocation")
 
     # ------------------------------------------------------------ span refs
@@ -458,6 +489,10 @@ class DeviceRuntime:
                 continue
             b = self.behaviors[0][aid]
             kind = getattr(b, "kernel", "")
+            if self.host_fired.get(aid) == "host":
+                self.launches.append(("host", aid))
+                done.add(aid)
+                continue
             if aid in bank_at:
                 grp = bank_at[aid]
                 x = g.actor(grp.router)
@@ -490,6 +525,9 @@ class DeviceRuntime:
                 self.launches.append(("fir", dev, len(members), key[1]))
                 self.fir_groups.append((dev, len(members), key[1]))
                 done.update(members)
+                for bid in members:
+                    if bid in self.host_fired:
+                        self.launches.append(("host", bid))
                 continue
             ins = sorted(a.data_inputs, key=lambda p: p.id)
             outs = sorted(a.output_ports, key=lambda p: p.id)
@@ -626,6 +664,8 @@ class DeviceRuntime:
                 raise UnsupportedGraph(f"actor {aid}: no device kernel for behaviour "
                                        f"{a.behavior!r}")
             done.add(aid)
+            if aid in self.host_fired:
+                self.launches.append(("host", aid))
 
         # bulk ring advance for every FIFO
         adv = []
@@ -942,6 +982,8 @@ class DeviceRuntime:
                 _lib.check(lib.pb_fire_dense(item[1], res, st), "dense")
             elif kind == "classify":
                 _lib.check(lib.pb_fire_classify(item[1], res, st), "classify_merge")
+            elif kind == "host":
+                self._fire_host(item[1], it0, E, res)
             if hook is not None:
                 hook(kind, "post")
         for dev, n, block in self.fir_groups:
@@ -953,6 +995,105 @@ class DeviceRuntime:
             _lib.check(lib.pb_rings_advance(self.advance, len(self.advance), res, st),
                        "pb_rings_advance")
         return lib.pb_launch_count() - n0
+
+    def _stage_ref(self, dev: int, span: int, cond: int) -> _lib.SpanRef:
+        """A host-staging buffer [S][epoch][span] as a span ref: row n of
+        stream s at iteration n, written/read only where `cond` is active."""
+        return _lib.SpanRef(dev, self.epoch * span, span, None, self.cap, ALWAYS, cond, 0)
+
+    def _copy_spans(self, srcs: list[_lib.SpanRef], dst: list[_lib.SpanRef], res) -> None:
+        act = _lib.BytesActor()
+        for k, r in enumerate(srcs):
+            act.in_[k] = r
+        for k, r in enumerate(dst):
+            act.out[k] = r
+        act.n_in, act.n_out, act.offset, act.cond = len(srcs), len(dst), 0, ALWAYS
+        _lib.check(self.lib.pb_fire_bytes(act, res, self.stream), "host staging copy")
+
+    def _fire_host(self, aid: str, it0: int, E: int, res) -> None:
+        """Fire a host-fired actor's firings of this epoch through the plugin
+        API (runtime.py:126-190): its active input spans are gathered from the
+        rings into staging and copied to the host, fire() runs per firing in
+        order (dynamic actors get control() first, inactive DRPs zero-length
+        spans), and the output spans go back into every target ring."""
+        g, plan, S, lib = self.graph, self.plan, self.n_streams, self.lib
+        a = g.actor(aid)
+        mode = self.host_fired[aid]
+        ins = sorted([p for p in a.input_ports if p.kind != CONTROL_IN], key=lambda p: p.id)
+        outs = sorted([p for p in a.output_ports if p.kind != CONTROL_OUT], key=lambda p: p.id)
+        for p in ins:
+            dev, hptr, _, span, fid = self.host_stage[(aid, p.id)]
+            self._copy_spans([self._ref(fid)], [self._stage_ref(dev, span, plan.fifo_cond[fid])],
+                             res)
+            _lib.check(lib.pb_memcpy_d2h(hptr, dev, S * E * span, self.stream))
+        for p in outs:
+            dev, hptr, harr, span, fid = self.host_stage[(aid, p.id)]
+            if mode == "observe":   # the device kernel's outputs, as fired
+                self._copy_spans([self._ref(fid, producer=True)],
+                                 [self._stage_ref(dev, span, plan.fifo_cond[fid])], res)
+                _lib.check(lib.pb_memcpy_d2h(hptr, dev, S * E * span, self.stream))
+            else:
+                harr[:S * E * span] = 0
+        n_cond = len(plan.conds)
+        act = np.ones((max(1, n_cond), S, self.cap), dtype=np.uint8)
+        if n_cond:
+            _lib.check(lib.pb_memcpy_d2h(act.ctypes.data, self.res_act, act.nbytes, self.stream))
+        _lib.check(lib.pb_stream_sync(self.stream), f"{aid}: host firing")
+
+        def active(c: int, s: int) -> np.ndarray:
+            return np.ones(E, dtype=bool) if c == ALWAYS else act[c, s, :E].astype(bool)
+
+        port_cond = {}
+        for p in ins + outs:
+            fid = self.host_stage[(aid, p.id)][4]
+            port_cond[p.id] = plan.fifo_cond[fid]
+        ctl = None
+        cp = a.control_input
+        if cp is not None:
+            src = g.fifo_into(PortRef(aid, cp.id)).src
+            stride = self.ctl_stride[src]
+            ctl = (self.ctl_host[src][1][:S * E * stride].reshape(S, E, stride),
+                   g.value_length(src))
+        rates_all = {p.id: p.rate for p in a.ports}
+        views = {p.id: self.host_stage[(aid, p.id)][2][:S * E * self.host_stage[(aid, p.id)][3]]
+                 .reshape(S, E, -1) for p in ins + outs}
+        for s in range(S):
+            b = self.behaviors[s][aid]
+            seed = actor_seed(self.seeds[s], aid)
+            on = active(plan.actor_cond[aid], s)
+            pact = {pid: active(c, s) for pid, c in port_cond.items()}
+            j = int(self.firings[aid][s])
+            for n in range(E):
+                if not on[n]:
+                    continue
+                values = None
+                try:
+                    if ctl is not None:
+                        values = decode_control(ctl[0][s, n], ctl[1])
+                        b.control(aid, j, values)
+                    rates = dict(rates_all)
+                    inputs, outputs = {}, {}
+                    for p in ins:
+                        live = bool(pact[p.id][n])
+                        rates[p.id] = p.rate if live else 0
+                        inputs[p.id] = memoryview(views[p.id][s, n]) if live else memoryview(b"")
+                    for p in outs:
+                        live = bool(pact[p.id][n])
+                        rates[p.id] = p.rate if live else 0
+                        outputs[p.id] = memoryview(views[p.id][s, n]) if live else \
+                            memoryview(bytearray(0))
+                    b.fire(FireContext(aid, j, rates, inputs, outputs, a.params, seed, values,
+                                       device_fired=mode == "observe"))
+                except Exception as e:  # noqa: BLE001
+                    raise ActorPanic(aid, e) from e
+                j += 1
+        for p in outs:
+            dev, hptr, _, span, fid = self.host_stage[(aid, p.id)]
+            _lib.check(lib.pb_memcpy_h2d(dev, hptr, S * E * span, self.stream))
+            targets = [self._ref(t, producer=True) for t in self._port_targets(aid, p.id)]
+            for k in range(0, len(targets), _lib.PB_MAX_PORTS):
+                self._copy_spans([self._stage_ref(dev, span, plan.fifo_cond[fid])],
+                                 targets[k:k + _lib.PB_MAX_PORTS], res)
 
     def set_fir_math(self, math: int) -> None:
         """Switch the FIR arithmetic mode (PB_FIR_EXACT / _EXACT_PAIRED / _FMA)
@@ -1056,7 +1197,7 @@ class DeviceRuntime:
                 b = self.behaviors[s][a.id]
                 if a.id in self.sources and self.plan.roles[a.id] == "source":
                     continue
-                if is_device(b):
+                if is_device(b) and a.id not in self.host_fired:
                     continue   # stateless kernels, configured at build time
                 try:
                     b.init(a.id, a.params, actor_seed(self.seeds[s], a.id))
@@ -1082,7 +1223,7 @@ class DeviceRuntime:
         """Bulk-only graphs (bulk sources, native policies, single-port
         always-active digest sinks) run with overlapped copies and hashing."""
         g = self.graph
-        if self.config.trace is not None or self.config.pipeline == 1:
+        if self.config.trace is not None or self.config.pipeline == 1 or self.host_fired:
             return False
         for a in g.actors:
             role = self.plan.roles[a.id]
