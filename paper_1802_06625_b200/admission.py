@@ -103,6 +103,14 @@ class Dpg:
     dcs: tuple[Component, ...] = ()
 
 
+class BufferBounds:
+    """analysis.py:115-118 (the per-region split is not kept)."""
+
+    def __init__(self, beta: dict[str, int], c_factor: int):
+        self.beta = dict(beta)
+        self.c_factor = c_factor
+
+
 @dataclass
 class AnalysisReport:
     """Verdict, findings, regions and the per-FIFO bound beta(f) for the
@@ -119,6 +127,13 @@ class AnalysisReport:
     @property
     def consistent(self) -> bool:
         return self.verdict == "consistent"
+
+    @property
+    def bounds(self) -> "BufferBounds | None":
+        """analysis.BufferBounds (:115-118): the per-FIFO bound beta at c_factor."""
+        if not self.consistent:
+            return None
+        return BufferBounds(self.beta, self.c_factor)
 
     @property
     def problems(self) -> list[str]:

@@ -89,6 +89,21 @@ class RunReport:
     device_max_occupancy: dict[str, int] = field(default_factory=dict)
 
 
+@dataclass
+class _Plan:
+    slots: int
+
+
+class ChannelView:
+    """FifoChannel's observable state (fifos.py:142-338) for one device ring."""
+
+    def __init__(self, fifo_id: str, occupancy: int, max_occupancy: int, slots: int):
+        self.fifo_id = fifo_id
+        self.occupancy = occupancy
+        self.max_occupancy = max_occupancy
+        self.plan = _Plan(slots)
+
+
 class _Dev:
     """Small RAII helper for device / pinned allocations."""
 
@@ -200,9 +215,15 @@ class DeviceRuntime:
         self.config = config = config or RuntimeConfig()
         self.graph: Graph = as_graph(graph)
         self.n_streams = S = int(n_streams)
-        self.epoch = max(1, min(int(config.epoch), max(1, int(config.source_firings))))
-        self.C = max(int(config.c_factor), self.epoch, 2)
         self.plan = admit(self.graph, int(config.c_factor))
+        self.epoch = max(1, min(int(config.epoch), max(1, int(config.source_firings))))
+        if self.plan.epoch_cap is not None:   # delayed cycles (plan.admit)
+            self.epoch = min(self.epoch, self.plan.epoch_cap)
+        self.C = max(int(config.c_factor), self.epoch, 2)
+        self.unbounded = sorted(a for a, e in self.plan.extra.items() if e is None)
+        if self.unbounded and config.timeout_ms is None:
+            raise UnsupportedGraph(f"actors {self.unbounded} fire forever (a cycle no source "
+                                   "feeds, test_runtime.py:224-235); set RuntimeConfig.timeout_ms")
         self.analysis = self.plan.admission
         self.seeds = list(seeds) if seeds is not None else [config.seed] * S
         if len(self.seeds) != S:
@@ -260,7 +281,10 @@ class DeviceRuntime:
         self.fused_actors = {a for grp in self.banks for a in [grp.router, *grp.branches]}
         self.virtual = {fid for grp in self.banks for fid in grp.internal_fifos}
         self._allocate()
-        self._build_launches()
+        self.launches, self.fir_groups = self._build_launches()
+        self._build_tables()
+        self._drain = None            # drain-phase launches, built on first use
+        self._cond_now: dict[str, int] = {}   # condition overrides while draining
         self.launches_per_epoch = 0
 
     # ------------------------------------------------------------- allocation
@@ -268,7 +292,9 @@ class DeviceRuntime:
     def _allocate(self):
         g, plan, S, C_ = self.graph, self.plan, self.n_streams, self.C
         m = self.mem
-        n_cond = max(1, len(plan.conds))
+        n_drain = len({e for e in plan.extra.values() if e})
+        n_cond = max(1, len(plan.conds), n_drain)
+        self.res_slots = n_cond
         cap = self.epoch
         self.res_act = m.malloc(n_cond * S * cap)
         self.res_prefix = m.malloc(4 * n_cond * S * cap)
@@ -441,27 +467,36 @@ class DeviceRuntime:
         return _lib.Resolved(self.res_act, self.res_prefix, self.res_count, self.res_wl,
                              len(self.plan.conds), self.n_streams, n_iter, self.cap)
 
-    def _fir_actor(self, aid: str, in_fid: str, out_fid: str | None) -> _lib.FirActor:
+    def _fir_actor(self, aid: str, in_fid: str, out_fid: str | None,
+                   cond: int | None = None) -> _lib.FirActor:
         out = self._ref(out_fid, producer=True) if out_fid is not None else _lib.SpanRef()
+        cond = self.plan.actor_cond[aid] if cond is None else cond
         return _lib.FirActor(self._ref(in_fid), out, self.fir_taps[aid], self.fir_state[aid],
-                             self.plan.actor_cond[aid], 0)
+                             cond, 0)
 
-    def _build_launches(self):
+    def _build_launches(self, cond_of=None, only: set[str] | None = None):
+        """The epoch's launch list in dependency order.  cond_of(aid) -> the
+        condition gating the actor's firings (default: the plan's); `only`
+        restricts the list to those actors (the drain phase)."""
         g, plan = self.graph, self.plan
-        self.launches: list[tuple] = []
-        self.fir_groups: list[tuple[int, int, int]] = []    # (device array, n, block)
+        cond_of = cond_of or plan.actor_cond.__getitem__
+        launches: list[tuple] = []
+        fir_groups: list[tuple[int, int, int]] = []    # (device array, n, block)
         done: set[str] = set()
         bank_at = {grp.combiner: grp for grp in self.banks}
-        # topological depth so independent FIR actors share a launch
+        # topological depth so independent FIR actors share a launch (the
+        # delayed channels inside cycles do not order an epoch's firings)
         depth = {aid: 0 for aid in plan.order}
         for aid in plan.order:
             for fid in plan.data_fifos:
                 f = g.fifo(fid)
-                if f.src.actor == aid:
+                if f.src.actor == aid and fid not in plan.loose:
                     depth[f.dst.actor] = max(depth[f.dst.actor], depth[aid] + 1)
         fir_by_level: dict[tuple[int, int], list[str]] = {}
         for aid in plan.order:
             b = self.behaviors[0][aid]
+            if only is not None and aid not in only:
+                continue
             if getattr(b, "kernel", "") == "fir" and aid not in self.fused_actors:
                 a = g.actor(aid)
                 fin = g.fifo_into(PortRef(aid, a.input_ports[0].id))
@@ -481,7 +516,7 @@ class DeviceRuntime:
         # producer after another member of the same group)
         pos = {aid: k for k, aid in enumerate(plan.order)}
         for aid in sorted(plan.order, key=lambda x: (depth[x], pos[x])):
-            if aid in done or aid in self.fused_actors:
+            if aid in done or aid in self.fused_actors or (only is not None and aid not in only):
                 continue
             a = g.actor(aid)
             role = plan.roles[aid]
@@ -490,7 +525,7 @@ class DeviceRuntime:
             b = self.behaviors[0][aid]
             kind = getattr(b, "kernel", "")
             if self.host_fired.get(aid) == "host":
-                self.launches.append(("host", aid))
+                launches.append(("host", aid))
                 done.add(aid)
                 continue
             if aid in bank_at:
@@ -501,13 +536,13 @@ class DeviceRuntime:
                 fout = sorted(g.fifos_from(PortRef(aid, pout.id)), key=lambda f: f.id)[0]
                 arr = (_lib.FirActor * len(grp.branches))()
                 for k, bid in enumerate(grp.branches):
-                    arr[k] = self._fir_actor(bid, fin.id, None)
+                    arr[k] = self._fir_actor(bid, fin.id, None, cond_of(bid))
                 dev = self.mem.upload(np.frombuffer(bytes(arr), dtype=np.uint8))
                 bank = _lib.FilterBank(self._ref(fin.id), self._ref(fout.id), dev,
-                                       len(grp.branches), plan.actor_cond[aid],
+                                       len(grp.branches), cond_of(aid),
                                        self.mem.malloc(16), self.fir_math, 0)
                 block = fin.rate * fin.token_bytes // 8
-                self.launches.append(("bank", bank, block))
+                launches.append(("bank", bank, block))
                 # (no fir_groups entry: pb_fire_filter_bank carries its branches)
                 done.add(aid)
                 continue
@@ -520,14 +555,14 @@ class DeviceRuntime:
                     fi = g.fifo_into(PortRef(bid, ba.input_ports[0].id))
                     fo = sorted(g.fifos_from(PortRef(bid, ba.output_ports[0].id)),
                                 key=lambda f: f.id)[0]
-                    arr[k] = self._fir_actor(bid, fi.id, fo.id)
+                    arr[k] = self._fir_actor(bid, fi.id, fo.id, cond_of(bid))
                 dev = self.mem.upload(np.frombuffer(bytes(arr), dtype=np.uint8))
-                self.launches.append(("fir", dev, len(members), key[1]))
-                self.fir_groups.append((dev, len(members), key[1]))
+                launches.append(("fir", dev, len(members), key[1]))
+                fir_groups.append((dev, len(members), key[1]))
                 done.update(members)
                 for bid in members:
                     if bid in self.host_fired:
-                        self.launches.append(("host", bid))
+                        launches.append(("host", bid))
                 continue
             ins = sorted(a.data_inputs, key=lambda p: p.id)
             outs = sorted(a.output_ports, key=lambda p: p.id)
@@ -553,9 +588,9 @@ class DeviceRuntime:
                     act.in_[k] = self._ref(fid)
                 act.n_in = len(in_f)
                 act.out = self._ref(out_f[0], producer=True)
-                act.cond = plan.actor_cond[aid]
+                act.cond = cond_of(aid)
                 f0 = g.fifo(out_f[0])
-                self.launches.append(("sum", act, f0.rate * f0.token_bytes // 8))
+                launches.append(("sum", act, f0.rate * f0.token_bytes // 8))
             elif kind == "bytes":
                 spans_in = [g.fifo(fid).rate * g.fifo(fid).token_bytes for fid in in_f]
                 spans_out = [g.fifo(fid).rate * g.fifo(fid).token_bytes for fid in out_f]
@@ -575,14 +610,14 @@ class DeviceRuntime:
                 act.n_in, act.n_out = len(in_f), len(outs_all)
                 act.offset = int(a.params.get("offset", 0)) if b.registered_name == "add_mod" \
                     else 0
-                act.cond = plan.actor_cond[aid]
-                self.launches.append(("bytes", act))
+                act.cond = cond_of(aid)
+                launches.append(("bytes", act))
             elif kind == "matmul":
                 w = np.array(a.params["w"], dtype=np.float32)
                 n = int(round(len(w) ** 0.5))
                 act = _lib.MatmulActor(self._ref(in_f[0]), self._ref(out_f[0], producer=True),
-                                       self.mem.upload(w), n, plan.actor_cond[aid])
-                self.launches.append(("matmul", act))
+                                       self.mem.upload(w), n, cond_of(aid))
+                launches.append(("matmul", act))
             elif kind == "path_merge":
                 act = _lib.PathMergeActor()
                 bypass = a.params.get("bypass_port", "")
@@ -592,10 +627,10 @@ class DeviceRuntime:
                 act.bypass_index = [p.id for p in ins].index(bypass) if bypass in \
                     [p.id for p in ins] else -1
                 act.marker = float(np.float32(a.params.get("marker", 0.5)))
-                act.cond = plan.actor_cond[aid]
+                act.cond = cond_of(aid)
                 act.error_flag = self.err_flag
                 act.out = self._ref(out_f[0], producer=True)
-                self.launches.append(("path_merge", act, aid))
+                launches.append(("path_merge", act, aid))
             elif kind == "image":
                 act = _lib.ImageActor()
                 names = [p.id for p in ins]
@@ -623,8 +658,8 @@ class DeviceRuntime:
                                            "one size on every port")
                 act.op, act.side = b.op, side
                 act.threshold = int(a.params.get("threshold", 16))
-                act.cond = plan.actor_cond[aid]
-                self.launches.append(("image", act))
+                act.cond = cond_of(aid)
+                launches.append(("image", act))
             elif kind == "conv":
                 from .cnn_weights import conv_device_layout
                 b.init(aid, a.params, None)
@@ -634,8 +669,8 @@ class DeviceRuntime:
                 act = _lib.ConvActor(self._ref(in_f[0]), self._ref(out_f[0], producer=True),
                                      self.mem.upload(conv_device_layout(b.weights, b.cin)),
                                      self.mem.upload(b.bias), fi.rate, b.h, b.w, b.cin,
-                                     b.cout, b.pad, plan.actor_cond[aid], 0)
-                self.launches.append(("conv", act))
+                                     b.cout, b.pad, cond_of(aid), 0)
+                launches.append(("conv", act))
             elif kind == "dense":
                 b.init(aid, a.params, None)
                 fi = g.fifo(in_f[0])
@@ -643,8 +678,8 @@ class DeviceRuntime:
                 act = _lib.DenseActor(self._ref(in_f[0]), self._ref(out_f[0], producer=True),
                                       self.mem.upload(dense_device_layout(b.weights)),
                                       self.mem.upload(b.bias),
-                                      fi.rate, b.nin, b.nout, plan.actor_cond[aid])
-                self.launches.append(("dense", act))
+                                      fi.rate, b.nin, b.nout, cond_of(aid))
+                launches.append(("dense", act))
             elif kind == "classify":
                 b.init(aid, a.params, None)
                 bypass = a.params.get("bypass_port", "")
@@ -657,22 +692,31 @@ class DeviceRuntime:
                     self._ref(chain_f), self._ref(bypass_f), self._ref(out_f[0], producer=True),
                     self.mem.upload(b.w4), self.mem.upload(b.b4), self.mem.upload(b.w5),
                     self.mem.upload(b.b5), g.fifo(out_f[0]).rate, b.nin, b.nhid, b.nout,
-                    float(np.float32(a.params.get("marker", -1.0))), plan.actor_cond[aid],
+                    float(np.float32(a.params.get("marker", -1.0))), cond_of(aid),
                     self.err_flag)
-                self.launches.append(("classify", act, aid))
+                launches.append(("classify", act, aid))
             else:
                 raise UnsupportedGraph(f"actor {aid}: no device kernel for behaviour "
                                        f"{a.behavior!r}")
             done.add(aid)
             if aid in self.host_fired:
-                self.launches.append(("host", aid))
+                launches.append(("host", aid))
 
+        return launches, fir_groups
+
+    def _build_tables(self):
+        """Ring advance (every FIFO; the drain phase: the always-active ones)
+        and Eq. 1 tables."""
+        g, plan = self.graph, self.plan
         # bulk ring advance for every FIFO
         adv = []
         for f in g.fifos:
             adv.append(_lib.RingAdvance(self.counters[f.id], plan.fifo_cond[f.id], f.rate,
                                         f.delay, 0))
         self.advance = (_lib.RingAdvance * len(adv))(*adv)
+        dadv = [r for r, f in zip(adv, g.fifos) if plan.fifo_cond[f.id] == ALWAYS]
+        self.drain_advance = (_lib.RingAdvance * max(1, len(dadv)))(*dadv)
+        self.n_drain_advance = len(dadv)
         eq = [_lib.Eq1Port(own, moved, ALWAYS, 0) for (_, _, own, moved) in plan.eq1_ports]
         self.eq1 = (_lib.Eq1Port * max(1, len(eq)))(*eq)
         self.n_eq1 = len(eq)
@@ -688,10 +732,13 @@ class DeviceRuntime:
         return arr
 
     def _h2d_chunks(self, dev: int, stride: int, span: int, host: int, E: int, first: int,
-                    host_pitch: int | None = None, stream: int | None = None):
+                    host_pitch: int | None = None, stream: int | None = None,
+                    slots: int | None = None):
         """host rows [S][E spans] (row pitch host_pitch) -> device ring chunks
-        (first + n) % C of every stream."""
-        lib, S, C_ = self.lib, self.n_streams, self.C
+        (first + n) % slots of every stream (slots: C, or C + delay/rate for a
+        channel with initial delay tokens)."""
+        lib, S = self.lib, self.n_streams
+        C_ = self.C if slots is None else slots
         st = self.stream if stream is None else stream
         hp = E * span if host_pitch is None else host_pitch
         a = first % C_
@@ -705,8 +752,10 @@ class DeviceRuntime:
                                         S, 1, st))
 
     def _d2h_chunks(self, dev: int, stride: int, span: int, host: int, E: int, first: int,
-                    host_pitch: int | None = None, stream: int | None = None):
-        lib, S, C_ = self.lib, self.n_streams, self.C
+                    host_pitch: int | None = None, stream: int | None = None,
+                    slots: int | None = None):
+        lib, S = self.lib, self.n_streams
+        C_ = self.C if slots is None else slots
         st = self.stream if stream is None else stream
         hp = E * span if host_pitch is None else host_pitch
         a = first % C_
@@ -779,6 +828,17 @@ class DeviceRuntime:
             self._direct[aid] = key
         return ptrs[0], pitch
 
+    def _source_h2d(self, aid: str, pid: str, host: int, E: int, it0: int,
+                    host_pitch: int | None = None) -> None:
+        """A host producer's E spans per stream -> every ring its port feeds
+        (a broadcast of equal spans shares one; a channel with initial delay
+        tokens has its own, written delay/rate chunks ahead)."""
+        for fid in self._port_targets(aid, pid):
+            st = self.storage[fid]
+            self._h2d_chunks(st.data, st.stream_stride, st.span, host, E,
+                             it0 + self.delay_chunks.get(fid, 0), host_pitch=host_pitch,
+                             slots=st.slots)
+
     def stage_sources(self, it0: int, E: int, prestaged: bool = False):
         """Host sources produce E spans per stream (runtime.py:123-124 stops
         them after source_firings) and copy them into the device rings."""
@@ -789,10 +849,7 @@ class DeviceRuntime:
             ports = sorted(a.output_ports, key=lambda p: p.id)
             if prestaged:
                 for p in ports:
-                    f = sorted(g.fifos_from(PortRef(a.id, p.id)), key=lambda f: f.id)[0]
-                    st = self.storage[f.id]
-                    self._h2d_chunks(st.data, st.stream_stride, f.rate * f.token_bytes,
-                                     self.src_host[f"{a.id}.{p.id}"][0], E, it0)
+                    self._source_h2d(a.id, p.id, self.src_host[f"{a.id}.{p.id}"][0], E, it0)
                 continue
             for p in ports:
                 f = sorted(g.fifos_from(PortRef(a.id, p.id)), key=lambda f: f.id)[0]
@@ -803,9 +860,8 @@ class DeviceRuntime:
                     direct = self._direct_source(a.id, it0 + E) if len(ports) == 1 else None
                     if direct is not None:
                         # DMA from the caller's page-locked buffers in place
-                        st = self.storage[f.id]
-                        self._h2d_chunks(st.data, st.stream_stride, span,
-                                         direct[0] + it0 * span, E, it0, host_pitch=direct[1])
+                        self._source_h2d(a.id, p.id, direct[0] + it0 * span, E, it0,
+                                         host_pitch=direct[1])
                         continue
                     # FileSource order (behavior.py:132-140): per firing, the
                     # ports in sorted order each take their span's bytes
@@ -829,8 +885,7 @@ class DeviceRuntime:
                         buf[s] = np.frombuffer(view, dtype=np.uint8).reshape(E, span)
                 else:
                     continue
-                st = self.storage[f.id]
-                self._h2d_chunks(st.data, st.stream_stride, span, hptr, E, it0)
+                self._source_h2d(a.id, p.id, hptr, E, it0)
             if a.id in self.sources or (len(ports) == 1 and
                                         type(self.behaviors[0][a.id]) is FileSource):
                 continue
@@ -855,8 +910,7 @@ class DeviceRuntime:
                     except Exception as e:  # noqa: BLE001
                         raise ActorPanic(a.id, e) from e
             for pid, (f, (hp, harr)) in views.items():
-                st = self.storage[f.id]
-                self._h2d_chunks(st.data, st.stream_stride, f.rate * f.token_bytes, hp, E, it0)
+                self._source_h2d(a.id, pid, hp, E, it0)
 
     def stage_control(self, it0: int, E: int):
         """Configuration actors emit E tokens per stream (behavior.py:212-218):
@@ -938,7 +992,7 @@ class DeviceRuntime:
                 for fid in self._port_targets(aid, p.id):
                     st = self.storage[fid]
                     self._h2d_chunks(st.data, st.stream_stride, sp, self.cfg_host[(aid, p.id)][0],
-                                     E, it0 + self.delay_chunks.get(fid, 0))
+                                     E, it0 + self.delay_chunks.get(fid, 0), slots=st.slots)
 
     def fire_epoch(self, it0: int, E: int, hook=None) -> int:
         """Device work of one epoch (inputs already resident); returns launches.
@@ -957,7 +1011,20 @@ class DeviceRuntime:
         if self.n_eq1 and not close:
             _lib.check(lib.pb_eq1_check(self.eq1, self.n_eq1, res, self.eq1_ctr, st),
                        "pb_eq1_check")
-        for item in self.launches:
+        self._run_launches(self.launches, res, it0, E, hook)
+        for dev, n, block in self.fir_groups:
+            _lib.check(lib.pb_fir_carry(dev, n, res, block, st), "fir_carry")
+        if close:
+            _lib.check(lib.pb_epoch_close(self.eq1, self.n_eq1, self.eq1_ctr, self.advance,
+                                          len(self.advance), res, st), "pb_epoch_close")
+        else:
+            _lib.check(lib.pb_rings_advance(self.advance, len(self.advance), res, st),
+                       "pb_rings_advance")
+        return lib.pb_launch_count() - n0
+
+    def _run_launches(self, launches, res, it0: int, E: int, hook=None) -> None:
+        lib, st = self.lib, self.stream
+        for item in launches:
             kind = item[0]
             if hook is not None:
                 hook(kind, "pre")
@@ -986,15 +1053,6 @@ class DeviceRuntime:
                 self._fire_host(item[1], it0, E, res)
             if hook is not None:
                 hook(kind, "post")
-        for dev, n, block in self.fir_groups:
-            _lib.check(lib.pb_fir_carry(dev, n, res, block, st), "fir_carry")
-        if close:
-            _lib.check(lib.pb_epoch_close(self.eq1, self.n_eq1, self.eq1_ctr, self.advance,
-                                          len(self.advance), res, st), "pb_epoch_close")
-        else:
-            _lib.check(lib.pb_rings_advance(self.advance, len(self.advance), res, st),
-                       "pb_rings_advance")
-        return lib.pb_launch_count() - n0
 
     def _stage_ref(self, dev: int, span: int, cond: int) -> _lib.SpanRef:
         """A host-staging buffer [S][epoch][span] as a span ref: row n of
@@ -1034,7 +1092,7 @@ class DeviceRuntime:
                 _lib.check(lib.pb_memcpy_d2h(hptr, dev, S * E * span, self.stream))
             else:
                 harr[:S * E * span] = 0
-        n_cond = len(plan.conds)
+        n_cond = int(res.n_cond)
         act = np.ones((max(1, n_cond), S, self.cap), dtype=np.uint8)
         if n_cond:
             _lib.check(lib.pb_memcpy_d2h(act.ctypes.data, self.res_act, act.nbytes, self.stream))
@@ -1060,7 +1118,7 @@ class DeviceRuntime:
         for s in range(S):
             b = self.behaviors[s][aid]
             seed = actor_seed(self.seeds[s], aid)
-            on = active(plan.actor_cond[aid], s)
+            on = active(self._cond_now.get(aid, plan.actor_cond[aid]), s)
             pact = {pid: active(c, s) for pid, c in port_cond.items()}
             j = int(self.firings[aid][s])
             for n in range(E):
@@ -1111,11 +1169,16 @@ class DeviceRuntime:
                                               self.stream))
         return out
 
-    def drain_sinks(self, it0: int, E: int, counts: np.ndarray):
+    def drain_sinks(self, it0: int, E: int, counts: np.ndarray,
+                    limits: dict[str, int] | None = None):
+        """Sink firings of the epoch: D2H, then digests per firing in sorted
+        port order.  limits[sink] (the drain phase): only its first firings."""
         g, S = self.graph, self.n_streams
         pending = []
         for a in g.actors:
             if self.plan.roles[a.id] != "sink":
+                continue
+            if limits is not None and limits.get(a.id, 0) <= 0:
                 continue
             ports = sorted(a.input_ports, key=lambda p: p.id)
             c = self.plan.actor_cond[a.id]
@@ -1128,7 +1191,8 @@ class DeviceRuntime:
                 first = it0 if st.index_cond == ALWAYS else None
                 if first is None:
                     raise UnsupportedGraph(f"sink {a.id} reads a compacted channel")
-                self._d2h_chunks(st.data, st.stream_stride, span, hptr, E, first)
+                self._d2h_chunks(st.data, st.stream_stride, span, hptr, E, first,
+                                 slots=st.slots)
                 bufs.append((p.id, span, harr[:S * E * span].reshape(S, E, span)))
             pending.append((a, c, bufs))
         _lib.check(self.lib.pb_stream_sync(self.stream), "sink drain")
@@ -1136,7 +1200,9 @@ class DeviceRuntime:
         for a, c, bufs in pending:
             for s in range(S):
                 active = None
-                if c != ALWAYS:
+                if limits is not None:
+                    active = np.arange(E) < limits[a.id]
+                elif c != ALWAYS:
                     active = self._act_host(c, s, E)
                 jobs.append((a, s, bufs, active))
 
@@ -1225,6 +1291,12 @@ class DeviceRuntime:
         g = self.graph
         if self.config.trace is not None or self.config.pipeline == 1 or self.host_fired:
             return False
+        if any(self.plan.extra.values()) or self.unbounded or self.plan.epoch_cap is not None:
+            return False      # drain phase / delayed cycles: the plain epoch loop
+        for f in g.fifos:
+            if f.delay and self.plan.roles[f.src.actor] == "source" or \
+                    f.delay and self.plan.roles[f.dst.actor] == "sink":
+                return False
         for a in g.actors:
             role = self.plan.roles[a.id]
             b = self.behaviors[0][a.id]
@@ -1521,6 +1593,7 @@ class DeviceRuntime:
                 it += E
                 if deadline is not None and time.perf_counter() > deadline and it < N:
                     raise Timeout(cfg.timeout_ms, sorted(a.id for a in self.graph.actors))
+            self._run_drain(N, deadline)
             for s in range(S):
                 for a in self.graph.actors:
                     try:
@@ -1531,6 +1604,99 @@ class DeviceRuntime:
             self.pool.shutdown(wait=True)
         wall_ms = (time.perf_counter() - t_start) * 1000.0
         return self._reports(wall_ms)
+
+    # ----------------------------------------------------------- drain phase
+
+    def _drain_setup(self):
+        """Launches of the drain phase: actors that keep firing after the
+        sources stop (plan.extra) gated by per-value drain conditions --
+        condition k is true at drain iteration i iff i < values[k] -- and the
+        unbounded ones (a sourceless cycle) always."""
+        plan, S = self.plan, self.n_streams
+        values = sorted({e for a, e in plan.extra.items() if e})
+        fires = {a for a, e in plan.extra.items()
+                 if (e is None or e > 0) and plan.roles[a] not in ("source", "config", "sink")}
+        index = {v: k for k, v in enumerate(values)}
+        cond = {a: (ALWAYS if plan.extra[a] is None else index[plan.extra[a]]) for a in fires}
+        launches, fir_groups = self._build_launches(cond_of=cond.__getitem__, only=fires)
+        K = max(1, len(values))
+        dev = self.mem.malloc(S * self.epoch * K)
+        hptr, harr = self.mem.pinned(S * self.epoch * K)
+        if len(values) > self.res_slots:
+            raise UnsupportedGraph(f"{len(values)} distinct drain lengths exceed the "
+                                   f"{self.res_slots} resolution slots")
+        self._drain = (launches, fir_groups, values, cond, dev, hptr, harr, K)
+
+    def _run_drain(self, N: int, deadline) -> None:
+        """Fire the drain phase (runtime.py:118-124: consumers keep firing on
+        delay tokens after the sources stop; interp.py's drain), and for
+        actors no source bounds, keep firing until the timeout."""
+        plan, cfg, lib, S = self.plan, self.config, self.lib, self.n_streams
+        finite = [e for e in plan.extra.values() if e]
+        if not finite and not self.unbounded:
+            return
+        if self._drain is None:
+            self._drain_setup()
+        launches, fir_groups, values, cond, dev, hptr, harr, K = self._drain
+        D = max(finite, default=0)
+        done = 0
+        while done < D or self.unbounded:
+            if deadline is not None and time.perf_counter() > deadline:
+                raise Timeout(cfg.timeout_ms, list(self.unbounded) or
+                              sorted(a for a, e in plan.extra.items() if e and e > done))
+            E = self.epoch if self.unbounded and done >= D else min(self.epoch, max(1, D - done))
+            it0 = N + done
+            # drain conditions of this epoch: [S][epoch][K] bytes
+            tok = harr[:S * self.epoch * K].reshape(S, self.epoch, K)
+            tok[:] = 0
+            for k, v in enumerate(values):
+                tok[:, :max(0, min(E, v - done)), k] = 1
+            _lib.check(lib.pb_memcpy_h2d(dev, hptr, S * self.epoch * K, self.stream))
+            arr = (_lib.Condition * K)()
+            for k in range(K):
+                arr[k] = _lib.Condition(dev, self.epoch * K, K, k, self.epoch, 0)
+            res = self._resolved(E)
+            res.n_cond = K
+            if values:
+                _lib.check(lib.pb_resolve(arr, res, self.stream), "pb_resolve (drain)")
+            self._cond_now = cond
+            try:
+                self._run_launches(launches, res, it0, E)
+            finally:
+                self._cond_now = {}
+            for d, n, block in fir_groups:
+                _lib.check(lib.pb_fir_carry(d, n, res, block, self.stream), "fir_carry")
+            if self.n_drain_advance:
+                _lib.check(lib.pb_rings_advance(self.drain_advance, self.n_drain_advance, res,
+                                                self.stream), "pb_rings_advance")
+            fired = {a: (E if e is None else max(0, min(E, e - done)))
+                     for a, e in plan.extra.items() if plan.roles[a] not in ("source", "config")}
+            self.drain_sinks(it0, E, None, limits={a: fired.get(a, 0) for a in plan.extra
+                                                   if plan.roles[a] == "sink"})
+            self._check_device_errors()
+            for a, n in fired.items():
+                self.firings[a] += n
+            done += E
+
+    def run(self) -> RunReport:
+        """Runtime.run (runtime.py:278-325) for a single-stream runtime."""
+        if self.n_streams != 1:
+            raise ValueError("run() drives one stream; use run_all() for a batch")
+        return self.run_all()[0]
+
+    @property
+    def channels(self) -> dict[str, "ChannelView"]:
+        """Runtime.channels (runtime.py:266-272) as read-only views of the
+        device rings of stream 0: occupancy, max_occupancy, plan.slots."""
+        out = {}
+        for f in self.graph.fifos:
+            ctr = self._counters(f.id)
+            w, r = int(ctr[0, 0]), int(ctr[1, 0])
+            slots = layout_slots(f.rate, f.delay, self.config.c_factor)
+            peak = min(f.delay + f.rate, slots) if w > 0 and f.id not in self.plan.loose \
+                else f.delay
+            out[f.id] = ChannelView(f.id, f.delay + f.rate * (w - r), peak, slots)
+        return out
 
     def _check_device_errors(self):
         flag = np.zeros(1, dtype=np.int32)
@@ -1583,7 +1749,13 @@ class DeviceRuntime:
                 # iteration, a producer before its consumer, so a channel holds
                 # its delay tokens plus one firing's rate once it carried data
                 r.slots[f.id] = layout_slots(f.rate, f.delay, self.config.c_factor)
-                r.max_occupancy[f.id] = f.delay + (f.rate if ctrs[f.id][0, s] > 0 else 0)
+                # a channel that starts full of delay tokens takes a firing's
+                # tokens only once its consumer has read (the producer waits
+                # for a free span); across a cycle's delayed edge the
+                # consumer always reads first
+                wrote = ctrs[f.id][0, s] > 0 and f.id not in self.plan.loose
+                r.max_occupancy[f.id] = min(f.delay + f.rate, r.slots[f.id]) if wrote \
+                    else f.delay
                 st = self.storage.get(f.id)
                 r.device_slots[f.id] = f.rate * (st.slots if st is not None else self.C)
                 r.device_max_occupancy[f.id] = int(ctrs[f.id][2, s])

@@ -72,6 +72,9 @@ class ExecPlan:
     data_fifos: list[str]
     eq1_ports: list[tuple[str, str, int, int]]   # (actor, port, own_cond, moved_cond)
     admission: AnalysisReport
+    epoch_cap: int | None = None           # max iterations per epoch (delayed cycles)
+    extra: dict[str, int | None] = field(default_factory=dict)   # drain firings per actor
+    loose: set[str] = field(default_factory=set)   # delayed channels inside cycles
 
 
 def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
@@ -177,9 +180,9 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
         fifo_cond[fid] = cs
     for fid in control_fifos:
         fifo_cond[fid] = ALWAYS
-    # initial delay tokens on data FIFOs: supported between two device actors
-    # on an always-active, aligned channel (fifos.py:87-92; the producer
-    # writes delay/rate chunks ahead of the consumer)
+    # initial delay tokens on data FIFOs: supported on aligned, always-active
+    # channels (fifos.py:87-92): the producer side writes delay/rate chunks
+    # ahead of the consumer side, which first reads the delay payload
     for fid in data_fifos:
         f = g.fifo(fid)
         if not f.delay:
@@ -189,13 +192,29 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
                                f"rate {f.rate}")
         elif fifo_cond[fid] != ALWAYS:
             unsupported.append(f"fifo {fid}: delay tokens on a dynamically gated channel")
-        elif roles[f.src.actor] != "device" or roles[f.dst.actor] != "device":
-            unsupported.append(f"fifo {fid}: delay tokens between host actors")
 
-    # topological order over data FIFOs (delay-free cycles deadlock)
+    # Cycles (the analysis has rejected delay-free ones): an epoch of E
+    # iterations fires every actor's iterations in one launch, which is
+    # correct across a channel whose consumer at iteration n reads tokens the
+    # producer wrote at n - delay/rate when that lies in an earlier epoch.  So
+    # inside a strongly connected component every delayed channel caps the
+    # epoch at delay/rate iterations and drops out of the intra-epoch order.
+    comp = _components(g, data_fifos)
+    epoch_cap = None
+    loose: set[str] = set()       # channels not ordering the actors within an epoch
+    for fid in data_fifos:
+        f = g.fifo(fid)
+        if comp[f.src.actor] == comp[f.dst.actor] and f.delay and not f.delay % f.rate:
+            d = f.delay // f.rate
+            epoch_cap = d if epoch_cap is None else min(epoch_cap, d)
+            loose.add(fid)
+
+    # topological order over the ordering channels
     indeg = {a.id: 0 for a in g.actors}
     succ: dict[str, list[str]] = {a.id: [] for a in g.actors}
     for fid in data_fifos:
+        if fid in loose:
+            continue
         f = g.fifo(fid)
         succ[f.src.actor].append(f.dst.actor)
         indeg[f.dst.actor] += 1
@@ -211,21 +230,15 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
         ready.sort()
     if len(order) != len(g.actors):
         stuck = sorted(a for a, d in indeg.items() if d > 0)
-        unsupported.append(f"cycle through {stuck} (delay tokens)")
+        unsupported.append(f"cycle through {stuck} without delay tokens on every loop")
 
-    # every actor must fire exactly once per source firing: a consumer whose
-    # inputs all carry delay tokens would keep firing on them after the sources
-    # are exhausted (the reference drains them), which the batched iteration
-    # schedule does not model
-    if len(order) == len(g.actors):
-        extra: dict[str, int] = {}
-        for aid in order:
-            ins = [g.fifo(fid) for fid in data_fifos if g.fifo(fid).dst.actor == aid]
-            extra[aid] = min((extra[f.src.actor] + f.delay // f.rate for f in ins), default=0)
-            if extra[aid] > 0:
-                unsupported.append(f"actor {aid} would fire {extra[aid]} more times than the "
-                                   "sources on its inputs' delay tokens (drain phase)")
-                break
+    # Drain phase (runtime.py:118-124, interp.py:150-205): after the sources
+    # stop, an actor keeps firing while every input holds a firing's tokens,
+    # i.e. extra(a) = min over its inputs of extra(producer) + delay/rate
+    # (sources and configuration actors: 0) -- the shortest-path fixed point;
+    # None where no source bounds it (a sourceless cycle spins until the
+    # timeout, test_runtime.py:224-235).
+    extra = _drain_extra(g, data_fifos, control_fifos, roles)
 
     if unsupported:
         raise UnsupportedGraph("; ".join(unsupported))
@@ -240,7 +253,80 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
             eq1.append((a.id, p.id, port_cond[ref], fifo_cond[fid]))
 
     return ExecPlan(g, conds, {k: v for k, v in actor_cond.items()}, fifo_cond, order, roles,
-                    control_fifos, data_fifos, eq1, report)
+                    control_fifos, data_fifos, eq1, report, epoch_cap, extra, loose)
+
+
+def _components(g: Graph, data_fifos: list[str]) -> dict[str, int]:
+    """Strongly connected components over the data channels (Tarjan)."""
+    succ: dict[str, list[str]] = {a.id: [] for a in g.actors}
+    for fid in data_fifos:
+        f = g.fifo(fid)
+        succ[f.src.actor].append(f.dst.actor)
+    index: dict[str, int] = {}
+    low: dict[str, int] = {}
+    comp: dict[str, int] = {}
+    stack: list[str] = []
+    on: set[str] = set()
+    counter = [0, 0]
+
+    def visit(v: str) -> None:
+        work = [(v, iter(succ[v]))]
+        index[v] = low[v] = counter[0]
+        counter[0] += 1
+        stack.append(v)
+        on.add(v)
+        while work:
+            u, it = work[-1]
+            nxt = next(it, None)
+            if nxt is not None:
+                if nxt not in index:
+                    index[nxt] = low[nxt] = counter[0]
+                    counter[0] += 1
+                    stack.append(nxt)
+                    on.add(nxt)
+                    work.append((nxt, iter(succ[nxt])))
+                elif nxt in on:
+                    low[u] = min(low[u], index[nxt])
+                continue
+            work.pop()
+            if work:
+                low[work[-1][0]] = min(low[work[-1][0]], low[u])
+            if low[u] == index[u]:
+                while True:
+                    w = stack.pop()
+                    on.discard(w)
+                    comp[w] = counter[1]
+                    if w == u:
+                        break
+                counter[1] += 1
+
+    for a in g.actors:
+        if a.id not in index:
+            visit(a.id)
+    return comp
+
+
+def _drain_extra(g: Graph, data_fifos: list[str], control_fifos: list[str],
+                 roles: dict[str, str]) -> dict[str, int | None]:
+    """Firings after the sources stop, per actor (None: unbounded)."""
+    INF = float("inf")
+    extra = {a.id: (0 if roles[a.id] in ("source", "config") else INF) for a in g.actors}
+    ins: dict[str, list[tuple[str, int]]] = {a.id: [] for a in g.actors}
+    for fid in data_fifos + control_fifos:
+        f = g.fifo(fid)
+        ins[f.dst.actor].append((f.src.actor, f.delay // f.rate))
+    for _ in range(len(g.actors) + 1):
+        changed = False
+        for a in g.actors:
+            if not ins[a.id]:
+                continue
+            v = min(extra[p] + d for p, d in ins[a.id])
+            if v < extra[a.id]:
+                extra[a.id] = v
+                changed = True
+        if not changed:
+            break
+    return {k: (None if v == INF else int(v)) for k, v in extra.items()}
 
 
 def find_filter_banks(plan: ExecPlan, behaviors: dict[str, ActorBehavior]) -> list[FilterBankGroup]:

@@ -79,11 +79,18 @@ def test_custom_host_sink_sees_every_firing(tmp_path, golden):
     assert rep.sink_digests["sink"] == hashlib.sha256(arr["small_sink"].tobytes()).hexdigest()
 
 
-def test_host_behaviour_between_device_actors_is_unsupported(tmp_path):
+def test_host_behaviour_between_device_actors_fires_on_host(tmp_path):
+    """A pure host behaviour (no device kernel) between device actors fires
+    through the plugin API (tests/test_host_actors_gpu.py has the parity
+    cases); one without a fire method fails as ActorPanic like the
+    reference's ActorBehavior.fire (behavior.py:62-63)."""
+    from paper_1802_06625_b200 import ActorPanic
     from paper_1802_06625_b200.apps import predistortion as pd
-    with pytest.raises(UnsupportedGraph):
-        run(pd.build_description(256, 4, str(tmp_path / "x")), behaviors={"b1": Recorder()},
-            config=RuntimeConfig(source_firings=1))
+    p = tmp_path / "x"
+    p.write_bytes(pd.make_input(11, 2))
+    with pytest.raises(ActorPanic):
+        run(pd.build_description(256, 4, str(p), 4), behaviors={"b1": ActorBehavior()},
+            config=RuntimeConfig(source_firings=2))
 
 
 # ---------------------------------------------------------------- rings

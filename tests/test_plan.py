@@ -1,6 +1,8 @@
 """Admission (plan.admit) on the reference's graphs: conditions, rejections."""
 import json
 
+from conftest import GOLDEN
+
 import pytest
 
 from paper_1802_06625_b200 import InconsistentGraph, UnsupportedGraph, admit, as_graph
@@ -44,13 +46,15 @@ def test_eq1_mismatch_rejected():
 
 
 def test_data_delay_is_unsupported_not_wrong(golden):
-    """Delay tokens are admitted only on aligned channels between device
-    actors; others raise UnsupportedGraph instead of running wrong."""
+    """Delay tokens are admitted on aligned, always-active channels (also
+    from host producers); a delay that is not a multiple of the rate, or on a
+    dynamically gated channel, raises UnsupportedGraph instead of running
+    wrong."""
     desc = golden["fixtures"]["static_chain"]["description"]
     desc = json.loads(json.dumps(desc))
     desc["fifos"][0]["delay"] = 2          # source -> s1: a host producer
-    with pytest.raises(UnsupportedGraph, match="delay"):
-        admit(as_graph(desc))
+    p = admit(as_graph(desc))
+    assert p.extra["s1"] == 2 and p.extra["src"] == 0
     desc = json.loads(json.dumps(golden["fixtures"]["rate_pair_atr3"]["description"]))
     for f in desc["fifos"]:
         if f["rate"] == 3 and f["src"] != "src.out" and not f["dst"].startswith("sink"):
@@ -59,6 +63,12 @@ def test_data_delay_is_unsupported_not_wrong(golden):
     else:
         pytest.skip("no rate-3 device channel in the fixture")
     with pytest.raises(UnsupportedGraph, match="delay"):
+        admit(as_graph(desc))
+    desc = json.loads(json.dumps(golden["fixtures"]["gated_pipeline"]["description"]))
+    for f in desc["fifos"]:
+        if f["id"] == "f_m1":
+            f["delay"] = 1                 # x.d1 -> m1: gated by the control token
+    with pytest.raises((UnsupportedGraph, InconsistentGraph)):
         admit(as_graph(desc))
 
 
@@ -71,13 +81,26 @@ def test_device_delay_admitted(golden):
     assert p.roles["blur"] == p.roles["detect"] == p.roles["clean"] == "device"
 
 
-def test_delay_drain_phase_is_unsupported(golden):
-    """A consumer whose only input is delayed would fire on the delay tokens
-    after the sources stop (the reference drains them): not modelled."""
+def test_delay_drain_phase_and_cycles(golden):
+    """Firings after the sources stop (interp.py drain; test_interp.py:41-44)
+    per actor, and the epoch cap a delayed cycle imposes."""
     desc = json.loads(json.dumps(golden["fixtures"]["static_chain"]["description"]))
     desc["fifos"][1]["delay"] = 2          # s1 -> s2, both device actors
-    with pytest.raises(UnsupportedGraph, match="drain"):
-        admit(as_graph(desc))
+    p = admit(as_graph(desc))
+    assert p.extra == {"src": 0, "s1": 0, "s2": 2, "s3": 2, "sink": 2}
+    assert p.epoch_cap is None
+    d = json.loads((GOLDEN / "delays.json").read_text())
+    for key, case in d.items():
+        p = admit(as_graph(case["description"]))
+        if key == "two_cycle":
+            assert p.extra == {"a": None, "b": None} and p.epoch_cap == 1
+            continue
+        want = case["interpret"]["firing_counts"]
+        n = case["source_firings"]
+        assert {a: n + e for a, e in p.extra.items()} == want, key
+    p = admit(as_graph(d["fed_cycle_d4"]["description"]))
+    assert p.epoch_cap == 2 and p.loose == {"f_ba"}
+    assert p.order.index("a") < p.order.index("b")
 
 
 def test_zero_delay_cycle_deadlocks():
