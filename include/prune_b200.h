@@ -50,7 +50,8 @@ enum {
   PB_E_CUDA = -5,        /* device runtime failure */
   PB_E_NOMEM = -6,       /* allocation failure */
   PB_E_UNSUPPORTED = -7, /* shape the kernels do not cover */
-  PB_E_ACTOR = -8        /* an actor firing reported a failure (ActorPanic) */
+  PB_E_ACTOR = -8,       /* an actor firing reported a failure (ActorPanic) */
+  PB_E_TIMEOUT = -9      /* a blocking ring transfer timed out (Timeout) */
 };
 
 #define PB_TAPS 10          /* FIR taps, predistortion.py:24 (TAPS) */
@@ -130,6 +131,16 @@ int pb_ring_push_host(pb_ring* ring, int stream, const void* src, int64_t n_chun
  * PB_E_PROTOCOL when open and short (the reference would block). */
 int pb_ring_pop_host(pb_ring* ring, int stream, void* dst, int64_t n_chunks,
                      void* cuda_stream);
+/* Blocking variants (FifoChannel.write_start / read_start wait,
+ * fifos.py:223-323): wait until the gate opens, the ring closes (pop:
+ * PB_E_EOS when short) or is poisoned (PB_E_POISONED), or timeout_ms elapses
+ * (PB_E_TIMEOUT; timeout_ms < 0 waits without limit).  A push and a pop may
+ * run concurrently on different threads (single producer, single consumer
+ * per stream); every host transfer of a ring is serialised by its lock. */
+int pb_ring_push_host_wait(pb_ring* ring, int stream, const void* src, int64_t n_chunks,
+                           void* cuda_stream, int64_t timeout_ms);
+int pb_ring_pop_host_wait(pb_ring* ring, int stream, void* dst, int64_t n_chunks,
+                          void* cuda_stream, int64_t timeout_ms);
 int pb_ring_counters(const pb_ring* ring, int stream, int64_t* writes, int64_t* reads,
                      int64_t* max_occupancy);
 int pb_ring_close(pb_ring* ring);

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-from .errors import (ActorPanic, DeviceUnavailable, EndOfStream, InvalidParams, Poisoned,
+from .errors import (ActorPanic, DeviceUnavailable, EndOfStream, InvalidParams, Poisoned, Timeout,
                      ProtocolError, UnsupportedGraph)
 
 # PB_LIB_PATH selects an alternative build of the same library (profiling
@@ -27,6 +27,7 @@ PB_E_CUDA = -5
 PB_E_NOMEM = -6
 PB_E_UNSUPPORTED = -7
 PB_E_ACTOR = -8
+PB_E_TIMEOUT = -9
 
 PB_TAPS = 10
 PB_FIR_EXACT = 0
@@ -167,6 +168,8 @@ SIGNATURES = {
     "pb_ring_storage": (C.c_int, [vp, C.POINTER(vp), C.POINTER(i64), C.POINTER(vp)]),
     "pb_ring_push_host": (C.c_int, [vp, C.c_int, vp, i64, vp]),
     "pb_ring_pop_host": (C.c_int, [vp, C.c_int, vp, i64, vp]),
+    "pb_ring_push_host_wait": (C.c_int, [vp, C.c_int, vp, i64, vp, i64]),
+    "pb_ring_pop_host_wait": (C.c_int, [vp, C.c_int, vp, i64, vp, i64]),
     "pb_ring_counters": (C.c_int, [vp, C.c_int, C.POINTER(i64), C.POINTER(i64),
                                    C.POINTER(i64)]),
     "pb_ring_close": (C.c_int, [vp]),
@@ -242,6 +245,8 @@ def check(rc: int, what: str = "") -> int:
         raise UnsupportedGraph(text)
     if rc == PB_E_ACTOR:
         raise ActorPanic(what or "device", RuntimeError(text))
+    if rc == PB_E_TIMEOUT:
+        raise Timeout(None, [], text)
     raise DeviceUnavailable(text or f"libprune_b200 status {rc}")
 
 

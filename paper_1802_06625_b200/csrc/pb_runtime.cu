@@ -2,6 +2,8 @@
 // the Eq. 2 capacity plan (fifos.py:49-139) and device-resident rings
 // (FifoChannel, fifos.py:142-338).
 #include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -302,6 +304,12 @@ struct pb_ring {
   bool closed;
   std::string poisoned;
   bool is_poisoned;
+  // host-side transfers are single-producer / single-consumer across threads
+  // (FifoChannel's contract, fifos.py:142-160): one lock serialises the
+  // counter read-modify-write of a push and a pop, and the blocking variants
+  // wait on `cv` for space / tokens / close / poison
+  std::mutex mu;
+  std::condition_variable cv;
 };
 
 namespace {
@@ -430,9 +438,13 @@ static int check_stream(const pb_ring* r, int s) {
   return PB_OK;
 }
 
-// write_start/write_end for n chunks, fifos.py:223-269
-int pb_ring_push_host(pb_ring* ring, int stream, const void* src, int64_t n_chunks,
-                      void* cuda_stream) {
+namespace {
+constexpr int kWouldBlock = 1;   // internal: the gate is not open yet
+}
+
+// write_start/write_end for n chunks, fifos.py:223-269 (ring->mu held)
+static int push_locked(pb_ring* ring, int stream, const void* src, int64_t n_chunks,
+                       void* cuda_stream) {
   int rc = check_stream(ring, stream);
   if (rc) return rc;
   if (ring->closed) return fail(PB_E_PROTOCOL, "write after close");
@@ -445,11 +457,12 @@ int pb_ring_push_host(pb_ring* ring, int stream, const void* src, int64_t n_chun
   if (n_chunks == 0) return PB_OK;
   // the writer gate is monotone in w: the last chunk's gate bounds them all
   int64_t need = pb_writer_gate(c[C_WRITES] + n_chunks - 1, p.rate, p.delay, p.factor, p.aligned);
-  if (c[C_READS] < need)
-    return fail(PB_E_PROTOCOL, "write of " + std::to_string(n_chunks) +
-                                   " chunks would block: ring full (" +
-                                   std::to_string(c[C_READS]) + " reads done, " +
-                                   std::to_string(need) + " needed)");
+  if (c[C_READS] < need) {
+    fail(PB_E_PROTOCOL, "write of " + std::to_string(n_chunks) +
+                            " chunks would block: ring full (" + std::to_string(c[C_READS]) +
+                            " reads done, " + std::to_string(need) + " needed)");
+    return kWouldBlock;
+  }
   const uint8_t* h = static_cast<const uint8_t*>(src);
   uint8_t* base = ring->data + (int64_t)stream * p.nbytes;
   int64_t span = (int64_t)p.rate * p.token_bytes;
@@ -474,8 +487,9 @@ int pb_ring_push_host(pb_ring* ring, int stream, const void* src, int64_t n_chun
   return store_counters(ring, stream, c);
 }
 
-// read_start/read_end for n chunks, fifos.py:280-323
-int pb_ring_pop_host(pb_ring* ring, int stream, void* dst, int64_t n_chunks, void* cuda_stream) {
+// read_start/read_end for n chunks, fifos.py:280-323 (ring->mu held)
+static int pop_locked(pb_ring* ring, int stream, void* dst, int64_t n_chunks,
+                      void* cuda_stream) {
   int rc = check_stream(ring, stream);
   if (rc) return rc;
   if (n_chunks < 0) return fail(PB_E_INVALID, "negative chunk count");
@@ -492,7 +506,8 @@ int pb_ring_pop_host(pb_ring* ring, int stream, void* dst, int64_t n_chunks, voi
   if (n_chunks > 0 && c[C_WRITES] < pb_reader_gate(last, p.rate, p.delay)) {
     if (ring->closed)
       return fail(PB_E_EOS, "channel closed with fewer tokens than requested");
-    return fail(PB_E_PROTOCOL, "read would block: not enough tokens published");
+    fail(PB_E_PROTOCOL, "read would block: not enough tokens published");
+    return kWouldBlock;
   }
   for (int64_t k = 0; k < n_chunks; ++k) {
     int64_t i = c[C_READS];
@@ -501,7 +516,8 @@ int pb_ring_pop_host(pb_ring* ring, int stream, void* dst, int64_t n_chunks, voi
         rc = run_copy(ring, stream, c, st);
         if (rc) return rc;
       } else {
-        return fail(PB_E_PROTOCOL, "read would block: wrap copy not ready");
+        fail(PB_E_PROTOCOL, "read would block: wrap copy not ready");
+        return kWouldBlock;
       }
     }
     int64_t slot = p.aligned ? (i * p.rate) % p.slots : (i % p.factor) * p.rate;
@@ -513,9 +529,63 @@ int pb_ring_pop_host(pb_ring* ring, int stream, void* dst, int64_t n_chunks, voi
   return store_counters(ring, stream, c);
 }
 
+}  // extern "C"
+
+// one transfer attempt, or (timeout_ms != 0) wait until it can proceed, the
+// ring closes / is poisoned, or timeout_ms elapses (< 0: no limit)
+template <typename Op>
+static int transfer(pb_ring* ring, int64_t timeout_ms, Op op) {
+  if (!ring) return fail(PB_E_INVALID, "null ring");
+  std::unique_lock<std::mutex> lk(ring->mu);
+  const auto until = std::chrono::steady_clock::now() + std::chrono::milliseconds(timeout_ms);
+  for (;;) {
+    const int rc = op();
+    if (rc != kWouldBlock) {
+      if (rc == PB_OK) ring->cv.notify_all();
+      return rc;
+    }
+    if (timeout_ms == 0) return PB_E_PROTOCOL;
+    if (timeout_ms < 0) {
+      ring->cv.wait(lk);
+    } else if (ring->cv.wait_until(lk, until) == std::cv_status::timeout) {
+      const int again = op();   // a last look after the deadline
+      if (again != kWouldBlock) {
+        if (again == PB_OK) ring->cv.notify_all();
+        return again;
+      }
+      return fail(PB_E_TIMEOUT, "ring transfer timed out after " + std::to_string(timeout_ms) +
+                                    " ms");
+    }
+  }
+}
+
+extern "C" {
+
+int pb_ring_push_host(pb_ring* ring, int stream, const void* src, int64_t n_chunks,
+                      void* cuda_stream) {
+  return transfer(ring, 0, [&] { return push_locked(ring, stream, src, n_chunks, cuda_stream); });
+}
+
+int pb_ring_pop_host(pb_ring* ring, int stream, void* dst, int64_t n_chunks, void* cuda_stream) {
+  return transfer(ring, 0, [&] { return pop_locked(ring, stream, dst, n_chunks, cuda_stream); });
+}
+
+int pb_ring_push_host_wait(pb_ring* ring, int stream, const void* src, int64_t n_chunks,
+                           void* cuda_stream, int64_t timeout_ms) {
+  return transfer(ring, timeout_ms,
+                  [&] { return push_locked(ring, stream, src, n_chunks, cuda_stream); });
+}
+
+int pb_ring_pop_host_wait(pb_ring* ring, int stream, void* dst, int64_t n_chunks,
+                          void* cuda_stream, int64_t timeout_ms) {
+  return transfer(ring, timeout_ms,
+                  [&] { return pop_locked(ring, stream, dst, n_chunks, cuda_stream); });
+}
+
 int pb_ring_counters(const pb_ring* ring, int stream, int64_t* writes, int64_t* reads,
                      int64_t* max_occupancy) {
   if (!ring) return fail(PB_E_INVALID, "null ring");
+  std::lock_guard<std::mutex> lk(const_cast<pb_ring*>(ring)->mu);
   if (stream < 0 || stream >= ring->n_streams) return fail(PB_E_INVALID, "bad stream");
   int64_t c[C_N];
   int rc = load_counters(ring, stream, c);
@@ -528,14 +598,22 @@ int pb_ring_counters(const pb_ring* ring, int stream, int64_t* writes, int64_t* 
 
 int pb_ring_close(pb_ring* ring) {
   if (!ring) return fail(PB_E_INVALID, "null ring");
-  if (!ring->is_poisoned) ring->closed = true;
+  {
+    std::lock_guard<std::mutex> lk(ring->mu);
+    if (!ring->is_poisoned) ring->closed = true;
+  }
+  ring->cv.notify_all();
   return PB_OK;
 }
 
 int pb_ring_poison(pb_ring* ring, const char* reason) {
   if (!ring) return fail(PB_E_INVALID, "null ring");
-  ring->is_poisoned = true;
-  ring->poisoned = (reason && *reason) ? reason : "failure elsewhere in the graph";
+  {
+    std::lock_guard<std::mutex> lk(ring->mu);
+    ring->is_poisoned = true;
+    ring->poisoned = (reason && *reason) ? reason : "failure elsewhere in the graph";
+  }
+  ring->cv.notify_all();
   return PB_OK;
 }
 

@@ -60,9 +60,10 @@ class ActorPanic(ExecutionError):
 class Timeout(ExecutionError):
     """runtime.py:45 — the run exceeded RuntimeConfig.timeout_ms."""
 
-    def __init__(self, ms: float, alive: list[str]):
+    def __init__(self, ms: float | None, alive: list[str], message: str | None = None):
         self.alive = alive
-        super().__init__(f"run exceeded {ms:.0f} ms; still running: {', '.join(alive)}")
+        super().__init__(message or f"run exceeded {ms:.0f} ms; still running: "
+                                    f"{', '.join(alive)}")
 
 
 class UnsupportedGraph(ExecutionError):

@@ -160,6 +160,99 @@ def test_ring_preserves_the_stream(rate, delay, factor):
     lib.pb_ring_destroy(r)
 
 
+try:
+    from hypothesis import given, settings
+    from hypothesis import strategies as hst
+except ImportError:  # pragma: no cover
+    given = None
+
+
+def _concurrent_roundtrip(rate, delay, factor, token_bytes, n_chunks):
+    """test_fifo.py:335-373 on a device ring: a producer THREAD pushes chunks
+    with the blocking push (pb_ring_push_host_wait) and closes; this thread
+    pops with the blocking pop until EndOfStream.  The consumer sees the delay
+    payload and then exactly the produced tokens, in full spans."""
+    import ctypes as C
+    import threading
+    payload = bytes(range(100, 100 + delay * token_bytes))
+    lib, r = make_ring(rate, token_bytes, delay, factor, payload or None)
+    span = rate * token_bytes
+    chunks = [bytes((k * span + j) % 256 for j in range(span)) for k in range(n_chunks)]
+    errors = []
+
+    def produce():
+        try:
+            for c in chunks:
+                b = C.create_string_buffer(c, len(c))
+                rc = lib.pb_ring_push_host_wait(r, 0, b, 1, None, 10000)
+                if rc != 0:
+                    errors.append(("push", rc, _lib.error_text()))
+                    return
+        finally:
+            lib.pb_ring_close(r)
+
+    t = threading.Thread(target=produce, daemon=True)
+    t.start()
+    out = bytearray()
+    buf = C.create_string_buffer(span)
+    while True:
+        rc = lib.pb_ring_pop_host_wait(r, 0, buf, 1, None, 10000)
+        if rc == _lib.PB_E_EOS:
+            break
+        assert rc == 0, (rc, _lib.error_text())
+        out += buf.raw
+    t.join(10.0)
+    assert not errors, errors
+    stream = payload + b"".join(chunks)
+    full = (delay + n_chunks * rate) // rate
+    assert bytes(out) == stream[:full * span]
+    wr, rd, mx = C.c_int64(), C.c_int64(), C.c_int64()
+    lib.pb_ring_counters(r, 0, C.byref(wr), C.byref(rd), C.byref(mx))
+    p = _lib.Plan()
+    lib.pb_ring_plan(r, C.byref(p))
+    assert mx.value <= p.slots
+    lib.pb_ring_destroy(r)
+
+
+if given is not None:
+    @settings(max_examples=60, deadline=None)
+    @given(rate=hst.integers(1, 4), delay=hst.integers(0, 5), factor=hst.integers(2, 4),
+           token_bytes=hst.integers(1, 3), n_chunks=hst.integers(0, 20))
+    def test_concurrent_transfer_preserves_the_stream(rate, delay, factor, token_bytes,
+                                                      n_chunks):
+        _concurrent_roundtrip(rate, delay, factor, token_bytes, n_chunks)
+
+
+@pytest.mark.parametrize("args", [(2, 5, 2, 1), (2, 5, 2, 5), (3, 7, 2, 12), (2, 9, 3, 20),
+                                  (1, 0, 2, 200), (4, 4, 3, 64)])
+def test_concurrent_transfer_layouts(args):
+    """The layouts test_fifo.py:324-330 once deadlocked on, threaded."""
+    rate, delay, factor, n = args
+    _concurrent_roundtrip(rate, delay, factor, 2, n)
+
+
+def test_ring_blocking_timeout_and_poison():
+    import ctypes as C
+    import threading
+    lib, r = make_ring(1, 4, 0, 2)
+    b = C.create_string_buffer(4)
+    assert lib.pb_ring_pop_host_wait(r, 0, b, 1, None, 50) == _lib.PB_E_TIMEOUT
+    from paper_1802_06625_b200 import Timeout
+    with pytest.raises(Timeout):
+        _lib.check(lib.pb_ring_pop_host_wait(r, 0, b, 1, None, 20), "pop")
+    # a blocked consumer is released by poison
+    res = []
+    t = threading.Thread(target=lambda: res.append(lib.pb_ring_pop_host_wait(r, 0, b, 1, None,
+                                                                              -1)))
+    t.start()
+    import time
+    time.sleep(0.05)
+    lib.pb_ring_poison(r, b"upstream failure")
+    t.join(5.0)
+    assert res == [_lib.PB_E_POISONED]
+    lib.pb_ring_destroy(r)
+
+
 def test_ring_protocol_errors():
     lib, r = make_ring(1, 4, 0, 2)
     assert push(lib, r, b"aaaa") == 0 and push(lib, r, b"bbbb") == 0
