@@ -69,6 +69,10 @@ def parse():
     ap.add_argument("--cnn-steps", type=int, default=20)
     ap.add_argument("--cnn-e2e-steps", type=int, default=2)
     ap.add_argument("--cnn-cpu-frames", type=int, default=24)
+    ap.add_argument("--skip-mixed", action="store_true")
+    ap.add_argument("--mixed-streams", type=int, default=16, help="mixed-graph streams per GPU")
+    ap.add_argument("--mixed-iters", type=int, default=32, help="mixed-graph iterations")
+    ap.add_argument("--mixed-steps", type=int, default=20)
     return ap.parse_args()
 
 
@@ -574,6 +578,113 @@ def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
 
 # ------------------------------------------------------------------ our arm
 
+def mixed_leg(args, rank, world, local, barrier, max_over_ranks):
+    """BASELINE config 5: one heterogeneous graph (apps/mixed.py) holding the
+    DPD filter-bank region (subset_policy control, K=4, B=4096) and the
+    adaptive CNN (alternate_policy: every other 24-frame firing bypasses the
+    conv chain), two host configuration actors with dynamic rates, on
+    S streams x I iterations per GPU.  value: device-resident iterations/s
+    (with DPD stream-samples/s and CNN frames/s of the same steps); e2e:
+    run_all() from the caller's numpy arrays, both sinks D2H + SHA-256;
+    parity: stream 0 of both halves against the oracles."""
+    import ctypes as C
+
+    from oracle import cnn as oc
+    from oracle import dpd as od
+    from paper_1802_06625_b200 import RuntimeConfig, _lib
+    from paper_1802_06625_b200.apps import mixed, vision
+    from paper_1802_06625_b200.apps import predistortion as pd
+    from paper_1802_06625_b200.engine import DeviceRuntime
+
+    S, It, B, K, R = args.mixed_streams, args.mixed_iters, 4096, 4, CNN_FRAMES_PER_FIRING
+    streams = [rank * S + s for s in range(S)]
+    X = np.stack([pd.stream_input(s, It, B) for s in streams])
+    Fr = np.stack([vision.make_frames(100 + s, It * R) for s in streams])
+    desc = mixed.build_description(B, K, R)
+    rt = DeviceRuntime(desc, config=RuntimeConfig(source_firings=It, epoch=It, device=local,
+                                                  exact=False, capture_sinks=True),
+                       n_streams=S, seeds=[500 + s for s in streams],
+                       sources={"dpd_src": list(X), "cnn_src": list(Fr)})
+    lib = rt.lib
+    rt.reset()
+    rt.stage_sources(0, It)
+    rt.stage_control(0, It)
+    for _ in range(max(3, args.warmup)):
+        rt.fire_epoch(0, It)
+    _lib.check(lib.pb_stream_sync(rt.stream))
+
+    def ev():
+        e = C.c_void_p()
+        _lib.check(lib.pb_event_create(C.byref(e)))
+        return e.value
+    barrier()
+    n0 = lib.pb_launch_count()
+    e0, e1 = ev(), ev()
+    lib.pb_event_record(e0, rt.stream)
+    for _ in range(args.mixed_steps):
+        rt.fire_epoch(0, It)
+    lib.pb_event_record(e1, rt.stream)
+    _lib.check(lib.pb_stream_sync(rt.stream))
+    launches = lib.pb_launch_count() - n0
+    ms = C.c_float()
+    _lib.check(lib.pb_event_elapsed_ms(e0, e1, C.byref(ms)))
+    step_ms = max_over_ranks(ms.value / args.mixed_steps)
+    its = S * It * world / (step_ms / 1e3)
+    # end to end from the caller's arrays
+    times, reps = [], None
+    for k in range(3):
+        barrier()
+        t0 = time.perf_counter()
+        reps = rt.run_all()
+        t1 = time.perf_counter()
+        if k:
+            times.append(max_over_ranks(t1 - t0))
+    e2e_s = statistics.median(times)
+    parity = None
+    if rank == 0:
+        sets = od.subset_schedule(500, It, length=K, actor="dpd_conf")
+        want = od.dpd_stream(X[0], sets, K)
+        got = np.frombuffer(reps[0].sink_data["dpd_sink"], np.float32).reshape(want.shape)
+        dpd_err = float((np.abs(got - want) / np.maximum(1.0, np.abs(want))).max())
+        p = oc.graph_params(vision.build_description(R))
+        logits = np.frombuffer(reps[0].sink_data["cnn_sink"], np.float32).reshape(It, R, -1)
+        w = oc.forward(Fr[0][:R], p)["logits"]
+        cnn_err = float(np.abs(logits[0] - w).max())
+        bypass_ok = bool((logits[1] == np.float32(p["marker"])).all())
+        parity = {"dpd_max_rel_err": dpd_err, "cnn_max_abs_logit_err": cnn_err,
+                  "cnn_top1_equal": bool((logits[0].argmax(-1) == w.argmax(-1)).all()),
+                  "bypass_marker_exact": bypass_ok,
+                  "ok": dpd_err <= 1e-5 and cnn_err <= 1e-3 and bypass_ok,
+                  "checked": "stream 0: the DPD sink against oracle/dpd.py (tolerance mode, "
+                             "<= 1e-5), CNN firing 0 against oracle/cnn.py (<= 1e-3), "
+                             "firing 1's bypass marker"}
+    rt.close()
+    dpd_samples = S * It * B * world
+    frames = S * It * R * world
+    return {
+        "metric": "mixed-graph iterations/s (DPD block + 24-frame CNN firing per iteration, "
+                  "whole job)",
+        "value": its, "unit": "iterations/s", "ms_per_step": step_ms,
+        "steps": args.mixed_steps,
+        "dpd_msamples_per_s": dpd_samples / (step_ms / 1e3) / 1e6,
+        "cnn_frames_per_s": frames / (step_ms / 1e3),
+        "cnn_frames_processed_per_s": frames / 2 / (step_ms / 1e3),
+        "config": {"workload": f"C5 mixed graph: {S} streams/GPU x {It} iterations; per "
+                               f"iteration one {B}-sample DPD block (K={K}, subset_policy) and "
+                               f"one {R}-frame CNN firing (alternate_policy bypass)",
+                   "fir_math": "tolerance (PB_FIR_MERGED)"},
+        "e2e": {"value": S * It * world / e2e_s, "unit": "iterations/s",
+                "seconds_per_step": e2e_s,
+                "h2d_bytes_per_step": int(X.nbytes + Fr.nbytes),
+                "d2h_bytes_per_step": int(X.nbytes + S * It * R * vision.N_CLASSES * 4),
+                "includes": "DeviceRuntime.run_all() from the caller's numpy arrays: H2D, "
+                            "both native control actors, device firings, both sinks D2H + "
+                            "SHA-256"},
+        "gpu_launches": launches,
+        "parity_stream0": parity,
+    }
+
+
 def plumbing(args, rank, world, local, dist):
     """--plumbing: exercise the multi-rank launch path without a GPU (gloo):
     every rank reports its (rank, local rank, pid); rank 0 prints one line.
@@ -872,6 +983,12 @@ def main():
             rt.close()
             rt = None
         cnn = cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks)
+    mixed_res = None
+    if not args.skip_mixed:
+        if rt is not None:
+            rt.close()
+            rt = None
+        mixed_res = mixed_leg(args, rank, world, local, barrier, max_over_ranks)
 
     if rank == 0:
         line = {
@@ -911,6 +1028,7 @@ def main():
             "output_gather": gather,
             "cpu_baseline": cpu,
             "cnn": cnn,
+            "mixed": mixed_res,
         }
         print(json.dumps(line), flush=True)
     if rt is not None:
