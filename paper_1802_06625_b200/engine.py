@@ -283,8 +283,10 @@ class DeviceRuntime:
         self._allocate()
         self.launches, self.fir_groups = self._build_launches()
         self._build_tables()
+
         self._drain = None            # drain-phase launches, built on first use
         self._cond_now: dict[str, int] = {}   # condition overrides while draining
+        self.eq1_host = 0             # Eq. 1 checks counted without a launch
         self.launches_per_epoch = 0
 
     # ------------------------------------------------------------- allocation
@@ -717,7 +719,15 @@ class DeviceRuntime:
         dadv = [r for r, f in zip(adv, g.fifos) if plan.fifo_cond[f.id] == ALWAYS]
         self.drain_advance = (_lib.RingAdvance * max(1, len(dadv)))(*dadv)
         self.n_drain_advance = len(dadv)
-        eq = [_lib.Eq1Port(own, moved, ALWAYS, 0) for (_, _, own, moved) in plan.eq1_ports]
+        # Eq. 1 recheck (runtime.py:195-220) per DRP: the port's own control
+        # element vs the condition that moved its channel's tokens.  Where both
+        # are the same condition (every DRP whose channel the executor gates by
+        # that DRP's own control entry) the check cannot fail and counts one per
+        # firing of the (always-firing) dynamic actor: counted on the host, no
+        # launch.  The others run on the device (pb_epoch_close / pb_eq1_check).
+        eq = [_lib.Eq1Port(own, moved, ALWAYS, 0) for (_, _, own, moved) in plan.eq1_ports
+              if own != moved]
+        self.n_eq1_static = sum(1 for (_, _, own, moved) in plan.eq1_ports if own == moved)
         self.eq1 = (_lib.Eq1Port * max(1, len(eq)))(*eq)
         self.n_eq1 = len(eq)
 
@@ -1006,6 +1016,7 @@ class DeviceRuntime:
             _lib.check(lib.pb_resolve(conds, res, st), "pb_resolve")
         # the Eq. 1 recheck closes the epoch together with the ring advance
         # (pb_epoch_close: one launch); PB_EPOCH_CLOSE=0 keeps them apart
+        self.eq1_host += self.n_eq1_static * E * self.n_streams
         close = (self.n_eq1 <= 256 and len(self.advance) <= 256 and
                  os.environ.get("PB_EPOCH_CLOSE", "1") != "0")
         if self.n_eq1 and not close:
@@ -1257,6 +1268,7 @@ class DeviceRuntime:
         for aid, p in self.fir_state.items():
             _lib.check(lib.pb_memset(p, 0, S * 2 * 9 * 4, self.stream))
         _lib.check(lib.pb_memset(self.eq1_ctr, 0, 16, self.stream))
+        self.eq1_host = 0
         _lib.check(lib.pb_memset(self.err_flag, 0, 16, self.stream))
         for s in range(S):
             for a in g.actors:
@@ -1763,7 +1775,7 @@ class DeviceRuntime:
             reports.append(r)
         # Eq. 1 counters are device-wide; attribute them evenly per stream
         for r in reports:
-            r.eq1_checks = int(eq[0]) // S
+            r.eq1_checks = (int(eq[0]) + self.eq1_host) // S
             r.eq1_failures = int(eq[1]) // S
         return reports
 
