@@ -180,9 +180,11 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
         fifo_cond[fid] = cs
     for fid in control_fifos:
         fifo_cond[fid] = ALWAYS
-    # initial delay tokens on data FIFOs: supported on aligned, always-active
-    # channels (fifos.py:87-92): the producer side writes delay/rate chunks
-    # ahead of the consumer side, which first reads the delay payload
+    # initial delay tokens on data FIFOs: supported on aligned channels
+    # (fifos.py:87-92): the producer side writes delay/rate chunks ahead of the
+    # consumer side, which first reads the delay payload -- on a gated channel
+    # both sides index by the condition's firing count, so the consumer's k-th
+    # firing reads the producer's (k - delay/rate)-th
     for fid in data_fifos:
         f = g.fifo(fid)
         if not f.delay:
@@ -190,8 +192,6 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
         if f.delay % f.rate:
             unsupported.append(f"fifo {fid}: {f.delay} delay tokens are not a multiple of its "
                                f"rate {f.rate}")
-        elif fifo_cond[fid] != ALWAYS:
-            unsupported.append(f"fifo {fid}: delay tokens on a dynamically gated channel")
 
     # Cycles (the analysis has rejected delay-free ones): an epoch of E
     # iterations fires every actor's iterations in one launch, which is
@@ -239,6 +239,13 @@ def admit(g: Graph, c_factor: int = 3) -> ExecPlan:
     # None where no source bounds it (a sourceless cycle spins until the
     # timeout, test_runtime.py:224-235).
     extra = _drain_extra(g, data_fifos, control_fifos, roles)
+    for aid, e in extra.items():
+        if e and actor_cond[aid] != ALWAYS:
+            # a gated actor left with tokens after the sources stop; the
+            # reference engines disagree on it (the interpreter reports
+            # stranded tokens, the threaded runtime fires it once more)
+            unsupported.append(f"actor {aid} is dynamically gated and would fire on delay "
+                               "tokens after the sources stop")
 
     if unsupported:
         raise UnsupportedGraph("; ".join(unsupported))
@@ -383,6 +390,8 @@ def find_filter_banks(plan: ExecPlan, behaviors: dict[str, ActorBehavior]) -> li
             continue
         if len([p for p in y.output_ports]) != 1:
             continue
+        if any(g.fifo(fid).delay for fid in internal):
+            continue            # a delayed branch channel stays materialised
         spans = {g.fifo(fid).rate * g.fifo(fid).token_bytes for fid in internal}
         src = g.fifo_into(PortRef(x.id, x.data_inputs[0].id))
         if spans != {src.rate * src.token_bytes}:

@@ -121,8 +121,39 @@ def broadcast_delayed():
                        "token_bytes": 2}]}
 
 
+def gated(fid: str, delay: int, payload: str | None = None, builder=None):
+    """A reference fixture with initial tokens on one channel (gated or not)."""
+    desc = (builder or fx.gated_pipeline)()
+    for f in desc["fifos"]:
+        if f["id"] == fid:
+            f["delay"] = delay
+            if payload:
+                f["delay_payload_hex"] = payload
+    return desc
+
+
+def dpd_branch_delay(path: str):
+    """The reference DPD app (B=256, K=4) with one initial token on the
+    branch-2 -> combiner channel (a dynamically gated channel)."""
+    from tokenflow.apps import predistortion as rpd
+    desc = rpd.build_description(path)
+    for f in desc["fifos"]:
+        if f["id"] == "f_fir2":
+            f["delay"] = 1
+            # one 256-sample token of ordinary floats (a NaN payload would
+            # compare by its NaN bits, which differ between IEEE implementations)
+            import numpy as np
+            f["delay_payload_hex"] = np.linspace(-0.75, 0.5, 512, dtype=np.float32).tobytes().hex()
+    return desc
+
+
 def cases() -> dict[str, tuple[dict, int]]:
     return {
+        "gated_e1_d1": (gated("f_e1", 1), 6),
+        "gated_e2_d2_payload": (gated("f_e2", 2, "0a0b"), 9),
+        "gated_src_d1": (gated("f_src", 1), 6),
+        "gated_out_d1": (gated("f_out", 1), 6),
+        "rate_pair_b_d2": (gated("f_b", 2, None, lambda: fx.rate_pair(2)), 5),
         "chain_mid_d1": (chain(2, {1: 1}), 6),              # test_interp.py:41-44
         "chain_mid_d2": (chain(2, {1: 2}), 4),              # test_interp.py:56-60
         "chain3_mid_d2": (chain(3, {1: 2}), 20),            # test_interp.py:140
@@ -140,9 +171,18 @@ def cases() -> dict[str, tuple[dict, int]]:
 
 def main():
     out = {}
-    for name, (desc, n) in cases().items():
+    import tempfile
+    from tokenflow.apps import predistortion as rpd
+    td = tempfile.mkdtemp()
+    inp = Path(td) / "dpd.bin"
+    inp.write_bytes(rpd.make_input(11, 12))
+    all_cases = dict(cases())
+    all_cases["dpd_branch_delay"] = (dpd_branch_delay(str(inp)), 12)
+    for name, (desc, n) in all_cases.items():
         g = build_graph(copy.deepcopy(desc))
         rec = {"description": desc, "source_firings": n, "seed": 5}
+        if name == "dpd_branch_delay":
+            rec["input_hex"] = inp.read_bytes().hex()
         ref = interpret(g, source_firings=n, seed=5, capture_sinks=True)
         rec["interpret"] = {"sink_digests": ref.sink_digests,
                             "sink_data_hex": {k: v.hex() for k, v in ref.sink_data.items()},

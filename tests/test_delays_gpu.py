@@ -22,12 +22,24 @@ CASES = json.loads((GOLDEN / "delays.json").read_text())
 RUNNABLE = sorted(k for k in CASES if k != "two_cycle")
 
 
+def description(case, tmp_path):
+    """The case's graph; a file source reads the recorded input from tmp_path."""
+    desc = json.loads(json.dumps(case["description"]))
+    if "input_hex" in case:
+        p = tmp_path / "input.bin"
+        p.write_bytes(bytes.fromhex(case["input_hex"]))
+        for a in desc["actors"]:
+            if a.get("behavior") == "file_source":
+                a["params"]["path"] = str(p)
+    return desc
+
+
 @pytest.mark.parametrize("epoch", [4096, 1, 3])
 @pytest.mark.parametrize("key", RUNNABLE)
-def test_delay_graph_matches_reference(key, epoch):
+def test_delay_graph_matches_reference(key, epoch, tmp_path):
     case = CASES[key]
     want = case["interpret"]
-    rep = run(case["description"], config=RuntimeConfig(
+    rep = run(description(case, tmp_path), config=RuntimeConfig(
         source_firings=case["source_firings"], seed=case["seed"], capture_sinks=True,
         epoch=epoch))
     assert rep.firing_counts == want["firing_counts"]
@@ -40,7 +52,27 @@ def test_delay_graph_matches_reference(key, epoch):
         assert rep.device_max_occupancy[fid] <= rep.device_slots[fid], fid
 
 
-@pytest.mark.parametrize("key", ["chain_all_d", "feedback_d2_payload", "fed_cycle", "bcast_delay"])
+@pytest.mark.parametrize("exact", [True, False])
+def test_dpd_with_delayed_branch_channel(exact, tmp_path):
+    """A delay on a gated branch channel of the DPD app keeps that region out
+    of the fused bank (its channel is materialised); bit-exact in the exact
+    mode, within 1e-5 in the tolerance mode."""
+    import numpy as np
+    case = CASES["dpd_branch_delay"]
+    rep = run(description(case, tmp_path), config=RuntimeConfig(
+        source_firings=case["source_firings"], seed=case["seed"], capture_sinks=True,
+        exact=exact))
+    assert rep.firing_counts == case["interpret"]["firing_counts"]
+    want = np.frombuffer(bytes.fromhex(case["interpret"]["sink_data_hex"]["sink"]), np.float32)
+    got = np.frombuffer(rep.sink_data["sink"], np.float32)
+    if exact:
+        assert rep.sink_digests == case["interpret"]["sink_digests"]
+    else:
+        assert (np.abs(got - want) / np.maximum(1.0, np.abs(want))).max() <= 1e-5
+
+
+@pytest.mark.parametrize("key", ["chain_all_d", "feedback_d2_payload", "fed_cycle", "bcast_delay",
+                                 "gated_e2_d2_payload", "rate_pair_b_d2"])
 def test_delay_graph_streams(key):
     case = CASES[key]
     S = 5
