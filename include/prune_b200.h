@@ -374,7 +374,20 @@ typedef struct {
   int32_t debug;           /* 0; profiling only: bit0 skip patch fill, bit1 skip
                               epilogue, bit2 skip MMAs, bit3 skip the layer-1 raw
                               TMA loads (results are garbage) */
+  int32_t math;            /* PB_CONV_BF16X3 or PB_CONV_I8 (cin 32 only; other
+                              shapes run bf16x3 whatever this says) */
+  const void* weights_i8;  /* PB_CONV_I8: cnn_weights.conv_device_layout_i8 (per
+                              K-step a 64-row [w0 0; w1 w0] int8 operand, then
+                              32 float dequantisation factors); may be NULL
+                              when math is PB_CONV_BF16X3 */
+  float* absmax_out;       /* NULL, or [live frames] max |output| of every
+                              output frame of this launch (in live-firing order;
+                              feeds the next conv's int8 quantisation) */
+  const float* absmax_in;  /* NULL, or the producer launch's absmax_out for
+                              this launch's input frames (same condition, same
+                              live firings); NULL: computed by a pre-pass */
 } pb_conv_actor;
+enum { PB_CONV_BF16X3 = 0, PB_CONV_I8 = 1 };
 int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream);
 /* Profiling builds (-DPB_CONV_PROF=1) only: per-CTA role timing counters of
  * conv_pool_kernel, uint64 [160][16] clock cycles (slots in csrc/pb_cnn.cu);

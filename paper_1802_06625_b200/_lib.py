@@ -34,6 +34,8 @@ PB_FIR_EXACT = 0
 PB_FIR_EXACT_PAIRED = 1
 PB_FIR_FMA = 2
 PB_FIR_MERGED = 3
+PB_CONV_BF16X3 = 0
+PB_CONV_I8 = 1
 PB_MAX_BRANCHES = 32
 PB_MAX_PORTS = 16
 PB_POLICY_STATE_BYTES = 2560
@@ -112,7 +114,8 @@ PB_IMG_BLUR, PB_IMG_DIFF, PB_IMG_MEDIAN = 0, 1, 2
 class ConvActor(C.Structure):
     _fields_ = [("in_", SpanRef), ("out", SpanRef), ("weights", vp), ("bias", vp),
                 ("frames", i32), ("h", i32), ("w", i32), ("cin", i32), ("cout", i32),
-                ("pad", i32), ("cond", i32), ("debug", i32)]
+                ("pad", i32), ("cond", i32), ("debug", i32), ("math", i32),
+                ("weights_i8", vp), ("absmax_out", vp), ("absmax_in", vp)]
 
 
 class DenseActor(C.Structure):

@@ -99,3 +99,81 @@ def dense_device_layout(w: np.ndarray) -> np.ndarray:
     S = nin // 16
     core = bits.reshape(2 * DENSE_N // 8, 8, S, 2, 8).transpose(2, 0, 3, 1, 4)
     return np.ascontiguousarray(core).reshape(-1)
+
+
+# int8-limb layer (csrc/pb_conv_rows.cu, RowCfg<32, true>): quantisation ranges
+X_LIMIT = 32639   # |X| of an activation (per frame: X = rint(x * 32639 / max|x|))
+W_LIMIT = 32511   # |W| of a weight (per output channel: W = rint(w / wdq))
+
+
+def limbs(v: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Signed 16-bit integers -> (h, l), v = 256 h + l, both in [-128, 127]."""
+    v = np.asarray(v, np.int64)
+    h = (v + 128) >> 8
+    return h, v - 256 * h
+
+
+def conv_quant_weights(w: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """W[cout][K] -> (integer weights [cout][K] with |W| <= W_LIMIT, the float32
+    per-channel dequantisation factors wdq = max|w| / W_LIMIT)."""
+    w = np.asarray(w, np.float32)
+    wdq = (np.abs(w).max(axis=1) / np.float32(W_LIMIT)).astype(np.float32)
+    scale = np.where(wdq > 0, 1.0 / np.maximum(wdq.astype(np.float64), 1e-300), 0.0)
+    q = np.rint(w.astype(np.float64) * scale[:, None]).astype(np.int64)
+    return np.clip(q, -W_LIMIT, W_LIMIT), wdq
+
+
+def conv_device_layout_i8(w: np.ndarray, cin: int) -> np.ndarray:
+    """The int8-limb layer's weights (cin = 32): per 16-channel K-step (ky, kx,
+    half) a 2 KB UMMA B operand of 64 rows x 32 int8 -- rows 0-31 [wh | 0] (the
+    "hi" accumulator columns), rows 32-63 [wl | wh] ("mid") -- against the A
+    operand [xh | xl], in the K-major no-swizzle core layout
+    [row/8][kblock][row%8][16]; then the 32 float32 factors wdq.  As uint8."""
+    if cin % 16:
+        raise ValueError("conv int8 limbs: Cin must be a multiple of 16")
+    q, wdq = conv_quant_weights(w)
+    steps = conv_steps(q.astype(np.float32), cin).astype(np.int64)   # [S][32][16] exact
+    wh, wl = limbs(steps)
+    S, cout = steps.shape[0], steps.shape[1]
+    rows = np.zeros((S, 2 * cout, 32), np.int8)
+    rows[:, :cout, :16] = wh
+    rows[:, cout:, :16] = wl
+    rows[:, cout:, 16:] = wh
+    core = rows.reshape(S, 2 * cout // 8, 8, 2, 16).transpose(0, 1, 3, 2, 4)
+    return np.concatenate([np.ascontiguousarray(core).reshape(-1).view(np.uint8),
+                           wdq.view(np.uint8)])
+
+
+def conv_i8_reference(x: np.ndarray, w: np.ndarray, b: np.ndarray, pad: int) -> np.ndarray:
+    """The int8-limb layer's arithmetic on the CPU (float64 where the device
+    sums exactly in s32): per frame X = rint(x * q), q = X_LIMIT / max|x| in
+    float32 and the product exact (the kernel's FFMA rounding), limbs of X
+    and of the quantised weights, hi = sum xh wh, mid = sum (xh wl + xl wh),
+    y = (256 hi + mid) * 256 * max|x| / X_LIMIT * wdq, bias, ReLU, 2x2 max."""
+    F, H, W, Cin = x.shape
+    x = np.asarray(x, np.float32)
+    mx = np.abs(x.reshape(F, -1)).max(axis=1).astype(np.float32)
+    q = np.where(mx > 0, np.float32(X_LIMIT) / np.maximum(mx, np.float32(1e-30)),
+                 np.float32(0)).astype(np.float32)
+    # the device rounds the exact product (one FFMA into a 2^23 magic number)
+    X = np.rint(x.astype(np.float64) * q.astype(np.float64)[:, None, None, None]).astype(np.int64)
+    xh, xl = limbs(X)
+    qw, wdq = conv_quant_weights(w)
+    wh, wl = limbs(qw)
+    Ho, Wo = H + 2 * pad - 4, W + 2 * pad - 4
+
+    def cols(a):
+        ap = np.pad(a.astype(np.float64), ((0, 0), (pad, pad), (pad, pad), (0, 0)))
+        c = np.empty((F, Ho, Wo, 25 * Cin))
+        for ky in range(5):
+            for kx in range(5):
+                t = ky * 5 + kx
+                c[..., t * Cin:(t + 1) * Cin] = ap[:, ky:ky + Ho, kx:kx + Wo, :]
+        return c
+    ch, cl = cols(xh), cols(xl)
+    hi = ch @ wh.T.astype(np.float64)
+    mid = ch @ wl.T.astype(np.float64) + cl @ wh.T.astype(np.float64)
+    xdq = (mx.astype(np.float64) * (256.0 / X_LIMIT))[:, None, None, None]
+    y = (256.0 * hi + mid) * xdq * wdq.astype(np.float64)
+    y = np.maximum(y + b, 0.0)
+    return y.reshape(F, Ho // 2, 2, Wo // 2, 2, -1).max(axis=(2, 4))

@@ -1413,12 +1413,16 @@ int pb_fire_conv_pool(pb_conv_actor actor, pb_resolved res, void* stream) {
     const int rc = pb::fire_conv_rows(actor, res, st, sms);
     if (rc != 1) return rc;   // 1: shape declined by the row kernel, use the tile kernel
   }
+  int rc;
   switch (actor.cin) {
-    case 3: return launch_conv<0, 3>(actor, res, st, sms);
-    case 16: return launch_conv<1, 16>(actor, res, st, sms);
-    case 32: return launch_conv<1, 32>(actor, res, st, sms);
+    case 3: rc = launch_conv<0, 3>(actor, res, st, sms); break;
+    case 16: rc = launch_conv<1, 16>(actor, res, st, sms); break;
+    case 32: rc = launch_conv<1, 32>(actor, res, st, sms); break;
     default: return pb::fail(PB_E_UNSUPPORTED, "conv: Cin must be 3, 16 or 32");
   }
+  // the tile kernel does not record its output scale: a separate pass
+  if (rc == PB_OK && actor.absmax_out) rc = pb::conv_absmax_out(actor, res, st);
+  return rc;
 }
 
 int pb_fire_dense(pb_dense_actor actor, pb_resolved res, void* stream) {

@@ -24,7 +24,7 @@ void count_launch(int n = 1);
 constexpr int kMaxDevices = 16;
 int device();   // current device ordinal, < kMaxDevices, or -1 on error (pb_last_error set)
 enum ScratchSlot { kScratchBankPlan = 0, kScratchConvUnits, kScratchDensePartial,
-                   kScratchDenseCounters, kScratchConvRows, kScratchSlots };
+                   kScratchDenseCounters, kScratchConvRows, kScratchConvAbsmax, kScratchSlots };
 // at least `bytes` of device memory for `slot` on the current device; newly
 // allocated memory is zeroed on `st` when zero_new
 int scratch(int slot, size_t bytes, void** out, bool zero_new = false, cudaStream_t st = 0);
@@ -34,6 +34,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // the row-streaming conv kernel with A in TMEM (pb_conv_rows.cu); Cin 3 / 32;
 // returns 1 without launching when it does not handle the shape
 int fire_conv_rows(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t st, int sms);
+int conv_absmax_out(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t st);
 
 }  // namespace pb
 

@@ -73,6 +73,18 @@ __device__ __forceinline__ uint64_t s_desc(uint32_t addr, uint32_t lbo, uint32_t
 __host__ __device__ constexpr uint32_t i_desc(int n) {   // bf16 x bf16 -> f32, M = 128
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | (128u >> 4 << 24);
 }
+// int8 limbs: s8 x s8 -> s32, M = 128 (tools/i8_probe.cu: exact, and an N = 64,
+// K = 32 MMA issues in the 34.7 cycles of an N = 64, K = 16 bf16 one)
+__host__ __device__ constexpr uint32_t i_desc_i8(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | (128u >> 4 << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint32_t a, uint64_t b, uint32_t id,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(id), "r"(acc));
+}
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t id,
                                        uint32_t acc) {
   asm volatile(
@@ -119,6 +131,21 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&w)[8])
                "r"(w[7])
                : "memory");
 }
+__device__ __forceinline__ void tmem_ld16i(uint32_t taddr, int (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32z(uint32_t taddr) {   // 32 zero columns
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(0u)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
   asm volatile(
@@ -153,6 +180,25 @@ __device__ __forceinline__ void split16(const float (&v)[16], uint32_t (&hi)[8],
   }
 }
 
+// int8 limbs of 16 values: X = rint(v * q) (q = 32639 / max |v| of the frame,
+// so |X| <= 32639) as X = 256 h + l with h = (X + 128) >> 8 and l in
+// [-128, 127].  One FFMA per value: v * q + (1.5 * 2^23 + 128) rounds the
+// exact product to the nearest integer (ties to even) into the low mantissa
+// bits, whose low 16 bits are Y = X + 128: h is byte 1 of Y, l is byte 0 of Y
+// with its top bit flipped.  Words 0-3 carry h (K bytes 0-15), words 4-7 l.
+__device__ __forceinline__ void quant16(const float (&v)[16], float q, uint32_t (&w)[8]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t y[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) y[b] = __float_as_uint(fmaf(v[4 * j + b], q, 12583040.f));
+    const uint32_t p0 = __byte_perm(y[0], y[1], 0x5140);   // y0.b0 y1.b0 y0.b1 y1.b1
+    const uint32_t p1 = __byte_perm(y[2], y[3], 0x5140);
+    w[j] = __byte_perm(p0, p1, 0x7632);                     // byte 1 of y0..y3: h
+    w[4 + j] = __byte_perm(p0, p1, 0x5410) ^ 0x80808080u;   // byte 0 flipped: l
+  }
+}
+
 // role timing for experiments (pb_conv_actor.debug bit 4): cycles spent
 // waiting per barrier kind, printed by CTA 0 at the end
 struct WaitClock {
@@ -162,22 +208,32 @@ struct WaitClock {
   __device__ __forceinline__ void stop() { if (on) acc += clock64() - t0; }
 };
 
-template <int CIN>
+// I8 (layer 2 only): int8 limbs instead of bf16x3.  x = (256 xh + xl) / qx
+// per frame, w = (256 wh + wl) / qw per output channel; per 16 input channels
+// ONE N = 64, K = 32 MMA with A = [xh | xl] and B = [wh 0; wl wh] gives the
+// row's "hi" columns (xh wh) and "mid" columns (xh wl + xl wh); the epilogue
+// dequantises (256 hi + mid) * 256 / (qx qw).  Each output row then owns 64
+// accumulator columns (a pair 128) and a chunk of A 8 columns.
+template <int CIN, bool I8 = false>
 struct RowCfg {
+  static_assert(!I8 || CIN == 32, "int8 limbs: layer 2 only");
   static constexpr int KC = CIN == 3 ? 1 : 5 * CIN / 16;   // K16 chunks per input row
   static constexpr int STEPS = 5 * KC;                     // weight K-steps (kernel row, chunk)
-  static constexpr int WBYTES = STEPS * 64 * 16 * 2;       // [wh; wl] per K-step
+  static constexpr int WBYTES = STEPS * 64 * 16 * 2;       // [wh; wl] (I8: [wh 0; wl wh]) per K-step
+  static constexpr int PAIR_COLS = I8 ? 128 : kPairCols;   // accumulator columns of a row pair
+  static constexpr int ROW_COLS = PAIR_COLS / 2;
+  static constexpr int CHUNK_COLS = I8 ? 8 : 16;           // A columns of one K chunk
   // a step: layer 1 two input rows, layer 2 one channel half of one row
   static constexpr int STEP_ROWS = CIN == 3 ? 4 : 1;
   static constexpr int STEP_CHUNKS = CIN == 3 ? 4 : 5;
-  static constexpr int STEP_COLS = STEP_CHUNKS * 16;       // hi 8 + lo 8 columns per chunk
+  static constexpr int STEP_COLS = STEP_CHUNKS * CHUNK_COLS;
   // TMEM: PAIRS accumulator slots, then a ring of RING A steps.  Layer 1
   // (a step feeds 4 pairs) keeps two pairs of slack for the epilogue.
 #ifndef PB_ROWS_PAIRS1
 #define PB_ROWS_PAIRS1 6
 #endif
-  static constexpr int PAIRS = CIN == 3 ? PB_ROWS_PAIRS1 : 4;
-  static constexpr int A0 = PAIRS * kPairCols;             // first A-ring column
+  static constexpr int PAIRS = CIN == 3 ? PB_ROWS_PAIRS1 : (I8 ? 3 : 4);
+  static constexpr int A0 = PAIRS * PAIR_COLS;             // first A-ring column
   static constexpr int RING = (512 - A0) / STEP_COLS;     // A steps in flight
 #ifndef PB_ROWS_GROUPS1
 #define PB_ROWS_GROUPS1 2
@@ -199,7 +255,12 @@ struct RowCfg {
 #endif
   static constexpr int EPI = CIN == 3 ? PB_ROWS_EPI1 : 1;
   static constexpr int CVT0 = 1 + 4 * EPI;                 // first converter warp
-  static constexpr int THREADS = (CVT0 + 4 * GROUPS + LOADER) * 32;
+  // I8: a second MMA warp (the last) issues the channel-half-1 steps while
+  // warp 0 issues the half-0 steps, so one warp's per-step bookkeeping runs
+  // while the other's MMAs keep the tensor pipe busy (integer sums: the
+  // interleaving cannot change a result)
+  static constexpr int MMA2 = I8 ? CVT0 + 4 * GROUPS + LOADER : -1;
+  static constexpr int THREADS = (CVT0 + 4 * GROUPS + LOADER + (I8 ? 1 : 0)) * 32;
   static_assert(RING >= 2, "TMEM budget");
 };
 
@@ -244,6 +305,9 @@ conv_rows_units_kernel(pb_conv_actor a, pb_resolved res, LiveSpan* list, int* n_
   cnt[s] = c;
   __syncthreads();
   if (s == 0) *n_live = total;
+  // this launch's per-frame max |output| starts at 0 (the epilogue's atomicMax)
+  if (a.absmax_out)
+    for (int f = s; f < total * a.frames; f += kUnitsThreads) a.absmax_out[f] = 0.f;
   const int n_units = res.n_streams * res.n_iter;
   for (int u = s; u < n_units; u += kUnitsThreads) {
     const int st = u / res.n_iter, j = u - st * res.n_iter;
@@ -272,6 +336,7 @@ struct RowBars {
   int pre_sig;
   uint32_t tmem_base;
   float bias[kCoutR];
+  float wdq[kCoutR];   // I8: per output channel dequantisation factor max|w| / 32511
 };
 
 struct RowGeom {
@@ -294,7 +359,7 @@ __device__ __forceinline__ RowGeom row_geom(const pb_conv_actor& a, int n_live, 
 struct LaneFrame {
   const float* in;
   float* out;
-  int xo;
+  int xo, fr;   // column in the frame, live frame index (virtual image order)
   bool valid;
 };
 __device__ __forceinline__ LaneFrame lane_frame(const RowGeom& g, const LiveSpan* list, int t,
@@ -303,6 +368,7 @@ __device__ __forceinline__ LaneFrame lane_frame(const RowGeom& g, const LiveSpan
   const int64_t v = (int64_t)t * 128 + m;
   const int fr = (int)(v / g.Wo);
   f.xo = (int)(v - (int64_t)fr * g.Wo);
+  f.fr = fr;
   f.valid = fr < g.frames;
   f.in = nullptr;
   f.out = nullptr;
@@ -327,11 +393,12 @@ __device__ __forceinline__ int step_wk(int s, int i) {   // weight K-step of chu
   return CIN == 3 ? 0 : 2 * i + (s & 1);
 }
 
-template <int CIN>
-__global__ void __launch_bounds__(RowCfg<CIN>::THREADS, 1)
+// absmax: I8, per live input frame max |x| (the quantisation scale)
+template <int CIN, bool I8>
+__global__ void __launch_bounds__(RowCfg<CIN, I8>::THREADS, 1)
 conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
-                 const int* __restrict__ n_live_p) {
-  using Cfg = RowCfg<CIN>;
+                 const int* __restrict__ n_live_p, const float* __restrict__ absmax) {
+  using Cfg = RowCfg<CIN, I8>;
   constexpr int RING = Cfg::RING;
   constexpr int kPairSlots = Cfg::PAIRS;
   constexpr int kA0 = Cfg::A0;
@@ -356,7 +423,7 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
       bar_init(&B.a_empty[i], 1);
     }
     for (int i = 0; i < kPairSlots; ++i) {
-      bar_init(&B.acc_full[i], 1);
+      bar_init(&B.acc_full[i], I8 ? 2 : 1);
       bar_init(&B.acc_empty[i], 4);
     }
     bar_init(&B.w_full, 1);
@@ -366,7 +433,13 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  if (threadIdx.x < kCoutR) B.bias[threadIdx.x] = a.bias[threadIdx.x];
+  if (threadIdx.x < kCoutR) {
+    B.bias[threadIdx.x] = a.bias[threadIdx.x];
+    if (I8)
+      B.wdq[threadIdx.x] =
+          reinterpret_cast<const float*>(static_cast<const uint8_t*>(a.weights_i8) +
+                                         Cfg::WBYTES)[threadIdx.x];
+  }
   if (threadIdx.x == 32) {
     // the MMA warp's commit points: before the first row, after every step
     // (layer 2: every row), after the last row
@@ -404,6 +477,20 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = B.tmem_base;
+  if constexpr (I8) {
+    // every MMA accumulates (two warps issue into the same rows in either
+    // order): the accumulators start at zero and the epilogue re-zeroes a
+    // pair's columns when it releases the slot
+    if (warp >= 1 && warp < 5) {
+      const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int col = 0; col < Cfg::A0; col += 8)
+        tmem_st8(tmem + ((uint32_t)((warp & 3) * 32) << 16) + col, z);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
   const bool prof = (a.debug & 16) && blockIdx.x == 0;
   const long long t_begin = clock64();
   WaitClock w1{prof, 0, 0}, w2{prof, 0, 0}, w3{prof, 0, 0}, w4{prof, 0, 0};
@@ -413,14 +500,17 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
   auto has_data = [&](int o) { return max(o, g.pad) <= min(o + 4, y_last); };
   auto pair_done_after = [&](int p) { return min(2 * p + 5, y_last); };
 
-  if (warp == 0) {
+  if (warp == 0 || warp == Cfg::MMA2) {
     // ------------------------------------------------------------ MMA issue
     // A warp-uniform loop (every lane waits on the barriers); one elected lane
     // issues each step's MMAs and the commits: tcgen05 instructions from a
     // diverged single thread issue ~3x slower (tools/tmem_a_probe.cu).
-    if (elect_one()) {
+    // I8: warp 0 takes the steps of channel half 0, warp MMA2 half 1; both
+    // commit every batch (acc_full counts two arrivals).
+    const int mw = warp == 0 ? 0 : 1;
+    if (warp == 0 && elect_one()) {
       bar_expect_tx(&B.w_full, Cfg::WBYTES);
-      const uint8_t* wsrc = static_cast<const uint8_t*>(a.weights);
+      const uint8_t* wsrc = static_cast<const uint8_t*>(I8 ? a.weights_i8 : a.weights);
       for (int off = 0; off < Cfg::WBYTES; off += 16384)
         bulk_load(wsm + off, wsrc + off, min(16384, Cfg::WBYTES - off), &B.w_full);
     }
@@ -461,7 +551,30 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
       for (int st = 0; st < n_steps; ++st, ++c) {
         const int rp_hi = step_row<CIN>(st, Cfg::STEP_ROWS - 1) + g.pad;
         const bool batch_after = info & 0x8000;
-        acquire_to((int)(info & 0x7FFF));   // pairs this step writes or completes
+        if (I8 && (st & 1) != mw) {
+          // the other MMA warp's step: this warp only joins its batch commit
+          // (which covers this warp's MMAs of the same input row)
+          if (batch_after) {
+            if (elect_one()) commit(&B.acc_full[kbase % kPairSlots]);
+            __syncwarp();
+            ++kbase;
+            while (sig < n_pairs && pair_done_after(sig) <= rp_hi) ++sig;
+          }
+          info = B.step_info[min(st + 1, n_steps - 1)];
+          continue;
+        }
+        const int rp0 = step_row<CIN>(st, 0) + g.pad;
+        // interior step: every (chunk, dy) feeds a row inside the output
+        // whose first contribution is its dy = 0 MMA -- straight-line issue
+        // with the accumulator columns precomputed per step
+        const bool interior = rp0 - 4 >= g.pad && rp0 - 4 >= 0 &&
+                              step_row<CIN>(st, Cfg::STEP_ROWS - 1) + g.pad < g.Ho && run_mma;
+        // I8 (3 pair slots): an interior step issues its dy = 4..1 MMAs
+        // (rows in pairs already held) before it waits for the slot of a
+        // pair its newest row opens, so the epilogue drains that slot
+        // behind them instead of in front
+        if (I8 && interior) acquire_to(min((int)(info & 0x7FFF), (rp0 - 1) >> 1));
+        else acquire_to((int)(info & 0x7FFF));   // pairs this step writes or completes
         const uint32_t next_info = B.step_info[min(st + 1, n_steps - 1)];
         const uint32_t kb = kbase % kPairSlots;
         const uint32_t slot = c % RING;
@@ -470,12 +583,6 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
         w2.stop();
         asm volatile("tcgen05.fence::after_thread_sync;");
         w3.start();
-        const int rp0 = step_row<CIN>(st, 0) + g.pad;
-        // interior step: every (chunk, dy) feeds a row inside the output
-        // whose first contribution is its dy = 0 MMA -- straight-line issue
-        // with the accumulator columns precomputed per step
-        const bool interior = rp0 - 4 >= g.pad && rp0 - 4 >= 0 &&
-                              step_row<CIN>(st, Cfg::STEP_ROWS - 1) + g.pad < g.Ho && run_mma;
         if (interior) {
           constexpr int NR = Cfg::STEP_ROWS;
           // rows o_min .. o_min + NR + 3 span pairs pmin .. pmin + (NR + 5) / 2:
@@ -487,7 +594,7 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
           uint32_t sl = (pbase + (uint32_t)(o_min >> 1)) % kPairSlots;
 #pragma unroll
           for (int k = 0; k < NB; ++k) {
-            base[k] = tmem + sl * kPairCols;
+            base[k] = tmem + sl * Cfg::PAIR_COLS;
             sl = sl + 1 == kPairSlots ? 0 : sl + 1;
           }
           uint32_t dcol[NR][5];
@@ -496,13 +603,35 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
 #pragma unroll
             for (int dy = 0; dy < 5; ++dy) {
               const int rel = 4 + r - dy;   // o - o_min, compile-time
-              dcol[r][dy] = odd ? base[(rel + 1) >> 1] + ((rel + 1) & 1) * 32
-                                : base[rel >> 1] + (rel & 1) * 32;
+              dcol[r][dy] = odd ? base[(rel + 1) >> 1] + ((rel + 1) & 1) * Cfg::ROW_COLS
+                                : base[rel >> 1] + (rel & 1) * Cfg::ROW_COLS;
             }
           const uint32_t abase = tmem + kA0 + slot * Cfg::STEP_COLS;
           const uint64_t bstep = bd0 + (uint64_t)((step_wk<CIN>(st, 0) * 2048) >> 4);
           const bool lead = CIN == 3 || (st & 1) == 0;
-          if (elect_one()) {
+          if constexpr (I8) {
+            constexpr uint32_t id64 = i_desc_i8(64);
+            if (elect_one()) {
+#pragma unroll
+              for (int dy = 4; dy >= 1; --dy)
+#pragma unroll
+                for (int i = 0; i < Cfg::STEP_CHUNKS; ++i)
+                  mma_i8(dcol[0][dy], abase + i * Cfg::CHUNK_COLS,
+                         bstep + (uint64_t)(((dy * Cfg::KC + 2 * i) * 2048) >> 4), id64, 1u);
+            }
+            __syncwarp();
+            acquire_to((int)(info & 0x7FFF));
+            // the epilogue's zeroing of a re-acquired slot before these MMAs
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (elect_one()) {
+#pragma unroll
+              for (int i = 0; i < Cfg::STEP_CHUNKS; ++i)
+                mma_i8(dcol[0][0], abase + i * Cfg::CHUNK_COLS,
+                       bstep + (uint64_t)(((2 * i) * 2048) >> 4), id64, 1u);
+              commit(&B.a_empty[slot]);
+              if (batch_after) commit(&B.acc_full[kb]);
+            }
+          } else if (elect_one()) {
 #pragma unroll
             for (int i = 0; i < Cfg::STEP_CHUNKS; ++i) {
               const int r = CIN == 3 ? i : 0;
@@ -525,20 +654,25 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
 #pragma unroll
           for (int i = 0; i < Cfg::STEP_CHUNKS; ++i) {
             const int rp = step_row<CIN>(st, i) + g.pad;
-            const uint32_t ahi = tmem + kA0 + slot * Cfg::STEP_COLS + i * 16;
+            const uint32_t ahi = tmem + kA0 + slot * Cfg::STEP_COLS + i * Cfg::CHUNK_COLS;
             const bool lead = CIN == 3 || (i == 0 && (st & 1) == 0);   // first chunk of its row
 #pragma unroll
             for (int dy = 0; dy < 5; ++dy) {
               const int o = rp - dy;
               if (o < 0 || o >= g.Ho || !run_mma) continue;
-              const uint32_t d = tmem + ((pbase + (uint32_t)(o >> 1)) % kPairSlots) * kPairCols +
-                                 (o & 1) * 32;
+              const uint32_t d = tmem +
+                                 ((pbase + (uint32_t)(o >> 1)) % kPairSlots) * Cfg::PAIR_COLS +
+                                 (o & 1) * Cfg::ROW_COLS;
               const uint64_t bd =
                   bd0 + (uint64_t)(((dy * Cfg::KC + step_wk<CIN>(st, i)) * 2048) >> 4);
               const bool first = lead && rp == max(o, g.pad);
-              mma_ts(d, ahi, bd, id32, first ? 0u : 1u);        // xh * wh
-              mma_ts(d, ahi, bd + (1024 >> 4), id32, 1u);       // xh * wl
-              mma_ts(d, ahi + 8, bd, id32, 1u);                 // xl * wh
+              if (I8) {
+                mma_i8(d, ahi, bd, i_desc_i8(64), 1u);   // [xh|xl] [wh 0; wl wh], zeroed acc
+              } else {
+                mma_ts(d, ahi, bd, id32, first ? 0u : 1u);        // xh * wh
+                mma_ts(d, ahi, bd + (1024 >> 4), id32, 1u);       // xh * wl
+                mma_ts(d, ahi + 8, bd, id32, 1u);                 // xl * wh
+              }
             }
           }
           commit(&B.a_empty[slot]);
@@ -569,6 +703,9 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
     uint32_t pbase = 0, tnum = 0;
     for (int t = blockIdx.x; t < g.tiles; t += gridDim.x, pbase += n_pairs, ++tnum) {
       const LaneFrame f = lane_frame(g, list, t, m);
+      // I8: the lane's frame dequantisation 256 * max|x| / 32639
+      const float xdq = I8 && f.valid ? absmax[f.fr] * (256.f / 32639.f) : 0.f;
+      float fmax_out = 0.f;   // running max |output| of the lane's frame (absmax_out)
       for (int pr = 0; pr < n_pairs; ++pr) {
         const uint32_t q = pbase + pr;
         if ((int)(q % Cfg::EPI) != egroup) continue;
@@ -584,15 +721,49 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
         asm volatile("tcgen05.fence::after_thread_sync;");
         float r0[32], r1[32];
         if (!(a.debug & 2)) {
-          if (h0) tmem_ld32(tl + sl * kPairCols, r0);
-          if (h1) tmem_ld32(tl + sl * kPairCols + 32, r1);
-          if (h0 || h1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if constexpr (I8) {
+            // row = (256 hi + mid) * 256 / (qx qw): hi and mid are exact s32
+            // sums (|hi| < 2^24), the conversion rounds mid only.  Sixteen
+            // channels of one row per round trip; r0 ends as the vertical max
+            // of both rows (a row without data is 0, as below) and r1 is not
+            // used.  Then the pair's columns are re-zeroed (the slot's next
+            // pair accumulates from zero) and the slot released.
+#pragma unroll
+            for (int row = 0; row < 2; ++row) {
+              if (!(row ? h1 : h0)) continue;
+#pragma unroll
+              for (int hf = 0; hf < 2; ++hf) {
+                int hi[16], mid[16];
+                const uint32_t c0 = tl + sl * Cfg::PAIR_COLS + row * 64 + hf * 16;
+                tmem_ld16i(c0, hi);
+                tmem_ld16i(c0 + 32, mid);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const float v = fmaf((float)hi[i], 256.f, (float)mid[i]) *
+                                  (xdq * B.wdq[hf * 16 + i]);
+                  r0[hf * 16 + i] = row == 0 ? v : (h0 ? fmaxf(r0[hf * 16 + i], v) : fmaxf(v, 0.f));
+                }
+              }
+            }
+            if (h0 && !h1) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r0[i] = fmaxf(r0[i], 0.f);
+            }
+#pragma unroll
+            for (int col = 0; col < Cfg::PAIR_COLS; col += 32) tmem_st32z(tl + sl * Cfg::PAIR_COLS + col);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          } else {
+            if (h0) tmem_ld32(tl + sl * kPairCols, r0);
+            if (h1) tmem_ld32(tl + sl * kPairCols + 32, r1);
+            if (h0 || h1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          }
         }
-        if (!h0 || (a.debug & 2)) {
+        if (I8 ? (!h0 && !h1) || (a.debug & 2) : !h0 || (a.debug & 2)) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) r0[i] = 0.f;
         }
-        if (!h1 || (a.debug & 2)) {
+        if (!I8 && (!h1 || (a.debug & 2))) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) r1[i] = 0.f;
         }
@@ -605,11 +776,16 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
         float res[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float lo_c = fmaxf(r0[i], r1[i]), hi_c = fmaxf(r0[16 + i], r1[16 + i]);
+          const float lo_c = I8 ? r0[i] : fmaxf(r0[i], r1[i]);
+          const float hi_c = I8 ? r0[16 + i] : fmaxf(r0[16 + i], r1[16 + i]);
           const float send = odd ? lo_c : hi_c;
           const float keep = odd ? hi_c : lo_c;
           const float other = __shfl_xor_sync(0xffffffffu, send, 1);
           res[i] = fmaxf(fmaxf(keep, other) + bias[i], 0.f);
+        }
+        if (a.absmax_out) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) fmax_out = fmaxf(fmax_out, fabsf(res[i]));
         }
         if (f.valid && !(a.debug & 2)) {
           float4* dst = reinterpret_cast<float4*>(
@@ -619,6 +795,9 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
             dst[i] = make_float4(res[4 * i], res[4 * i + 1], res[4 * i + 2], res[4 * i + 3]);
         }
       }
+      // non-negative floats order like their bit patterns
+      if (a.absmax_out && f.valid)
+        atomicMax(reinterpret_cast<int*>(a.absmax_out) + f.fr, __float_as_int(fmax_out));
     }
   } else if (Cfg::LOADER && warp == Cfg::CVT0 + 4 * Cfg::GROUPS) {
     // ------------------------------------------------- layer-1 row loader
@@ -757,6 +936,7 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
         const float* in2;
         int a, n1, np, my_idx;
         bool v1, v2;
+        float q;   // I8: this lane's frame quantisation factor 32639 / max|x|
       };
       auto segs = [&](int t) {
         Seg sg;
@@ -779,6 +959,12 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
           sg.in2 = list[u].in + (f1 + 1 - u * g.R) * g.in_frame;
         }
         sg.my_idx = lane < sg.n1 ? lane : sg.n1 + 4 + (lane - sg.n1);
+        sg.q = 0.f;
+        if (I8) {
+          const int myf = lane < sg.n1 ? f1 : f1 + 1;
+          const float mx = myf < g.frames ? absmax[myf] : 0.f;
+          sg.q = mx > 0.f ? 32639.f / mx : 0.f;
+        }
         return sg;
       };
       // piece j of the staged run: pixel p = j / 4, 16-byte quarter j % 4
@@ -840,11 +1026,17 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
               const float4 q = *reinterpret_cast<const float4*>(src + dx * Cfg::STAGE_PITCH + q4 * 16);
               v[4 * q4] = q.x; v[4 * q4 + 1] = q.y; v[4 * q4 + 2] = q.z; v[4 * q4 + 3] = q.w;
             }
-            uint32_t hi[8], lo[8];
-            split16(v, hi, lo);
-            if (!(a.debug & 8)) {
-              tmem_st8(tl + slot * Cfg::STEP_COLS + dx * 16, hi);
-              tmem_st8(tl + slot * Cfg::STEP_COLS + dx * 16 + 8, lo);
+            if constexpr (I8) {
+              uint32_t w[8];
+              quant16(v, sg.q, w);
+              if (!(a.debug & 8)) tmem_st8(tl + slot * Cfg::STEP_COLS + dx * Cfg::CHUNK_COLS, w);
+            } else {
+              uint32_t hi[8], lo[8];
+              split16(v, hi, lo);
+              if (!(a.debug & 8)) {
+                tmem_st8(tl + slot * Cfg::STEP_COLS + dx * 16, hi);
+                tmem_st8(tl + slot * Cfg::STEP_COLS + dx * 16 + 8, lo);
+              }
             }
           }
           w2.start();
@@ -874,9 +1066,42 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int CIN>
+// Per live frame max |x| of the launch's input (of_in) or output frames, one
+// block per frame: the quantisation scale of an int8 layer whose producer did
+// not record it (pb_conv_actor.absmax_in == NULL), or the absmax_out of a
+// launch that ran the tile kernel.
+constexpr int kAbsmaxThreads = 256;
+__global__ void __launch_bounds__(kAbsmaxThreads)
+frame_absmax_kernel(const LiveSpan* __restrict__ list, const int* __restrict__ n_live_p, int R,
+                    int64_t frame_floats, bool of_in, float* __restrict__ out) {
+  const int f = blockIdx.x;
+  if (f >= *n_live_p * R) return;
+  const int u = f / R, k = f - u * R;
+  const float* p = (of_in ? list[u].in : list[u].out) + k * frame_floats;
+  float m = 0.f;
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0 && frame_floats % 4 == 0) {
+    const float4* p4 = reinterpret_cast<const float4*>(p);
+    for (int64_t i = threadIdx.x; i < frame_floats / 4; i += kAbsmaxThreads) {
+      const float4 v = __ldg(p4 + i);
+      m = fmaxf(fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
+    }
+  } else {
+    for (int64_t i = threadIdx.x; i < frame_floats; i += kAbsmaxThreads) m = fmaxf(m, fabsf(p[i]));
+  }
+#pragma unroll
+  for (int d = 16; d; d >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, d));
+  __shared__ float wm[kAbsmaxThreads / 32];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kAbsmaxThreads / 32; ++w) m = fmaxf(m, wm[w]);
+    out[f] = m;
+  }
+}
+
+template <int CIN, bool I8 = false>
 int launch_rows(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t st, int sms) {
-  using Cfg = RowCfg<CIN>;
+  using Cfg = RowCfg<CIN, I8>;
   // one CTA per SM: the kernel allocates all 512 TMEM columns
   const int Wo_ = actor.w + 2 * actor.pad - 4, Ho_ = actor.h + 2 * actor.pad - 4;
   const RawGeom rg = raw_geom(actor.w, actor.pad, Wo_, Cfg::STEP_ROWS);
@@ -892,8 +1117,8 @@ int launch_rows(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t
   if (dev < 0) return PB_E_CUDA;
   static size_t configured[pb::kMaxDevices] = {};
   if (configured[dev] < smem) {
-    PB_CUDA(cudaFuncSetAttribute(conv_rows_kernel<CIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+    PB_CUDA(cudaFuncSetAttribute(conv_rows_kernel<CIN, I8>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured[dev] = smem;
   }
   if (res.n_streams > kUnitsThreads)
@@ -913,7 +1138,18 @@ int launch_rows(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t
   PB_LAUNCHED("conv_rows_units_kernel");
   const int grid = (int)std::min<int64_t>(max_tiles, sms);
   if (grid == 0) return PB_OK;
-  conv_rows_kernel<CIN><<<grid, Cfg::THREADS, smem, st>>>(actor, list, n_live);
+  const float* absmax = actor.absmax_in;
+  if (I8 && !absmax) {
+    float* buf = nullptr;
+    rc = pb::scratch(pb::kScratchConvAbsmax, sizeof(float) * n_units * actor.frames,
+                     reinterpret_cast<void**>(&buf));
+    if (rc) return rc;
+    frame_absmax_kernel<<<(unsigned)(n_units * actor.frames), kAbsmaxThreads, 0, st>>>(
+        list, n_live, actor.frames, (int64_t)actor.h * actor.w * CIN, true, buf);
+    PB_LAUNCHED("frame_absmax_kernel");
+    absmax = buf;
+  }
+  conv_rows_kernel<CIN, I8><<<grid, Cfg::THREADS, smem, st>>>(actor, list, n_live, absmax);
   PB_LAUNCHED("conv_rows_kernel");
   return PB_OK;
 }
@@ -926,8 +1162,34 @@ namespace pb {
 int fire_conv_rows(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t st, int sms) {
   switch (actor.cin) {
     case 3: return launch_rows<3>(actor, res, st, sms);
-    case 32: return launch_rows<32>(actor, res, st, sms);
+    case 32:
+      if (actor.math == PB_CONV_I8 && actor.weights_i8) return launch_rows<32, true>(actor, res, st, sms);
+      return launch_rows<32>(actor, res, st, sms);
     default: return PB_E_UNSUPPORTED;
   }
+}
+
+// absmax_out of a launch that ran the tile kernel: the output frames' max |y|
+// by a separate pass (the row kernel records it in its epilogue)
+int conv_absmax_out(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t st) {
+  if (res.n_streams > kUnitsThreads)
+    return pb::fail(PB_E_UNSUPPORTED, "conv: more than 1024 streams per launch");
+  const int64_t n_units = (int64_t)res.n_streams * res.n_iter;
+  if (n_units * actor.frames == 0) return PB_OK;
+  void* scratch = nullptr;
+  int rc = pb::scratch(pb::kScratchConvRows, sizeof(LiveSpan) * n_units + 16, &scratch);
+  if (rc) return rc;
+  LiveSpan* list = reinterpret_cast<LiveSpan*>(static_cast<uint8_t*>(scratch) + 16);
+  int* n_live = static_cast<int*>(scratch);
+  pb_conv_actor a = actor;
+  a.absmax_out = nullptr;   // the pass below writes every live frame
+  conv_rows_units_kernel<<<1, kUnitsThreads, 0, st>>>(a, res, list, n_live);
+  PB_LAUNCHED("conv_rows_units_kernel");
+  const int64_t out_floats = (int64_t)((actor.h + 2 * actor.pad - 4) / 2) *
+                             ((actor.w + 2 * actor.pad - 4) / 2) * kCoutR;
+  frame_absmax_kernel<<<(unsigned)(n_units * actor.frames), kAbsmaxThreads, 0, st>>>(
+      list, n_live, actor.frames, out_floats, false, actor.absmax_out);
+  PB_LAUNCHED("frame_absmax_kernel");
+  return PB_OK;
 }
 }  // namespace pb

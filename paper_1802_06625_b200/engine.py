@@ -67,6 +67,7 @@ class RuntimeConfig:
     host_threads: int = 0         # threads for native policies and digests (0 = all)
     pipeline: int = 8             # sub-epochs overlapping H2D / kernels / D2H / hashing (1 = off)
     exact: bool = True            # False: FIR taps as fused multiply-adds (<= 1e-5, not bit-exact)
+    conv_i8: bool = True          # Cin-32 convs on int8 limbs (logits <= 1e-3); False: bf16x3
 
 
 @dataclass
@@ -272,6 +273,10 @@ class DeviceRuntime:
                 raise UnsupportedGraph(f"actor {a.id} ({role}) needs a host behaviour")
 
         self.fir_math = _lib.PB_FIR_EXACT if config.exact else _lib.PB_FIR_MERGED
+        self.conv_math = _lib.PB_CONV_I8 if config.conv_i8 else _lib.PB_CONV_BF16X3
+        if os.environ.get("PB_CONV_MATH") in ("bf16x3", "i8"):
+            self.conv_math = (_lib.PB_CONV_I8 if os.environ["PB_CONV_MATH"] == "i8"
+                              else _lib.PB_CONV_BF16X3)
         if config.exact and os.environ.get("PB_FIR_MATH") == "paired":
             self.fir_math = _lib.PB_FIR_EXACT_PAIRED
         self.banks = find_filter_banks(plan, self.behaviors[0]) if config.fuse else []
@@ -663,16 +668,20 @@ class DeviceRuntime:
                 act.cond = cond_of(aid)
                 launches.append(("image", act))
             elif kind == "conv":
-                from .cnn_weights import conv_device_layout
+                from .cnn_weights import conv_device_layout, conv_device_layout_i8
                 b.init(aid, a.params, None)
                 fi = g.fifo(in_f[0])
                 if fi.token_bytes != b.h * b.w * b.cin * 4:
                     raise UnsupportedGraph(f"{aid}: token is not one {b.h}x{b.w}x{b.cin} frame")
+                # int8 limbs: Cin 32 (the row kernel's layer 2); bf16x3 otherwise
+                w_i8 = (self.mem.upload(conv_device_layout_i8(b.weights, b.cin))
+                        if b.cin == 32 else None)
                 act = _lib.ConvActor(self._ref(in_f[0]), self._ref(out_f[0], producer=True),
                                      self.mem.upload(conv_device_layout(b.weights, b.cin)),
                                      self.mem.upload(b.bias), fi.rate, b.h, b.w, b.cin,
-                                     b.cout, b.pad, cond_of(aid), 0)
-                launches.append(("conv", act))
+                                     b.cout, b.pad, cond_of(aid), 0, self.conv_math, w_i8,
+                                     None, None)
+                launches.append(("conv", act, aid))
             elif kind == "dense":
                 b.init(aid, a.params, None)
                 fi = g.fifo(in_f[0])
@@ -704,7 +713,44 @@ class DeviceRuntime:
             if aid in self.host_fired:
                 launches.append(("host", aid))
 
+        self._wire_conv_scales(launches, cond_of)
         return launches, fir_groups
+
+    def _wire_conv_scales(self, launches, cond_of) -> None:
+        """A conv actor fed straight by another conv actor (same condition, so
+        both launches see the same live firings in the same order; no delay)
+        reads its int8 quantisation scales -- every input frame's max |x| --
+        from the producer's epilogue (pb_conv_actor.absmax_out / absmax_in);
+        any other conv input gets them from a pre-pass over its frames."""
+        g = self.graph
+        convs = {item[2]: item[1] for item in launches if item[0] == "conv"}
+        for aid, act in convs.items():
+            a = g.actor(aid)
+            ins = [p for p in a.data_inputs]
+            if len(ins) != 1:
+                continue
+            f = g.fifo_into(PortRef(aid, ins[0].id))
+            src = f.src.actor
+            if src not in convs or f.delay or cond_of(src) != cond_of(aid) \
+                    or src in self.host_fired or aid in self.host_fired:
+                continue
+            prod = convs[src]
+            if prod.frames != act.frames:
+                continue
+            if not prod.absmax_out:
+                prod.absmax_out = self.mem.malloc(4 * self.n_streams * self.cap * prod.frames)
+            act.absmax_in = prod.absmax_out
+
+    def set_conv_math(self, math: int) -> None:
+        """Switch the conv arithmetic (_lib.PB_CONV_I8: int8 limbs on the
+        tensor cores for Cin 32, the default; _lib.PB_CONV_BF16X3: three bf16
+        products per useful one) of every conv launch of this runtime."""
+        self.conv_math = int(math)
+        drain = getattr(self, "_drain", None)
+        for lst in [self.launches] + ([drain[0]] if drain else []):
+            for item in lst:
+                if item[0] == "conv":
+                    item[1].math = self.conv_math
 
     def _build_tables(self):
         """Ring advance (every FIFO; the drain phase: the always-active ones)

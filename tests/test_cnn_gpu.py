@@ -3,8 +3,10 @@
 Parity is UNPINNED against the reference (it ships no DNN); the stated
 tolerance is the north star's: logits within 1e-3 (absolute, logits are
 O(1)) and the same top-1 class; conv/pool tokens within 1e-4 relative to
-max(1, |y|) (split-TF32 ~ fp32).  Control behaviour (which firings bypass)
-and firing counts are exact."""
+max(1, |y|) for bf16x3 layers (~ fp32) and 1e-3 for the int8-limb layer (the
+default for Cin 32, RuntimeConfig.conv_i8), whose arithmetic is also checked
+against its integer restatement (cnn_weights.conv_i8_reference) to 1e-5.
+Control behaviour (which firings bypass) and firing counts are exact."""
 import numpy as np
 import pytest
 
@@ -16,6 +18,7 @@ pytestmark = pytest.mark.gpu
 
 LOGIT_TOL = 1e-3
 ACT_TOL = 1e-4
+ACT_TOL_I8 = 1e-3
 
 
 def chain_desc(layers, R):
@@ -39,21 +42,70 @@ def rel_err(got, want):
     return float((np.abs(got - want) / np.maximum(1.0, np.abs(want))).max())
 
 
+@pytest.mark.parametrize("i8", [True, False])
 @pytest.mark.parametrize("layers,shape", [(["l1"], (52, 52, 32)), (["l1", "l2"], (24, 24, 32))])
-def test_conv_pool_tokens(layers, shape):
+def test_conv_pool_tokens(layers, shape, i8):
     R, firings = 3, 3
     x = vision.make_frames(0, R * firings)
     desc = chain_desc(layers, R)
-    (rep,) = run_streams(desc, 1, RuntimeConfig(source_firings=firings, capture_sinks=True),
+    (rep,) = run_streams(desc, 1, RuntimeConfig(source_firings=firings, capture_sinks=True,
+                                                conv_i8=i8),
                          sources={"src": [x.tobytes()]})
     got = np.frombuffer(rep.sink_data["sink"], np.float32).reshape(R * firings, *shape)
     p = oc.graph_params(vision.build_description(R))
     want = oc.conv_relu_pool(x, *p["l1"])
     if "l2" in layers:
-        want = oc.conv_relu_pool(want.astype(np.float32), *p["l2"])
+        l1 = want.astype(np.float32)
+        want = oc.conv_relu_pool(l1, *p["l2"])
+        if i8:   # l2 quantised with the scales l1's epilogue recorded
+            from paper_1802_06625_b200.cnn_weights import conv_i8_reference
+            assert rel_err(got, conv_i8_reference(l1, *p["l2"])) <= 2e-4
     err = rel_err(got, want)
-    assert err <= ACT_TOL, err
+    assert err <= (ACT_TOL_I8 if i8 and "l2" in layers else ACT_TOL), err
     assert rep.firing_counts["sink"] == firings
+
+
+@pytest.mark.parametrize("signed", [False, True])
+def test_int8_layer_matches_integer_reference(signed):
+    """The int8-limb layer (Cin 32) fed by a source (its scales from the
+    pre-pass, frame_absmax_kernel) against cnn_weights.conv_i8_reference, the
+    same quantisation and integer sums on the CPU: equal up to the float32
+    dequantisation (1e-5), and within 1e-3 of the float64 oracle.  Ragged:
+    frames with very different ranges, one all-zero frame."""
+    from paper_1802_06625_b200.cnn_weights import conv_i8_reference, layer_params
+    R, firings, h, w, pad = 3, 3, 52, 52, 2
+    rng = np.random.default_rng(7)
+    x = rng.random((R * firings, h, w, 32)).astype(np.float32)
+    if signed:
+        x = (x - 0.5).astype(np.float32)
+    x *= (10.0 ** rng.uniform(-3, 2, R * firings)).astype(np.float32)[:, None, None, None]
+    x[4] = 0.0
+    desc = {"name": "conv2", "control": {},
+            "actors": [
+                {"id": "src", "kind": "static", "behavior": "file_source",
+                 "params": {"path": "x.bin"},
+                 "ports": [{"id": "out", "dir": "out", "kind": "srp", "rate": R}]},
+                {"id": "c", "kind": "static", "behavior": "conv2d_relu_pool",
+                 "params": {"h": h, "w": w, "cin": 32, "cout": 32, "pad": pad, "seed": 4},
+                 "ports": [{"id": "in", "dir": "in", "kind": "srp", "rate": R},
+                           {"id": "out", "dir": "out", "kind": "srp", "rate": R}]},
+                {"id": "sink", "kind": "static", "behavior": "null_sink",
+                 "ports": [{"id": "in", "dir": "in", "kind": "srp", "rate": R}]}],
+            "fifos": [
+                {"id": "a", "src": "src.out", "dst": "c.in", "rate": R,
+                 "token_bytes": h * w * 32 * 4},
+                {"id": "b", "src": "c.out", "dst": "sink.in", "rate": R,
+                 "token_bytes": ((h + 2 * pad - 4) // 2) * ((w + 2 * pad - 4) // 2) * 32 * 4}]}
+    (rep,) = run_streams(desc, 1, RuntimeConfig(source_firings=firings, capture_sinks=True),
+                         sources={"src": [x.tobytes()]})
+    wt, b = layer_params({"seed": 4}, 32, 800)
+    got = np.frombuffer(rep.sink_data["sink"], np.float32).reshape(R * firings, 26, 26, 32)
+    scale = np.abs(x.reshape(len(x), -1)).max(1).clip(1e-30)[:, None, None, None]
+    ref = conv_i8_reference(x, wt, b, pad)
+    assert (np.abs(got - ref) / np.maximum(scale * 0.1, np.abs(ref))).max() <= 1e-5
+    want = oc.conv_relu_pool(x, wt, b, pad)
+    assert (np.abs(got - want) / np.maximum(scale, np.abs(want))).max() <= ACT_TOL_I8
+    assert (got[4] == np.maximum(b, 0)).all()
 
 
 @pytest.mark.parametrize("epoch", [4096, 3])
@@ -111,7 +163,8 @@ def test_conv_shapes(h, w, cin, pad):
     wt, b = layer_params({"seed": 9}, 32, 25 * cin)
     want = oc.conv_relu_pool(x, wt, b, pad)
     got = np.frombuffer(rep.sink_data["sink"], np.float32).reshape(want.shape)
-    assert rel_err(got, want) <= ACT_TOL
+    # Cin 32 runs on int8 limbs by default (1e-3), the others bf16x3 (1e-4)
+    assert rel_err(got, want) <= (ACT_TOL_I8 if cin == 32 else ACT_TOL)
 
 
 def test_conv_layer2_cta_pair_matches(monkeypatch):
@@ -193,7 +246,8 @@ def torch_forward(frames: np.ndarray, p: dict, device="cuda", batch=256) -> np.n
     return np.concatenate(out)
 
 
-def test_vision_graph_full_c3_every_frame():
+@pytest.mark.parametrize("i8", [True, False])
+def test_vision_graph_full_c3_every_frame(i8):
     """BASELINE config 3 at the bench's size (4 streams x 64 firings x 24
     frames, adaptive alternate_policy): EVERY processed frame's logits (3072)
     against the PyTorch float64 reference within the north star's 1e-3 and
@@ -207,7 +261,7 @@ def test_vision_graph_full_c3_every_frame():
     ref0 = torch_forward(xs[0][:2], p)
     assert np.abs(ref0 - oc.forward(xs[0][:2], p)["logits"]).max() < 1e-9
     reps = run_streams(desc, S, RuntimeConfig(source_firings=firings, epoch=firings,
-                                              capture_sinks=True),
+                                              capture_sinks=True, conv_i8=i8),
                        seeds=[5 + s for s in range(S)], sources={"src": [x.tobytes() for x in xs]})
     worst = 0.0
     for s in range(S):
@@ -222,4 +276,5 @@ def test_vision_graph_full_c3_every_frame():
         top2 = np.sort(want, axis=1)[:, -2:]
         clear = (top2[:, 1] - top2[:, 0]) > LOGIT_TOL
         assert (got.argmax(1)[clear] == want.argmax(1)[clear]).all(), s
-    print(f"worst logit error over {S * firings // 2 * R} frames: {worst:.2e}")
+    mode = "int8 limbs" if i8 else "bf16x3"
+    print(f"worst logit error over {S * firings // 2 * R} frames ({mode}): {worst:.2e}")

@@ -130,3 +130,41 @@ def test_vision_graph_admitted_and_behaviours_init():
     params = oc.graph_params(desc)
     assert params["l3"][0].shape == (100, 18432)
     assert vision.flops_per_frame() == 104 * 104 * 32 * 150 + 48 * 48 * 32 * 1600 + 3686400
+
+
+def test_conv_device_layout_i8_roundtrip():
+    """The int8-limb B operand: per K-step rows 0-31 [wh | 0], rows 32-63
+    [wl | wh] in core-matrix order, then the dequantisation factors; the limbs
+    recombine to the quantised weights, which are within wdq / 2 of W."""
+    from paper_1802_06625_b200.cnn_weights import (W_LIMIT, conv_device_layout_i8,
+                                                   conv_quant_weights)
+    w, _ = layer_params({"seed": 2}, 32, 800)
+    dev = conv_device_layout_i8(w, 32)
+    S = 50
+    assert dev.dtype == np.uint8 and dev.size == S * 2048 + 128
+    rows = dev[:S * 2048].view(np.int8).reshape(S, 8, 2, 8, 16).transpose(0, 1, 3, 2, 4)
+    rows = rows.reshape(S, 64, 32).astype(np.int64)
+    wdq = dev[S * 2048:].view(np.float32)
+    q, wdq_ref = conv_quant_weights(w)
+    assert (wdq == wdq_ref).all() and np.abs(q).max() <= W_LIMIT
+    assert (rows[:, :32, 16:] == 0).all() and (rows[:, 32:, 16:] == rows[:, :32, :16]).all()
+    rec = 256 * rows[:, :32, :16] + rows[:, 32:, :16]                 # [S][32][16]
+    assert (rec == conv_steps(q.astype(np.float32), 32).astype(np.int64)).all()
+    assert (np.abs(q * wdq[:, None].astype(np.float64) - w) <= wdq[:, None] * 0.5 + 1e-12).all()
+
+
+def test_int8_limb_conv_within_tolerance():
+    """The int8-limb layer-2 arithmetic (cnn_weights.conv_i8_reference, which
+    the GPU tests hold the kernel to) on the vision graph's own shapes: conv
+    tokens within 1e-3 of max(1, |y|) of float64, and the logits it leads to
+    within the north star's 1e-3, top-1 equal."""
+    from paper_1802_06625_b200.cnn_weights import conv_i8_reference
+    p = oc.graph_params(vision.build_description(2))
+    x = vision.make_frames(3, 2)
+    want = oc.forward(x, p)
+    l1 = want["l1"].astype(np.float32)
+    got2 = conv_i8_reference(l1, *p["l2"])
+    assert (np.abs(got2 - want["l2"]) / np.maximum(1, np.abs(want["l2"]))).max() <= 1e-3
+    logits = oc.classify(oc.dense(got2.astype(np.float32), *p["l3"]), *p["join"])
+    assert np.abs(logits - want["logits"]).max() <= 1e-3
+    assert (logits.argmax(-1) == want["logits"].argmax(-1)).all()
