@@ -259,8 +259,15 @@ struct RowCfg {
   // warp 0 issues the half-0 steps, so one warp's per-step bookkeeping runs
   // while the other's MMAs keep the tensor pipe busy (integer sums: the
   // interleaving cannot change a result)
-  static constexpr int MMA2 = I8 ? CVT0 + 4 * GROUPS + LOADER : -1;
-  static constexpr int THREADS = (CVT0 + 4 * GROUPS + LOADER + (I8 ? 1 : 0)) * 32;
+  // ROWSPLIT (layer 1, fp32 accumulation): the two MMA warps split every
+  // step by OUTPUT ROW parity instead -- each accumulator is written by one
+  // warp in one order, so the fp32 sums stay deterministic
+#ifndef PB_ROWS_SPLIT1
+#define PB_ROWS_SPLIT1 1
+#endif
+  static constexpr bool ROWSPLIT = CIN == 3 && PB_ROWS_SPLIT1;
+  static constexpr int MMA2 = (I8 || ROWSPLIT) ? CVT0 + 4 * GROUPS + LOADER : -1;
+  static constexpr int THREADS = (CVT0 + 4 * GROUPS + LOADER + (MMA2 >= 0 ? 1 : 0)) * 32;
   static_assert(RING >= 2, "TMEM budget");
 };
 
@@ -420,10 +427,10 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
   if (threadIdx.x == 0) {
     for (int i = 0; i < RING; ++i) {
       bar_init(&B.a_full[i], 4);
-      bar_init(&B.a_empty[i], 1);
+      bar_init(&B.a_empty[i], Cfg::ROWSPLIT ? 2 : 1);
     }
     for (int i = 0; i < kPairSlots; ++i) {
-      bar_init(&B.acc_full[i], I8 ? 2 : 1);
+      bar_init(&B.acc_full[i], Cfg::MMA2 >= 0 ? 2 : 1);
       bar_init(&B.acc_empty[i], 4);
     }
     bar_init(&B.w_full, 1);
@@ -632,12 +639,14 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
               if (batch_after) commit(&B.acc_full[kb]);
             }
           } else if (elect_one()) {
+            const int par = mw ^ odd;   // ROWSPLIT: this warp's rows have rel & 1 == par
 #pragma unroll
             for (int i = 0; i < Cfg::STEP_CHUNKS; ++i) {
               const int r = CIN == 3 ? i : 0;
               const uint32_t ahi = abase + i * 16;
 #pragma unroll
               for (int dy = 0; dy < 5; ++dy) {
+                if (Cfg::ROWSPLIT && ((4 + r - dy) & 1) != par) continue;
                 const uint32_t d = dcol[r][dy];
                 const uint64_t bd = bstep + (uint64_t)(((dy * Cfg::KC + (CIN == 3 ? 0 : 2 * i)) *
                                                         2048) >> 4);
@@ -660,6 +669,7 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
             for (int dy = 0; dy < 5; ++dy) {
               const int o = rp - dy;
               if (o < 0 || o >= g.Ho || !run_mma) continue;
+              if (Cfg::ROWSPLIT && (o & 1) != mw) continue;
               const uint32_t d = tmem +
                                  ((pbase + (uint32_t)(o >> 1)) % kPairSlots) * Cfg::PAIR_COLS +
                                  (o & 1) * Cfg::ROW_COLS;

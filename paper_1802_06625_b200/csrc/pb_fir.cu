@@ -1185,6 +1185,9 @@ bank_merged_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
 #ifndef PB_MS_WARPS
 #define PB_MS_WARPS 4
 #endif
+#ifndef PB_MS_EARLY   // 1: the first stages' input tiles load while the planner runs
+#define PB_MS_EARLY 0    // (measured 0.2075 vs 0.2052 ms per C2 step: not adopted)
+#endif
 #ifndef PB_MS_CARRY   // 1: the stream kernel also carries the branch histories
 #define PB_MS_CARRY 1
 #endif
@@ -1223,7 +1226,16 @@ static_assert(sizeof(BankPlan) % 16 == 0, "BankPlan is bulk-copied");
 __global__ void __launch_bounds__(kMSThreads, PB_MS_MINB)
 bank_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPlan* plan,
                    int tiles) {
+  // PDL: this grid may start while the planner (its predecessor) still runs.
+  // Everything before the planner has completed by then (the planner waited
+  // for it before it let this grid launch), so the input spans are final and
+  // the output spans free; only the plans and the carried states the planner
+  // reads need the planner's completion (griddepcontrol.wait below).
+#if PB_MS_EARLY
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#else
   pb::pdl_enter();
+#endif
   extern __shared__ __align__(128) uint8_t ms_raw[];
   MSSmem& sm = *reinterpret_cast<MSSmem*>(ms_raw);
   if (threadIdx.x == 0) {
@@ -1249,6 +1261,7 @@ bank_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
       // branch's last firing this epoch (fir_carry_kernel's work; the planner
       // that reads the old state has completed before this grid started)
       const int q = (threadIdx.x & 31) - 1;
+      asm volatile("griddepcontrol.wait;" ::: "memory");   // the planner read the old state
       if (q < 2 * kHist) {
         const int nb = bank.n_branches, plane = q / kHist, k = q - plane * kHist;
         for (int64_t i = blockIdx.x; i < (int64_t)res.n_streams * nb; i += gridDim.x) {
@@ -1273,6 +1286,10 @@ bank_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
     int tile = (int)(w0 - span * tiles) - 1;
     const float* in = nullptr;
     u64 out = 0;
+    // the first ring's worth of tiles streams in before the planner finished;
+    // their plans follow once it has (the stage barriers count both)
+    const int64_t pre = !PB_MS_EARLY ? 0 : n_items < kMSStages ? n_items : kMSStages;
+    if (pre == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int64_t k = 0; k < n_items; ++k) {
       if (k == 0 || ++tile == tiles) {   // (next) span: its ring addresses
         if (k > 0) {
@@ -1296,7 +1313,7 @@ bank_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
       sm.out[stage] = out;
       sm.t0[stage] = (int)t0;
       mbar_arrive_tx(&sm.full[stage], 2 * bytes + (uint32_t)sizeof(BankPlan));
-      bulk_g2s(&sb.plan, plan + span, (uint32_t)sizeof(BankPlan), &sm.full[stage]);
+      if (k >= pre) bulk_g2s(&sb.plan, plan + span, (uint32_t)sizeof(BankPlan), &sm.full[stage]);
 #if PB_MS_L2HINT
       bulk_g2s_hint(sb.re + kPad - lead, in + t0 - lead, bytes, &sm.full[stage], pol);
       bulk_g2s_hint(sb.im + kPad - lead, in + B + t0 - lead, bytes, &sm.full[stage], pol);
@@ -1304,6 +1321,12 @@ bank_stream_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, const BankPl
       bulk_g2s(sb.re + kPad - lead, in + t0 - lead, bytes, &sm.full[stage]);
       bulk_g2s(sb.im + kPad - lead, in + B + t0 - lead, bytes, &sm.full[stage]);
 #endif
+      if (k == pre - 1) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        for (int64_t j = 0; j < pre; ++j)
+          bulk_g2s(&sm.st[j].plan, plan + (w0 + j) / tiles, (uint32_t)sizeof(BankPlan),
+                   &sm.full[j]);
+      }
     }
     return;
   }

@@ -59,8 +59,9 @@ e = last("fir_persistent<1, 0>")
 if e:
     traffic["fir_persistent<bank, EXACT>"] = e["dram_read"] + e["dram_write"]
 # both conv layers run as the row-streaming kernel (pb_conv_rows.cu)
-for nm, pat in (("conv_rows_kernel<3>", "conv_rows_kernel<3>"),
-                ("conv_rows_kernel<32>", "conv_rows_kernel<32>"), ("dense_kernel", "dense_kernel")):
+for nm, pat in (("conv_rows_kernel<3, false>", "conv_rows_kernel<3, false>"),
+                ("conv_rows_kernel<32, true>", "conv_rows_kernel<32, true>"),
+                ("dense_kernel", "dense_kernel")):
     x = last(pat)
     if x:
         traffic[nm] = x["dram_read"] + x["dram_write"]

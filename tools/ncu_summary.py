@@ -49,5 +49,15 @@ def summarise(path):
     return res
 
 
+def metric_list():
+    """The counters above as an ncu --metrics list: hardware counters only (no
+    SASS-patching sections), for kernels whose --set full replay stalls."""
+    return ",".join(WANT + [f"smsp__average_warps_issue_stalled_{s}_per_issue_active.ratio"
+                            for s in STALLS])
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "--metrics":
+        print(metric_list())
+        sys.exit(0)
     print(json.dumps(summarise(sys.argv[1]), indent=1))
