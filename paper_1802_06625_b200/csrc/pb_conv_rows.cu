@@ -235,8 +235,8 @@ struct RowCfg {
   static constexpr int PAIRS = CIN == 3 ? PB_ROWS_PAIRS1 : (I8 ? 3 : 4);
   static constexpr int A0 = PAIRS * PAIR_COLS;             // first A-ring column
   static constexpr int RING = (512 - A0) / STEP_COLS;     // A steps in flight
-#ifndef PB_ROWS_GROUPS1
-#define PB_ROWS_GROUPS1 2
+#ifndef PB_ROWS_GROUPS1   // layer 1 with the row-parity MMA split: 1 converter group
+#define PB_ROWS_GROUPS1 1    // + 2 epilogue groups 1.12 ms, 2 + 1 1.20 ms per 6144 frames
 #endif
   static constexpr int GROUPS = CIN == 3 ? PB_ROWS_GROUPS1 : 2;   // converter groups of 4 warps
   // layer 2: each converter warp stages its lanes' row-half pixels in shared
@@ -251,7 +251,7 @@ struct RowCfg {
   // epilogue groups of 4 warps taking alternate pairs: layer 1 has 2.2 pairs
   // per step to drain (its epilogue chain per pair is latency-bound)
 #ifndef PB_ROWS_EPI1
-#define PB_ROWS_EPI1 1
+#define PB_ROWS_EPI1 2
 #endif
   static constexpr int EPI = CIN == 3 ? PB_ROWS_EPI1 : 1;
   static constexpr int CVT0 = 1 + 4 * EPI;                 // first converter warp
