@@ -287,13 +287,6 @@ def device_steps(rt, blocks, math_mode, n_steps, warmup, barrier, max_over_ranks
     for _ in range(max(3, warmup)):
         rt.fire_epoch(0, blocks)
     _lib.check(lib.pb_stream_sync(rt.stream))
-    # keep the GPU busy until the timed region (clocks and memory P-state at
-    # their loaded level; the clock sampler gets its first samples meanwhile)
-    t_w = time.time()
-    while time.time() - t_w < 0.3:
-        for _ in range(8):
-            rt.fire_epoch(0, blocks)
-        _lib.check(lib.pb_stream_sync(rt.stream))
     kev = []
 
     def hook(kind, phase):
@@ -301,6 +294,10 @@ def device_steps(rt, blocks, math_mode, n_steps, warmup, barrier, max_over_ranks
             e = new_event()
             lib.pb_event_record(e, rt.stream)
             kev.append(e)
+    if clocks is not None:   # the sampler's first samples before the timed region
+        time.sleep(0.3)
+        for _ in range(max(3, warmup)):
+            rt.fire_epoch(0, blocks)
     barrier()
     _lib.check(lib.pb_stream_sync(rt.stream))
     e0, e1 = new_event(), new_event()

@@ -315,6 +315,23 @@ typedef struct {
 } pb_matmul_actor;
 int pb_fire_matmul(pb_matmul_actor actor, pb_resolved res, void* stream);
 
+/* A chain of matmul actors fired as one launch (the engine fuses consecutive
+ * matmul actors under one condition whose link channels are exclusive and
+ * undelayed; those channels are then not materialised): out = W_{L-1} ...
+ * W_1 W_0 x, every layer in MatMul.fire's order (bypass.py:36-49: ascending k,
+ * separate mul/add roundings), so the result is bit-identical to L
+ * pb_fire_matmul launches.  N = 8 (16 lanes per firing). */
+typedef struct {
+  pb_span_ref in;
+  pb_span_ref out;
+  const float* weights; /* device [layers][N][N] row-major */
+  int32_t n;
+  int32_t layers;       /* 2 .. 8 */
+  int32_t cond;
+  int32_t pad_;
+} pb_matmul_chain_actor;
+int pb_fire_matmul_chain(pb_matmul_chain_actor actor, pb_resolved res, void* stream);
+
 /* path_merge (bypass.py:52-66): exactly one live input is forwarded; the
  * marker is added when it is the bypass port.  A firing with != 1 live input
  * sets *error_flag (device int32) -> ActorPanic. */

@@ -97,6 +97,11 @@ class MatmulActor(C.Structure):
     _fields_ = [("in_", SpanRef), ("out", SpanRef), ("weights", vp), ("n", i32), ("cond", i32)]
 
 
+class MatmulChainActor(C.Structure):
+    _fields_ = [("in_", SpanRef), ("out", SpanRef), ("weights", vp), ("n", i32),
+                ("layers", i32), ("cond", i32), ("pad_", i32)]
+
+
 class PathMergeActor(C.Structure):
     _fields_ = [("in_", SpanRef * PB_MAX_PORTS), ("out", SpanRef), ("n_in", i32),
                 ("bypass_index", i32), ("marker", C.c_float), ("cond", i32),
@@ -188,6 +193,7 @@ SIGNATURES = {
     "pb_fire_branch_sum": (C.c_int, [SumActor, Resolved, i64, vp]),
     "pb_fire_bytes": (C.c_int, [BytesActor, Resolved, vp]),
     "pb_fire_matmul": (C.c_int, [MatmulActor, Resolved, vp]),
+    "pb_fire_matmul_chain": (C.c_int, [MatmulChainActor, Resolved, vp]),
     "pb_fire_path_merge": (C.c_int, [PathMergeActor, Resolved, vp]),
     "pb_fire_image": (C.c_int, [ImageActor, Resolved, vp]),
     "pb_fire_conv_pool": (C.c_int, [ConvActor, Resolved, vp]),

@@ -173,6 +173,90 @@ matmul_packed_kernel(pb_matmul_actor a, pb_resolved res, int L) {
   }
 }
 
+// A fused chain of 8x8 matmul layers (pb_matmul_chain_actor): the layout of
+// matmul_packed_kernel (16 lanes per firing, lane = (row i, column block cb),
+// 4 outputs each, kMF firings per lane group) with the layer's result handed
+// to the next layer through registers: the next layer's lane (i, cb) needs
+// column block cb of every row k, i.e. the float4 lane (k, cb) holds -- eight
+// shuffles of a float4 per layer.  Same products and sums in the same order
+// as one matmul_packed_kernel launch per layer.
+constexpr int kChainMax = 8;
+#ifndef PB_CHAIN_MF
+#define PB_CHAIN_MF 2
+#endif
+constexpr int kCMF = PB_CHAIN_MF;   // firings per lane group (32 floats of x each)
+__global__ void __launch_bounds__(256)
+matmul_chain_kernel(pb_matmul_chain_actor a, pb_resolved res) {
+  constexpr int N = 8, L = 16;
+  const int s = blockIdx.y, lane = threadIdx.x & 31;
+  __shared__ float w[kChainMax * N * N];
+  for (int e = threadIdx.x; e < a.layers * N * N; e += blockDim.x) w[e] = a.weights[e];
+  __syncthreads();
+  const int g = lane / L, sub = lane - g * L;
+  const int j0 = (((int)blockIdx.x * 8 + (threadIdx.x >> 5)) * 2 + g) * kCMF;
+  const int leader = g * L;
+  const unsigned grp = 0xFFFFu << leader;
+  const int cnt = pb::cond_count(res, a.cond, s);
+  if (j0 >= cnt) return;   // whole lane groups leave together
+  const float* x[kCMF];
+  float* out[kCMF];
+#pragma unroll
+  for (int f = 0; f < kCMF; ++f) {
+    x[f] = nullptr;
+    out[f] = nullptr;
+    if (sub == 0 && j0 + f < cnt) {
+      const int n = pb::firing_iter(res, a.cond, s, j0 + f);
+      x[f] = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n));
+      out[f] = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < kCMF; ++f) {
+    x[f] = reinterpret_cast<const float*>(
+        __shfl_sync(grp, reinterpret_cast<unsigned long long>(x[f]), leader));
+    out[f] = reinterpret_cast<float*>(
+        __shfl_sync(grp, reinterpret_cast<unsigned long long>(out[f]), leader));
+  }
+  const int i = sub >> 1, cb = sub & 1;   // row i, columns 4 cb .. 4 cb + 3
+  // every lane of the group loads the column block cb of all 8 rows
+  float4 col[kCMF][N];
+#pragma unroll
+  for (int f = 0; f < kCMF; ++f)
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+      col[f][k] = x[f] != nullptr ? __ldg(reinterpret_cast<const float4*>(x[f] + k * N) + cb)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int l = 0; l < a.layers; ++l) {
+    const float* wl = w + l * N * N + i * N;
+#pragma unroll
+    for (int f = 0; f < kCMF; ++f) {
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const float wk = wl[k];
+        acc[0] = __fadd_rn(acc[0], __fmul_rn(wk, col[f][k].x));
+        acc[1] = __fadd_rn(acc[1], __fmul_rn(wk, col[f][k].y));
+        acc[2] = __fadd_rn(acc[2], __fmul_rn(wk, col[f][k].z));
+        acc[3] = __fadd_rn(acc[3], __fmul_rn(wk, col[f][k].w));
+      }
+      if (l + 1 == a.layers) {
+        if (x[f] != nullptr)
+          reinterpret_cast<float4*>(out[f])[sub] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      } else {
+        // row k of the next input, column block cb, lives in lane 2 k + cb
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const int src = leader + 2 * k + cb;
+          col[f][k].x = __shfl_sync(grp, acc[0], src);
+          col[f][k].y = __shfl_sync(grp, acc[1], src);
+          col[f][k].z = __shfl_sync(grp, acc[2], src);
+          col[f][k].w = __shfl_sync(grp, acc[3], src);
+        }
+      }
+    }
+  }
+}
+
 // Packed form for tokens of 16..512 bytes in 16-byte units (the reference's
 // 256-B matrices: 16 lanes per firing, two firings per warp): the first lane
 // of each firing's lane group resolves the firing (activity, live input,
@@ -282,6 +366,17 @@ int pb_fire_matmul(pb_matmul_actor actor, pb_resolved res, void* stream) {
   matmul_kernel<<<grid, per_cta * NN, NN * sizeof(float), pb::as_stream(stream)>>>(actor, res,
                                                                                    per_cta);
   PB_LAUNCHED("matmul_kernel");
+  return PB_OK;
+}
+
+int pb_fire_matmul_chain(pb_matmul_chain_actor actor, pb_resolved res, void* stream) {
+  if (res.n_iter == 0) return PB_OK;
+  if (actor.n != 8 || actor.layers < 1 || actor.layers > kChainMax)
+    return pb::fail(PB_E_UNSUPPORTED, "matmul chain: N = 8 and 1..8 layers");
+  const int per_cta = 8 * 2 * kCMF;
+  dim3 grid((unsigned)((res.n_iter + per_cta - 1) / per_cta), res.n_streams);
+  matmul_chain_kernel<<<grid, 256, 0, pb::as_stream(stream)>>>(actor, res);
+  PB_LAUNCHED("matmul_chain_kernel");
   return PB_OK;
 }
 

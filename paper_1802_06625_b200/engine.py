@@ -44,7 +44,7 @@ from .behaviors import (ActorBehavior, DeviceBehavior, FileSource, FireContext, 
                         decode_control, native_policy_kind, resolve)
 from .errors import ActorPanic, DeviceUnavailable, Timeout, UnsupportedGraph
 from .graph import CONTROL_IN, CONTROL_OUT, DRP, Graph, PortRef, as_graph
-from .plan import ALWAYS, ExecPlan, admit, find_filter_banks, is_device
+from .plan import ALWAYS, ExecPlan, admit, find_filter_banks, find_matmul_chains, is_device
 
 
 @dataclass
@@ -283,8 +283,14 @@ class DeviceRuntime:
         # a region with a host-fired member keeps its channels materialised
         self.banks = [grp for grp in self.banks
                       if not ({grp.router, grp.combiner, *grp.branches} & set(self.host_fired))]
+        # matmul chains (bypass.py's l1 -> l2 -> l3): one launch per chain at
+        # its head, the link channels stay in registers
+        self.chains = [c for c in find_matmul_chains(plan, self.behaviors[0])
+                       if not (set(c.actors) & set(self.host_fired))] if config.fuse else []
         self.fused_actors = {a for grp in self.banks for a in [grp.router, *grp.branches]}
+        self.fused_actors |= {a for c in self.chains for a in c.actors[1:]}
         self.virtual = {fid for grp in self.banks for fid in grp.internal_fifos}
+        self.virtual |= {fid for c in self.chains for fid in c.internal_fifos}
         self._allocate()
         self.launches, self.fir_groups = self._build_launches()
         self._build_tables()
@@ -491,6 +497,7 @@ class DeviceRuntime:
         fir_groups: list[tuple[int, int, int]] = []    # (device array, n, block)
         done: set[str] = set()
         bank_at = {grp.combiner: grp for grp in self.banks}
+        chain_at = {c.actors[0]: c for c in self.chains}
         # topological depth so independent FIR actors share a launch (the
         # delayed channels inside cycles do not order an epoch's firings)
         depth = {aid: 0 for aid in plan.order}
@@ -552,6 +559,20 @@ class DeviceRuntime:
                 launches.append(("bank", bank, block))
                 # (no fir_groups entry: pb_fire_filter_bank carries its branches)
                 done.add(aid)
+                continue
+            if aid in chain_at:
+                c = chain_at[aid]
+                x = g.actor(c.actors[0])
+                fin = g.fifo_into(PortRef(x.id, x.data_inputs[0].id))
+                y = g.actor(c.actors[-1])
+                fout = sorted(g.fifos_from(PortRef(y.id, y.output_ports[0].id)),
+                              key=lambda f: f.id)[0]
+                w = np.concatenate([np.array(g.actor(m).params["w"], dtype=np.float32)
+                                    for m in c.actors])
+                act = _lib.MatmulChainActor(self._ref(fin.id), self._ref(fout.id, producer=True),
+                                            self.mem.upload(w), 8, len(c.actors), cond_of(aid), 0)
+                launches.append(("matmul_chain", act))
+                done.update(c.actors)
                 continue
             if kind == "fir":
                 key = next(k for k, v in fir_by_level.items() if aid in v)
@@ -1096,6 +1117,8 @@ class DeviceRuntime:
                 _lib.check(lib.pb_fire_bytes(item[1], res, st), "bytes")
             elif kind == "matmul":
                 _lib.check(lib.pb_fire_matmul(item[1], res, st), "matmul")
+            elif kind == "matmul_chain":
+                _lib.check(lib.pb_fire_matmul_chain(item[1], res, st), "matmul chain")
             elif kind == "path_merge":
                 _lib.check(lib.pb_fire_path_merge(item[1], res, st), "path_merge")
             elif kind == "image":

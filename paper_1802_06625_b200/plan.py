@@ -401,5 +401,67 @@ def find_filter_banks(plan: ExecPlan, behaviors: dict[str, ActorBehavior]) -> li
     return groups
 
 
+@dataclass
+class MatmulChain:
+    """Consecutive matmul actors fired as one kernel (pb_fire_matmul_chain)."""
+
+    actors: list[str]            # in data order
+    internal_fifos: set[str]     # the link channels (not materialised)
+
+
+def find_matmul_chains(plan: ExecPlan, behaviors: dict[str, ActorBehavior]) -> list[MatmulChain]:
+    """Maximal chains a_1 -> ... -> a_k (k >= 2) of 8x8 matmul actors
+    (bypass.py:36-49) under one condition whose link channels are exclusive
+    (the producer's only output, the consumer's only input), undelayed and one
+    token per firing, and whose members fire no extra drain firings.  Such a
+    chain's tokens between members never need to leave registers."""
+    g = plan.graph
+
+    def is_mm(aid):
+        b = behaviors.get(aid)
+        if getattr(b, "kernel", None) != "matmul":
+            return False
+        a = g.actor(aid)
+        if len(a.data_inputs) != 1 or len(a.output_ports) != 1:
+            return False
+        n2 = len(g.actor(aid).params.get("w", []))
+        return n2 == 64 and plan.extra.get(aid, 0) == 0
+
+    def link(aid):   # the channel to the next member, or None
+        a = g.actor(aid)
+        fs = g.fifos_from(PortRef(aid, a.output_ports[0].id))
+        if len(fs) != 1:
+            return None
+        f = fs[0]
+        nxt = f.dst.actor
+        if not is_mm(nxt) or f.delay or f.rate != 1 or f.token_bytes != 256 or \
+                plan.actor_cond[nxt] != plan.actor_cond[aid] or \
+                plan.fifo_cond[f.id] != plan.actor_cond[aid]:
+            return None
+        return f
+    chains = []
+    heads = [a.id for a in g.actors if is_mm(a.id)]
+    has_pred = set()
+    for aid in heads:
+        f = link(aid)
+        if f is not None:
+            has_pred.add(f.dst.actor)
+    for aid in heads:
+        if aid in has_pred:
+            continue
+        members, internal = [aid], set()
+        cur = aid
+        while True:
+            f = link(cur)
+            if f is None or len(members) == 8:
+                break
+            members.append(f.dst.actor)
+            internal.add(f.id)
+            cur = f.dst.actor
+        if len(members) >= 2:
+            chains.append(MatmulChain(members, internal))
+    return chains
+
+
 def is_device(b: ActorBehavior) -> bool:
     return isinstance(b, DeviceBehavior) or bool(getattr(b, "kernel", ""))

@@ -59,14 +59,14 @@ e = last("fir_persistent<1, 0>")
 if e:
     traffic["fir_persistent<bank, EXACT>"] = e["dram_read"] + e["dram_write"]
 # both conv layers run as the row-streaming kernel (pb_conv_rows.cu)
-for nm, pat in (("conv_rows_kernel<3, false>", "conv_rows_kernel<3, false>"),
-                ("conv_rows_kernel<32, true>", "conv_rows_kernel<32, true>"),
+for nm, pat in (("conv_rows_kernel<3, false>", "conv_rows_kernel<3, 0>"),
+                ("conv_rows_kernel<32, true>", "conv_rows_kernel<32, 1>"),
                 ("dense_kernel", "dense_kernel")):
     x = last(pat)
     if x:
         traffic[nm] = x["dram_read"] + x["dram_write"]
 (prof / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1))
-for r in ("merged", "exact", "cnn"):
+for r in ("merged", "exact", "cnn", "dense"):
     src = out / f"{R}_ncu_{r}.json"
     if src.exists():
         shutil.copy(src, prof / f"{R}_ncu_{r}.json")
