@@ -31,6 +31,72 @@ def test_bypass_app_matches_reference(golden, tmp_path, epoch):
     assert rep.firing_counts == g["firing_counts"]
 
 
+@pytest.mark.parametrize("fuse", [True, False])
+def test_bypass_chain_fused_and_unfused(golden, tmp_path, fuse):
+    """The l1 -> l2 -> l3 matmul chain fired as one kernel (matmul_chain_kernel,
+    link channels in registers; the default) and as three matmul launches give
+    the reference's sink bytes, digests, firing counts and channel reports."""
+    from paper_1802_06625_b200.engine import DeviceRuntime
+    arr = golden["bypass_small"]
+    p = tmp_path / "input.bin"
+    p.write_bytes(arr["input"].tobytes())
+    desc = bypass_desc(str(p))
+    cfg = RuntimeConfig(source_firings=32, seed=5, capture_sinks=True, fuse=fuse)
+    rep = run(desc, config=cfg)
+    g = golden["bypass"]["default"]
+    assert rep.sink_data["sink"] == arr["sink"].tobytes()
+    assert rep.firing_counts == g["firing_counts"]
+    rt = DeviceRuntime(desc, config=cfg, n_streams=1, seeds=[5])
+    kinds = [item[0] for item in rt.launches]
+    assert ("matmul_chain" in kinds) == fuse and ("matmul" in kinds) != fuse
+    rt.close()
+
+
+def test_matmul_chain_layers_exact(tmp_path):
+    """A 5-layer chain with a condition (route -> chain -> merge): every active
+    firing bit-identical to the layers applied one by one in MatMul.fire's
+    order (numpy float32 products and sums, ascending k)."""
+    import numpy as np
+    from paper_1802_06625_b200 import run_streams
+    from paper_1802_06625_b200.apps import bypass
+    desc = bypass.build_description(str(tmp_path / "x.bin"))
+    acts = [a for a in desc["actors"] if a["id"] not in ("l1", "l2", "l3")]
+    fifos = [f for f in desc["fifos"] if f["id"] not in ("f_l1", "f_l2", "f_l3", "f_chain")]
+    layers = [f"m{k}" for k in range(5)]
+    rng = np.random.default_rng(3)
+    ws = [rng.uniform(-1, 1, 64).astype(np.float32) for _ in layers]
+    for k, lid in enumerate(layers):
+        acts.append({"id": lid, "kind": "static", "behavior": "matmul",
+                     "params": {"w": [float(v) for v in ws[k]]},
+                     "ports": [{"id": "in", "dir": "in", "kind": "srp", "rate": 1},
+                               {"id": "out", "dir": "out", "kind": "srp", "rate": 1}]})
+    chain = ["fork.d1"] + [f"{m}.in" for m in layers]
+    outs = [f"{m}.out" for m in layers] + ["join.e1"]
+    for k in range(len(layers) + 1):
+        src = chain[k] if k == 0 else outs[k - 1]
+        dst = chain[k + 1] if k < len(layers) else "join.e1"
+        fifos.append({"id": f"c{k}", "src": src, "dst": dst, "rate": 1, "delay": 0,
+                      "token_bytes": 256})
+    desc = dict(desc, actors=acts, fifos=fifos)
+    F = 40
+    x = rng.uniform(-1, 1, (F, 8, 8)).astype(np.float32)
+    (rep,) = run_streams(desc, 1, RuntimeConfig(source_firings=F, capture_sinks=True),
+                         seeds=[5], sources={"src": [x.tobytes()]})
+    got = np.frombuffer(rep.sink_data["sink"], np.float32).reshape(F, 8, 8)
+    for j in range(F):
+        if j % 2:   # alternate_policy: odd firings bypass (+ marker)
+            assert (got[j] == x[j] + np.float32(bypass.MARKER)).all()
+            continue
+        y = x[j]
+        for w in ws:
+            W = w.reshape(8, 8)
+            z = np.zeros((8, 8), np.float32)
+            for k in range(8):
+                z = (z + (W[:, k:k + 1] * y[k:k + 1, :]).astype(np.float32)).astype(np.float32)
+            y = z
+        assert (got[j] == y).all(), j
+
+
 def test_source_exhaustion_is_actor_panic(tmp_path):
     from paper_1802_06625_b200.apps import predistortion as pd
     p = tmp_path / "short.bin"

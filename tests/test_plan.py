@@ -160,3 +160,45 @@ def test_mixed_graph_admitted():
     assert p.roles["dpd_conf"] == p.roles["cnn_conf"] == "config"
     assert {p.roles[a] for a in ("cnn_l1", "cnn_l2", "cnn_l3", "dpd_b1")} == {"device"}
     assert len(p.conds) == 6     # 4 DPD branches + CNN process / bypass
+
+
+def test_matmul_chain_found_in_bypass_app():
+    """plan.find_matmul_chains: the bypass app's l1 -> l2 -> l3 (link channels
+    f_l2, f_l3); a second consumer of l2's output ends the chain at l2."""
+    from paper_1802_06625_b200.apps import bypass
+    from paper_1802_06625_b200.behaviors import resolve
+    from paper_1802_06625_b200.plan import find_matmul_chains
+
+    def chains(desc):
+        p = admit(as_graph(desc))
+        behaviors = {}
+        for a in desc["actors"]:
+            b = resolve(a["behavior"])
+            if a["behavior"] != "file_source":
+                b.init(a["id"], a.get("params", {}), None)
+            behaviors[a["id"]] = b
+        return [(c.actors, sorted(c.internal_fifos)) for c in find_matmul_chains(p, behaviors)]
+    desc = bypass.build_description("x.bin")
+    assert chains(desc) == [(["l1", "l2", "l3"], ["f_l2", "f_l3"])]
+    # a static chain src -> m1 -> m2 -> m3 -> sink; a second consumer of m2's
+    # output ends the chain at m2
+    from paper_1802_06625_b200.apps.bypass import layer_weights
+
+    def port(pid, d):
+        return {"id": pid, "dir": d, "kind": "srp", "rate": 1}
+    acts = [{"id": "src", "kind": "static", "behavior": "file_source", "params": {"path": "x"},
+             "ports": [port("out", "out")]},
+            {"id": "sink", "kind": "static", "behavior": "null_sink", "ports": [port("in", "in")]}]
+    acts += [{"id": f"m{k}", "kind": "static", "behavior": "matmul",
+              "params": {"w": layer_weights(k)}, "ports": [port("in", "in"), port("out", "out")]}
+             for k in (1, 2, 3)]
+
+    def ff(fid, src, dst):
+        return {"id": fid, "src": src, "dst": dst, "rate": 1, "delay": 0, "token_bytes": 256}
+    fifos = [ff("a", "src.out", "m1.in"), ff("b", "m1.out", "m2.in"), ff("c", "m2.out", "m3.in"),
+             ff("d", "m3.out", "sink.in")]
+    lin = {"name": "lin", "actors": acts, "fifos": fifos, "control": {}}
+    assert chains(lin) == [(["m1", "m2", "m3"], ["b", "c"])]
+    tap = {"id": "tap", "kind": "static", "behavior": "null_sink", "ports": [port("in", "in")]}
+    lin2 = dict(lin, actors=acts + [tap], fifos=fifos + [ff("t", "m2.out", "tap.in")])
+    assert chains(lin2) == [(["m1", "m2"], ["b"])]

@@ -35,9 +35,9 @@ def _ref_stream(args):
         return time.perf_counter() - t0
 
 
-def measure(S=1024, mats=1024, steps=50):
+def measure(S=1024, mats=1024, steps=50, fuse=1):
     rt = DeviceRuntime(bypass.build_description(), config=RuntimeConfig(
-        source_firings=mats, epoch=mats), n_streams=S, seeds=list(range(S)),
+        source_firings=mats, epoch=mats, fuse=bool(fuse)), n_streams=S, seeds=list(range(S)),
         sources={"src": [None] * S})
     st = rt.source_staging("src")
     for s in range(S):
@@ -84,7 +84,17 @@ def measure(S=1024, mats=1024, steps=50):
            "step_ms": step_ms, "matrices_per_s": n / (step_ms / 1e3),
            "kernel_ms_per_step": per_kind,
            "note": "half the firings run l1 -> l2 -> l3 (3 x 512 rounded mul/add per matrix), "
-                   "half the bypass; every firing moves 256-B tokens through rings"}
+                   "half the bypass; tokens are 256-B matrices in rings"}
+    # algorithmic HBM bytes per matrix: fused, a chain firing reads its matrix
+    # and writes l3's (the link channels stay in registers) and the merge
+    # moves 512 B; unfused, each of the 3 matmuls moves 512 B; a bypass firing
+    # moves 512 B in the merge (route aliases its input)
+    per = (512 + 512 + 512) / 2 if fuse else (3 * 512 + 512 + 512) / 2
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs") \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else 6555.5
+    out["fused_chain"] = bool(fuse)
+    out["hbm"] = {"bytes_per_matrix_avg": per, "achieved_gbs": per * n / (step_ms / 1e3) / 1e9,
+                  "peak_gbs": peak, "frac": per * n / (step_ms / 1e3) / 1e9 / peak}
     if (ROOT / "oracle" / "_ref").is_dir():
         cores = os.cpu_count() or 1
         ref_mats = 256
