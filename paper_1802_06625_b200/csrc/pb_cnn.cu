@@ -1114,6 +1114,9 @@ int launch_conv(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t
 // the frame chunk is split to bf16 hi/lo by the converter warps.  When there
 // are fewer M-tiles than SMs the K range is split across CTAs and the last
 // CTA of a tile sums the partials in split order (deterministic).
+#ifndef PB_DENSE_PF
+#define PB_DENSE_PF 0   // 1: L2 prefetch of the frame chunk after next (measured: no gain)
+#endif
 constexpr int kDN = 112;                    // padded outputs per precision half
 constexpr int kDKC = 64;                    // K per pipeline chunk (4 K16 steps)
 constexpr int kDStages = 3;
@@ -1211,7 +1214,20 @@ dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, i
                           : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     };
+    // chunk c + 2 is requested into L2 (no registers) while c + 1 is in
+    // flight into registers: twice the frame bytes in flight per SM
+    auto prefetch_chunk = [&](int c) {
+#pragma unroll
+      for (int k = 0; k < kDItems; ++k) {
+        const int i = ct + k * kDCvtThreads;
+        const int r = i >> 2, q = i & 3;
+        const float* rp = S.rowp[r];
+        if (PB_DENSE_PF && rp != nullptr && (q & 1) == 0)   // one request per 128-B line
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + (int64_t)c * kDKC + 16 * q));
+      }
+    };
     if (c0 < c1) load_chunk(c0);
+    if (c0 + 1 < c1) prefetch_chunk(c0 + 1);
     for (int c = c0, it = 0; c < c1; ++c, ++it) {
       const int st = it % kDStages;
       const uint32_t use = (uint32_t)(it / kDStages);
@@ -1220,6 +1236,7 @@ dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, i
       for (int k = 0; k < kDItems; ++k)
 #pragma unroll
         for (int u = 0; u < 4; ++u) cur[k][u] = nxt[k][u];
+      if (c + 2 < c1) prefetch_chunk(c + 2);
       if (c + 1 < c1) load_chunk(c + 1);
       mbar_wait(&S.empty[st], (use & 1) ^ 1);
       if (ct == 0) {
@@ -1311,12 +1328,27 @@ dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, i
       asm volatile("bar.sync 1, %0;" ::"n"(kDEpiThreads));
       if (S.last) {
         __threadfence();
-        if (op != nullptr) {
-          for (int o = 0; o < a.nout; ++o) {
-            float acc = 0.f;
-            for (int sp = 0; sp < splits; ++sp)
-              acc = __fadd_rn(acc, __ldcg(partial + ((int64_t)sp * gridDim.x * 128 + m) * kDN + o));
-            op[o] = __fadd_rn(acc, __ldg(a.bias + o));
+        // the tile's partials are [split][128 rows][kDN] contiguous: the 128
+        // threads sum them as float4s (coalesced, every load independent) in
+        // split order, then scatter each row's outputs to its frame
+        constexpr int kQ = kDN / 4;                       // float4 per row
+        const float4* pp = reinterpret_cast<const float4*>(partial) + (int64_t)mt * 128 * kQ;
+        const int64_t split_stride = (int64_t)gridDim.x * 128 * kQ;
+#pragma unroll 4
+        for (int i = r; i < 128 * kQ; i += kDEpiThreads) {
+          const int row = i / kQ, q = i - row * kQ;
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int sp = 0; sp < splits; ++sp) {
+            const float4 v = __ldcg(pp + sp * split_stride + i);
+            acc.x = __fadd_rn(acc.x, v.x); acc.y = __fadd_rn(acc.y, v.y);
+            acc.z = __fadd_rn(acc.z, v.z); acc.w = __fadd_rn(acc.w, v.w);
+          }
+          float* orow = S.outp[row];
+          if (orow != nullptr) {
+            const float o4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (4 * q + u < a.nout) orow[4 * q + u] = __fadd_rn(o4[u], __ldg(a.bias + 4 * q + u));
           }
         }
         if (r == 0) counters[mt] = 0;
