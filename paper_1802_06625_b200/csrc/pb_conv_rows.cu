@@ -781,6 +781,7 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
         __syncwarp();
         if (lane == 0) bar_arrive(&B.acc_empty[sl]);
         w2.stop();
+        w3.start();
         // 2x2 max: rows (2p, 2p+1) in registers, columns (xo, xo+1) on lanes
         // (m, m^1); the even lane keeps channels 0-15, the odd lane 16-31
         float res[16];
@@ -804,6 +805,7 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
           for (int i = 0; i < 4; ++i)
             dst[i] = make_float4(res[4 * i], res[4 * i + 1], res[4 * i + 2], res[4 * i + 3]);
         }
+        w3.stop();
       }
       // non-negative floats order like their bit patterns
       if (a.absmax_out && f.valid)
@@ -829,7 +831,9 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
       const bool mine = j < nseg && i < Cfg::STEP_ROWS && !(a.debug & 1);
       for (int st = 0; st < n_steps; ++st, ++c) {
         const uint32_t rslot = c % Cfg::RAW;
+        w1.start();
         bar_wait(&B.raw_empty[rslot], ((c / Cfg::RAW) & 1) ^ 1);
+        w1.stop();
         if (lane == 0)
           bar_expect_tx(&B.raw_full[rslot],
                         (a.debug & 1) ? 0u : row_bytes * nseg * Cfg::STEP_ROWS);
@@ -1067,7 +1071,8 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
     }
   }
 
-  if (prof && lane == 0 && (warp == 0 || warp == 1 || warp == Cfg::CVT0 || warp == Cfg::CVT0 + 4))
+  if (prof && lane == 0 && (warp == 0 || warp == 1 || warp == Cfg::CVT0 || warp == Cfg::CVT0 + 4 ||
+                            warp == Cfg::MMA2 || (Cfg::LOADER && warp == Cfg::CVT0 + 4 * Cfg::GROUPS)))
     printf("{\"conv_rows_prof\": %d, \"warp\": %d, \"total\": %lld, \"wait1\": %lld, \"wait2\": %lld, \"w3\": %lld, \"w4\": %lld}\n",
            CIN, warp, clock64() - t_begin, w1.acc, w2.acc, w3.acc, w4.acc);
   asm volatile("tcgen05.fence::before_thread_sync;");

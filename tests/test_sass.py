@@ -72,3 +72,17 @@ def test_exact_fir_paths_have_no_fma(sass):
     # rounded separately (predistortion.py:51-65 under numpy), so no FFMA
     for body in ops(sass, r"fir_persistentILb[01]ELi0E"):
         assert not re.search(r"\bFFMA\b", body)
+
+
+def test_row_conv_kernels_are_tensor_memory_native(sass):
+    """The default conv path (pb_conv_rows.cu): layer 1 bf16 TS MMAs (A in
+    TMEM: UTCHMMA with a tmem A operand, tcgen05.st = STTM) fed by bulk copies
+    (UBLKCP); layer 2 on the int8 tensor cores (UTCIMMA) with its A operand
+    written to TMEM (STTM) and its accumulators read back (LDTM)."""
+    (l1,) = ops(sass, r"conv_rows_kernelILi3ELb0E")
+    assert re.search(r"\bUTCHMMA\b.*tmem\[", l1) and re.search(r"\bSTTM\b", l1)
+    assert re.search(r"\bUBLKCP\b", l1) and re.search(r"\bLDTM\b", l1)
+    (l2,) = ops(sass, r"conv_rows_kernelILi32ELb1E")
+    assert re.search(r"\bUTCIMMA\b", l2) and re.search(r"\bSTTM\b", l2)
+    assert re.search(r"\bLDTM\b", l2)
+    assert not re.search(r"\bUTCHMMA\b", l2)   # no bf16 products left in the int8 layer
