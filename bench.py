@@ -1018,6 +1018,10 @@ def main():
         except Exception as e:  # noqa: BLE001
             gather = {"error": f"{type(e).__name__}: {e}"}
 
+    def trace(what):   # PB_BENCH_TRACE=1: leg progress on stderr (multi-rank debugging)
+        if os.environ.get("PB_BENCH_TRACE"):
+            print(f"[rank {rank}] {what} {time.strftime('%H:%M:%S')}", file=sys.stderr, flush=True)
+    trace("dpd done")
     k10 = None
     if not args.skip_k10:
         rt.close()
@@ -1028,13 +1032,16 @@ def main():
         if rt is not None:
             rt.close()
             rt = None
+        trace("k10 done")
         cnn = cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks)
+        trace("cnn done")
     mixed_res = None
     if not args.skip_mixed:
         if rt is not None:
             rt.close()
             rt = None
         mixed_res = mixed_leg(args, rank, world, local, barrier, max_over_ranks)
+        trace("mixed done")
 
     if rank == 0:
         line = {
