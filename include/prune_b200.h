@@ -369,6 +369,25 @@ typedef struct {
 } pb_image_actor;
 int pb_fire_image(pb_image_actor actor, pb_resolved res, void* stream);
 
+/* The motion region blur -> frame_diff_threshold(cur = blur, prev = blur one
+ * frame earlier through a delay-1 channel) -> plus_median as ONE launch
+ * (motion.py:74-108; the engine fuses it when all three always fire): a CTA
+ * takes a run of consecutive frames of one stream, blurs each once and keeps
+ * the previous blurred frame in shared memory, so the f_cur and f_mask
+ * channels never reach HBM.  The delayed channel stays a ring: its token is
+ * read at the epoch's first iteration and written at the last (the next
+ * epoch's first).  Same integers as the three image actors.  Power-of-two
+ * sides 8..128. */
+typedef struct {
+  pb_span_ref in;        /* blur's input */
+  pb_span_ref prev_in;   /* frame_diff_threshold.prev (consumer side of the delayed ring) */
+  pb_span_ref prev_out;  /* blur -> delayed ring (producer side) */
+  pb_span_ref out;       /* plus_median's output */
+  int32_t side;
+  int32_t threshold;
+} pb_motion_region;
+int pb_fire_motion_region(pb_motion_region region, pb_resolved res, void* stream);
+
 /* ------------------------------------------------ CNN actors (vision example) */
 /* The paper's adaptive DNN is not in the reference
  * package; these actors and their oracle (oracle/cnn.py) are builder-defined.

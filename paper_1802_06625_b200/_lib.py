@@ -116,6 +116,11 @@ class ImageActor(C.Structure):
 PB_IMG_BLUR, PB_IMG_DIFF, PB_IMG_MEDIAN = 0, 1, 2
 
 
+class MotionRegion(C.Structure):
+    _fields_ = [("in_", SpanRef), ("prev_in", SpanRef), ("prev_out", SpanRef), ("out", SpanRef),
+                ("side", i32), ("threshold", i32)]
+
+
 class ConvActor(C.Structure):
     _fields_ = [("in_", SpanRef), ("out", SpanRef), ("weights", vp), ("bias", vp),
                 ("frames", i32), ("h", i32), ("w", i32), ("cin", i32), ("cout", i32),
@@ -194,6 +199,7 @@ SIGNATURES = {
     "pb_fire_bytes": (C.c_int, [BytesActor, Resolved, vp]),
     "pb_fire_matmul": (C.c_int, [MatmulActor, Resolved, vp]),
     "pb_fire_matmul_chain": (C.c_int, [MatmulChainActor, Resolved, vp]),
+    "pb_fire_motion_region": (C.c_int, [MotionRegion, Resolved, vp]),
     "pb_fire_path_merge": (C.c_int, [PathMergeActor, Resolved, vp]),
     "pb_fire_image": (C.c_int, [ImageActor, Resolved, vp]),
     "pb_fire_conv_pool": (C.c_int, [ConvActor, Resolved, vp]),

@@ -280,9 +280,158 @@ image_fast_kernel(pb_image_actor a, pb_resolved res) {
   }
 }
 
+// ---------------------------------------------- fused motion region
+// blur -> diff(cur, prev) -> median per frame, frames of one stream in order
+// (kMRF per CTA): the word-parallel arithmetic of image_fast_kernel, with the
+// blurred frame and the mask kept in shared memory.
+#ifndef PB_MRF
+#define PB_MRF 8
+#endif
+constexpr int kMRF = PB_MRF;   // frames per CTA (one extra blur per run)
+
+template <int LW>
+__device__ __forceinline__ void mr_blur(const uint32_t* fr, uint32_t* hs, uint32_t* out, int tid) {
+  constexpr int W = 1 << LW, side = 4 * W, rows = kFastThreads >> LW;
+  constexpr uint32_t K4 = 0x04060401u;
+  const int xw = tid & (W - 1);
+  for (int y = tid >> LW; y < side; y += rows) {
+    const uint32_t* row = fr + y * W;
+    const uint32_t wa = xw > 0 ? row[xw - 1] : 0u, wb = row[xw];
+    const uint32_t wc = xw < W - 1 ? row[xw + 1] : 0u;
+    const uint32_t h0 = __dp4a(__byte_perm(wa, wb, 0x5432), K4, (wb >> 16) & 0xFFu);
+    const uint32_t h1 = __dp4a(__byte_perm(wa, wb, 0x6543), K4, wb >> 24);
+    const uint32_t h2 = __dp4a(wb, K4, wc & 0xFFu);
+    const uint32_t h3 = __dp4a(__byte_perm(wb, wc, 0x4321), K4, (wc >> 8) & 0xFFu);
+    reinterpret_cast<uint2*>(hs)[y * W + xw] = make_uint2(h0 | (h1 << 16), h2 | (h3 << 16));
+  }
+  __syncthreads();
+  for (int y = tid >> LW; y < side; y += rows) {
+    const uint32_t orig = fr[y * W + xw];
+    uint32_t word = orig;
+    if (y >= 2 && y < side - 2) {
+      const uint2* h = reinterpret_cast<const uint2*>(hs) + (y - 2) * W + xw;
+      const uint2 r0 = h[0], r1 = h[W], r2 = h[2 * W], r3 = h[3 * W], r4 = h[4 * W];
+      uint32_t lo = r0.x + 4u * r1.x + 6u * r2.x + 4u * r3.x + r4.x;
+      uint32_t hi = r0.y + 4u * r1.y + 6u * r2.y + 4u * r3.y + r4.y;
+      lo = (lo >> 8) & 0x00FF00FFu;
+      hi = (hi >> 8) & 0x00FF00FFu;
+      word = __byte_perm(lo, hi, 0x6420);
+      if (xw == 0) word = __byte_perm(word, orig, 0x3254);
+      if (xw == W - 1) word = __byte_perm(word, orig, 0x7610);
+    }
+    out[y * W + xw] = word;
+  }
+}
+
+template <int LW>
+__global__ void __launch_bounds__(kFastThreads)
+motion_region_kernel(pb_motion_region r, pb_resolved res) {
+  constexpr int W = 1 << LW, side = 4 * W, nw = side * W, rows = kFastThreads >> LW;
+  const int s = blockIdx.y, tid = threadIdx.x;
+  const int n0 = blockIdx.x * kMRF, n1 = min(res.n_iter, n0 + kMRF);
+  if (n0 >= res.n_iter) return;
+  extern __shared__ uint4 mr_smem[];
+  uint32_t* fr = reinterpret_cast<uint32_t*>(mr_smem);   // [nw] source frame
+  uint32_t* hs = fr + nw;                                 // [2 nw] horizontal sums
+  uint32_t* bl[2] = {hs + 2 * nw, hs + 3 * nw};           // blurred frames (cur / prev)
+  uint32_t* mk = hs + 4 * nw;                             // [nw] mask
+  const int thr = r.threshold;
+  const uint32_t t4 = (uint32_t)min(max(thr, 0), 255) * 0x01010101u;
+  auto load = [&](const uint8_t* src, uint32_t* dst) {
+    for (int i = tid; i < nw / 4; i += kFastThreads)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  };
+  // the frame before n0: the delayed channel's token at the epoch's first
+  // iteration (its initial token, or the previous epoch's last blurred
+  // frame), else this epoch's source frame n0 - 1 blurred again
+  int cur = 0;
+  if (n0 == 0) {
+    load(pb::span_ptr(r.prev_in, res, s, 0), bl[1]);
+  } else {
+    load(pb::span_ptr(r.in, res, s, n0 - 1), fr);
+    __syncthreads();
+    mr_blur<LW>(fr, hs, bl[1], tid);
+  }
+  // the next frame's words are in flight (registers) while this one is computed
+  constexpr int kPre = (nw / 4 + kFastThreads - 1) / kFastThreads;
+  uint4 pre[kPre];
+  auto fetch = [&](int n) {
+    const uint4* src = reinterpret_cast<const uint4*>(pb::span_ptr(r.in, res, s, n));
+#pragma unroll
+    for (int q = 0; q < kPre; ++q)
+      if (tid + q * kFastThreads < nw / 4) pre[q] = src[tid + q * kFastThreads];
+  };
+  fetch(n0);
+  for (int n = n0; n < n1; ++n) {
+    __syncthreads();   // fr / hs free again
+#pragma unroll
+    for (int q = 0; q < kPre; ++q)
+      if (tid + q * kFastThreads < nw / 4) reinterpret_cast<uint4*>(fr)[tid + q * kFastThreads] = pre[q];
+    if (n + 1 < n1) fetch(n + 1);
+    __syncthreads();
+    uint32_t* const c = bl[cur];
+    const uint32_t* const pv = bl[cur ^ 1];
+    mr_blur<LW>(fr, hs, c, tid);
+    __syncthreads();
+    for (int i = tid; i < nw; i += kFastThreads)
+      mk[i] = thr < 0 ? 0xFFFFFFFFu : thr >= 255 ? 0u : __vcmpgtu4(__vabsdiffu4(c[i], pv[i]), t4);
+    if (n == res.n_iter - 1) {   // the next epoch's first "prev"
+      uint32_t* po = reinterpret_cast<uint32_t*>(pb::span_ptr(r.prev_out, res, s, n));
+      for (int i = tid; i < nw / 4; i += kFastThreads)
+        reinterpret_cast<uint4*>(po)[i] = reinterpret_cast<const uint4*>(c)[i];
+    }
+    __syncthreads();
+    uint32_t* o = reinterpret_cast<uint32_t*>(pb::span_ptr(r.out, res, s, n));
+    const int xw = tid & (W - 1);
+    for (int y = tid >> LW; y < side; y += rows) {
+      const uint32_t cw = mk[y * W + xw];
+      uint32_t word = cw;
+      if (y >= 1 && y < side - 1) {
+        const uint32_t up = mk[(y - 1) * W + xw], dn = mk[(y + 1) * W + xw];
+        const uint32_t pl = xw > 0 ? mk[y * W + xw - 1] : 0u;
+        const uint32_t nx = xw < W - 1 ? mk[y * W + xw + 1] : 0u;
+        const uint32_t lf = __byte_perm(pl, cw, 0x6543), rt = __byte_perm(cw, nx, 0x4321);
+        word = med5(cw, up, dn, lf, rt);
+        if (xw == 0) word = __byte_perm(word, cw, 0x3214);
+        if (xw == W - 1) word = __byte_perm(word, cw, 0x7210);
+      }
+      o[y * W + xw] = word;
+    }
+    cur ^= 1;
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+int pb_fire_motion_region(pb_motion_region r, pb_resolved res, void* stream) {
+  if (res.n_iter == 0) return PB_OK;
+  const int side = r.side;
+  if (side < 8 || side > kMaxSide || (side & (side - 1)))
+    return pb::fail(PB_E_UNSUPPORTED, "motion region: power-of-two sides 8..128");
+  const size_t smem = (size_t)side * side * 6;   // frame, sums (2x), two blurred, mask
+  static bool attr[pb::kMaxDevices] = {};
+  const int dev = pb::device();
+  if (dev < 0) return PB_E_CUDA;
+  if (!attr[dev]) {
+    PB_CUDA(cudaFuncSetAttribute(motion_region_kernel<5>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 6 * kMaxSide * kMaxSide));
+    attr[dev] = true;
+  }
+  dim3 grid((res.n_iter + kMRF - 1) / kMRF, res.n_streams);
+  cudaStream_t st = pb::as_stream(stream);
+  switch (side) {
+    case 8: motion_region_kernel<1><<<grid, kFastThreads, smem, st>>>(r, res); break;
+    case 16: motion_region_kernel<2><<<grid, kFastThreads, smem, st>>>(r, res); break;
+    case 32: motion_region_kernel<3><<<grid, kFastThreads, smem, st>>>(r, res); break;
+    case 64: motion_region_kernel<4><<<grid, kFastThreads, smem, st>>>(r, res); break;
+    default: motion_region_kernel<5><<<grid, kFastThreads, smem, st>>>(r, res); break;
+  }
+  PB_LAUNCHED("motion_region_kernel");
+  return PB_OK;
+}
 
 int pb_fire_image(pb_image_actor actor, pb_resolved res, void* stream) {
   if (res.n_iter == 0) return PB_OK;

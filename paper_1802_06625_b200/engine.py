@@ -44,7 +44,8 @@ from .behaviors import (ActorBehavior, DeviceBehavior, FileSource, FireContext, 
                         decode_control, native_policy_kind, resolve)
 from .errors import ActorPanic, DeviceUnavailable, Timeout, UnsupportedGraph
 from .graph import CONTROL_IN, CONTROL_OUT, DRP, Graph, PortRef, as_graph
-from .plan import ALWAYS, ExecPlan, admit, find_filter_banks, find_matmul_chains, is_device
+from .plan import (ALWAYS, ExecPlan, admit, find_filter_banks, find_matmul_chains,
+                   find_motion_regions, is_device)
 
 
 @dataclass
@@ -287,10 +288,17 @@ class DeviceRuntime:
         # its head, the link channels stay in registers
         self.chains = [c for c in find_matmul_chains(plan, self.behaviors[0])
                        if not (set(c.actors) & set(self.host_fired))] if config.fuse else []
+        # motion regions (motion.py's blur -> detect -> clean): one launch at
+        # the blur, f_cur / f_mask in shared memory, the delayed f_prev a ring
+        self.motions = [m for m in find_motion_regions(plan, self.behaviors[0])
+                        if not ({m.blur, m.detect, m.clean} & set(self.host_fired))] \
+            if config.fuse else []
         self.fused_actors = {a for grp in self.banks for a in [grp.router, *grp.branches]}
         self.fused_actors |= {a for c in self.chains for a in c.actors[1:]}
+        self.fused_actors |= {a for m in self.motions for a in (m.detect, m.clean)}
         self.virtual = {fid for grp in self.banks for fid in grp.internal_fifos}
         self.virtual |= {fid for c in self.chains for fid in c.internal_fifos}
+        self.virtual |= {fid for m in self.motions for fid in (m.cur_fifo, m.mask_fifo)}
         self._allocate()
         self.launches, self.fir_groups = self._build_launches()
         self._build_tables()
@@ -498,6 +506,7 @@ class DeviceRuntime:
         done: set[str] = set()
         bank_at = {grp.combiner: grp for grp in self.banks}
         chain_at = {c.actors[0]: c for c in self.chains}
+        motion_at = {m.blur: m for m in self.motions}
         # topological depth so independent FIR actors share a launch (the
         # delayed channels inside cycles do not order an epoch's firings)
         depth = {aid: 0 for aid in plan.order}
@@ -559,6 +568,17 @@ class DeviceRuntime:
                 launches.append(("bank", bank, block))
                 # (no fir_groups entry: pb_fire_filter_bank carries its branches)
                 done.add(aid)
+                continue
+            if aid in motion_at:
+                m = motion_at[aid]
+                x = g.actor(m.blur)
+                fin = g.fifo_into(PortRef(x.id, x.data_inputs[0].id))
+                act = _lib.MotionRegion(self._ref(fin.id), self._ref(m.prev_fifo),
+                                        self._ref(m.prev_fifo, producer=True),
+                                        self._ref(m.out_fifo, producer=True), m.side,
+                                        int(g.actor(m.detect).params.get("threshold", 16)))
+                launches.append(("motion_region", act))
+                done.update({m.blur, m.detect, m.clean})
                 continue
             if aid in chain_at:
                 c = chain_at[aid]
@@ -1119,6 +1139,8 @@ class DeviceRuntime:
                 _lib.check(lib.pb_fire_matmul(item[1], res, st), "matmul")
             elif kind == "matmul_chain":
                 _lib.check(lib.pb_fire_matmul_chain(item[1], res, st), "matmul chain")
+            elif kind == "motion_region":
+                _lib.check(lib.pb_fire_motion_region(item[1], res, st), "motion region")
             elif kind == "path_merge":
                 _lib.check(lib.pb_fire_path_merge(item[1], res, st), "path_merge")
             elif kind == "image":

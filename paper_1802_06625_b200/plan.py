@@ -463,5 +463,70 @@ def find_matmul_chains(plan: ExecPlan, behaviors: dict[str, ActorBehavior]) -> l
     return chains
 
 
+@dataclass
+class MotionRegion:
+    """blur -> frame_diff_threshold (cur, prev delayed one frame) -> plus_median
+    fired as one kernel (pb_fire_motion_region)."""
+
+    blur: str
+    detect: str
+    clean: str
+    cur_fifo: str
+    prev_fifo: str
+    mask_fifo: str
+    out_fifo: str
+    side: int
+
+
+def find_motion_regions(plan: ExecPlan, behaviors: dict[str, ActorBehavior]) -> list[MotionRegion]:
+    """The motion app's chain (apps/motion.py:74-108): a gauss_blur whose one
+    output port feeds exactly a frame_diff_threshold's "cur" (undelayed) and
+    "prev" (one token of delay), whose one output feeds only a plus_median with
+    one output channel; every actor and channel always active, one frame per
+    firing, a power-of-two side, no drain firings."""
+    g = plan.graph
+    op = lambda aid: getattr(behaviors.get(aid), "op", None) \
+        if getattr(behaviors.get(aid), "kernel", None) == "image" else None
+    out = []
+    for a in g.actors:
+        if op(a.id) != 0 or len(a.data_inputs) != 1 or len(a.output_ports) != 1:
+            continue
+        fs = g.fifos_from(PortRef(a.id, a.output_ports[0].id))
+        if len(fs) != 2:
+            continue
+        d = fs[0].dst.actor
+        if fs[1].dst.actor != d or op(d) != 1:
+            continue
+        by_port = {f.dst.port: f for f in fs}
+        if set(by_port) != {"cur", "prev"}:
+            continue
+        fc, fp = by_port["cur"], by_port["prev"]
+        tb = fc.token_bytes
+        side = int(round(tb ** 0.5))
+        if fc.delay or fp.delay != 1 or fc.rate != 1 or fp.rate != 1 or fp.token_bytes != tb \
+                or side * side != tb or side < 8 or side > 128 or side & (side - 1):
+            continue
+        da = g.actor(d)
+        if len(da.output_ports) != 1:
+            continue
+        fm = g.fifos_from(PortRef(d, da.output_ports[0].id))
+        if len(fm) != 1 or fm[0].delay or fm[0].rate != 1 or fm[0].token_bytes != tb:
+            continue
+        m = fm[0].dst.actor
+        ma = g.actor(m)
+        if op(m) != 2 or len(ma.output_ports) != 1:
+            continue
+        fo = g.fifos_from(PortRef(m, ma.output_ports[0].id))
+        if len(fo) != 1 or fo[0].delay or fo[0].rate != 1 or fo[0].token_bytes != tb:
+            continue
+        members = (a.id, d, m)
+        fifos = (fc.id, fp.id, fm[0].id, fo[0].id)
+        if any(plan.actor_cond[x] != ALWAYS or plan.extra.get(x, 0) != 0 for x in members) or \
+                any(plan.fifo_cond[f] != ALWAYS for f in fifos):
+            continue
+        out.append(MotionRegion(a.id, d, m, fc.id, fp.id, fm[0].id, fo[0].id, side))
+    return out
+
+
 def is_device(b: ActorBehavior) -> bool:
     return isinstance(b, DeviceBehavior) or bool(getattr(b, "kernel", ""))

@@ -202,3 +202,29 @@ def test_matmul_chain_found_in_bypass_app():
     tap = {"id": "tap", "kind": "static", "behavior": "null_sink", "ports": [port("in", "in")]}
     lin2 = dict(lin, actors=acts + [tap], fifos=fifos + [ff("t", "m2.out", "tap.in")])
     assert chains(lin2) == [(["m1", "m2"], ["b"])]
+
+
+def test_motion_region_found():
+    """plan.find_motion_regions: the motion app's blur -> detect -> clean with
+    f_cur / f_mask internal and f_prev kept; a delay of 2 on f_prev does not
+    match."""
+    from paper_1802_06625_b200.apps import motion
+    from paper_1802_06625_b200.behaviors import resolve
+    from paper_1802_06625_b200.plan import find_motion_regions
+
+    def regions(desc):
+        p = admit(as_graph(desc))
+        behaviors = {}
+        for a in desc["actors"]:
+            b = resolve(a["behavior"])
+            if a["behavior"] != "file_source":
+                b.init(a["id"], a.get("params", {}), None)
+            behaviors[a["id"]] = b
+        return [(m.blur, m.detect, m.clean, m.cur_fifo, m.prev_fifo, m.mask_fifo, m.side)
+                for m in find_motion_regions(p, behaviors)]
+    desc = motion.build_description()
+    assert regions(desc) == [("blur", "detect", "clean", "f_cur", "f_prev", "f_mask", 64)]
+    d2 = dict(desc, fifos=[dict(f, delay=2) if f["id"] == "f_prev" else f
+                           for f in desc["fifos"]])
+    assert regions(d2) == []
+    assert regions(motion.build_description(12)) == []    # not a power-of-two side

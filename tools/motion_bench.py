@@ -26,6 +26,9 @@ FB = SIDE * SIDE
 # the frame and writes f_cur and the delayed f_prev ring; detect reads both
 # and writes the mask; median reads the mask and writes the output
 BYTES_PER_FRAME = (FB + 2 * FB) + (2 * FB + FB) + (FB + FB)
+# the fused region (motion_region_kernel) reads each frame and writes its output;
+# the frame before each CTA's run is read a second time (kMRF = 8 frames per CTA)
+BYTES_PER_FRAME_FUSED = FB + FB + FB / 8
 
 
 def _ref_stream(args):
@@ -42,9 +45,9 @@ def _ref_stream(args):
         return time.perf_counter() - t0
 
 
-def measure(S=256, frames=256, steps=50):
+def measure(S=256, frames=256, steps=50, fuse=1):
     rt = DeviceRuntime(motion.build_description(), config=RuntimeConfig(
-        source_firings=frames, epoch=frames), n_streams=S, seeds=list(range(S)),
+        source_firings=frames, epoch=frames, fuse=bool(fuse)), n_streams=S, seeds=list(range(S)),
         sources={"src": [None] * S})
     st = rt.source_staging("src")
     for s in range(S):
@@ -77,26 +80,32 @@ def measure(S=256, frames=256, steps=50):
     lib.pb_event_elapsed_ms(e0, e1, C.byref(ms))
     step_ms = ms.value / steps
     kern = []
-    evs = marks.get("image", [])
+    evs = marks.get("image", []) or marks.get("motion_region", [])
     for i in range(0, len(evs) - 1, 2):
         lib.pb_event_elapsed_ms(evs[i], evs[i + 1], C.byref(ms))
         kern.append(ms.value)
     per_step_kernels = sum(kern) / steps if kern else float("nan")
-    ops = ["blur", "diff", "median"]   # launch order of one epoch
-    per_op = {op: statistics.mean(kern[k::3]) for k, op in enumerate(ops)} if kern else {}
+    if fuse:
+        per_op = {"motion_region": statistics.mean(kern)} if kern else {}
+    else:
+        ops = ["blur", "diff", "median"]   # launch order of one epoch
+        per_op = {op: statistics.mean(kern[k::3]) for k, op in enumerate(ops)} if kern else {}
+    bpf = BYTES_PER_FRAME_FUSED if fuse else BYTES_PER_FRAME
     n = S * frames
     rt.close()
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-    achieved = n * BYTES_PER_FRAME / (per_step_kernels / 1e3) / 1e9
+    achieved = n * bpf / (per_step_kernels / 1e3) / 1e9
     out = {"metric": "motion frames/s (64x64, blur -> diff -> median, device-resident)",
            "streams": S, "frames_per_stream": frames, "frames_per_step": n,
            "step_ms": step_ms, "frames_per_s": n / (step_ms / 1e3),
            "image_kernels_ms_per_step": per_step_kernels, "kernel_ms": per_op,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                         "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                        "bytes_per_frame": BYTES_PER_FRAME,
-                        "note": "bytes as the unfused graph moves them (three launches); "
-                                "a fused region would move 2 x 4 KiB per frame"}}
+                        "bytes_per_frame": bpf,
+                        "note": "fused region: the frame in, the output out, the frame "
+                                "before each 8-frame run again" if fuse else
+                                "bytes as the unfused graph moves them (three launches)"},
+           "fused_region": bool(fuse)}
     if (ROOT / "oracle" / "_ref").is_dir():
         cores = os.cpu_count() or 1
         ref_frames = 64
