@@ -860,6 +860,96 @@ __host__ __device__ inline size_t plan_par_tails_smem(int n_iter, int nb) {
 // the scan are known -- a branch's history is the tail of the bank input at
 // its previous firing, the same bytes for every branch -- so the gather's
 // round trip overlaps phases 1-2 instead of following them.
+#ifndef PB_PLAN_QUAD   // 1: four threads per span in phase 4 (measured 0.2072 vs 0.2064 ms per
+#define PB_PLAN_QUAD 0    // C2 step: the one-thread form stays the default)
+#endif
+
+// One quarter of the plans of a block's spans (bank_plan_par_kernel phase 4):
+// merged taps t and corrections k with t % 4 == k % 4 == PART, every sum in the
+// order of the one-thread-per-span form.
+template <int PART, bool kTails>
+__device__ __forceinline__ void plan_part(const pb_filter_bank& bank, const pb_resolved& res,
+                                          int64_t B, BankPlan* plan, int s, int E, int lo, int np,
+                                          int i0, int nb, const float4* taps, const float* hist,
+                                          const uint32_t* mask, const int* prev,
+                                          const uint8_t* have, const float* tails,
+                                          const float* stails, int t0, int64_t in_base) {
+  constexpr int NT = (kTaps - PART + 3) / 4, NK = (kHist - PART + 3) / 4;
+  for (int i = i0; i < np; i += kPlanParThreads / 4) {
+    const int n = lo + i;
+    BankPlan& p = plan[(int64_t)s * E + n];
+    if (!have[n]) {
+      if (PART == 0) p.have = 0;
+      continue;
+    }
+    const uint32_t m = mask[n];
+    float4 mt[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) mt[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float cr[NK], ci[NK];
+#pragma unroll
+    for (int j = 0; j < NK; ++j) cr[j] = ci[j] = 0.f;
+    for (int b = 0; b < nb; ++b) {
+      if (!((m >> b) & 1u)) continue;
+      const int pv = prev[b * kPC + i];
+      float h_r[kHist], h_i[kHist];
+      if (!kTails) {
+        const float* h = hist + (i * nb + b) * 2 * kHist;
+#pragma unroll
+        for (int q = 0; q < kHist; ++q) {
+          h_r[q] = h[q];
+          h_i[q] = h[kHist + q];
+        }
+      } else if (pv < 0) {
+        const float* h = stails + b * 2 * kHist;
+#pragma unroll
+        for (int q = 0; q < kHist; ++q) {
+          h_r[q] = h[q];
+          h_i[q] = h[kHist + q];
+        }
+      } else if (pv >= t0) {
+        const float* h = tails + (pv - t0) * 2 * kTailF;
+#pragma unroll
+        for (int q = 0; q < kHist; ++q) {
+          h_r[q] = h[kTailF - kHist + q];
+          h_i[q] = h[kTailF + kTailF - kHist + q];
+        }
+      } else {
+        const float* pvp = reinterpret_cast<const float*>(span_ptr_b(bank.in, in_base, res, s, pv));
+#pragma unroll
+        for (int q = 0; q < kHist; ++q) {
+          h_r[q] = pvp[B - kHist + q];
+          h_i[q] = pvp[2 * B - kHist + q];
+        }
+      }
+      const float4* tb = taps + b * kTaps;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const float4 c = tb[PART + 4 * j];
+        mt[j].x += c.x; mt[j].y += c.y; mt[j].z += c.z; mt[j].w += c.w;
+      }
+#pragma unroll
+      for (int j = 0; j < NK; ++j) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int k = PART + 4 * j;
+#pragma unroll
+        for (int t = k + 1; t < kTaps; ++t) {
+          const float4 c = tb[t];
+          const float xr = h_r[k - t + kHist], xi = h_i[k - t + kHist];
+          cr[j] = __fmaf_rn(-c.y, xi, __fmaf_rn(c.x, xr, cr[j]));
+          ci[j] = __fmaf_rn(c.y, xr, __fmaf_rn(c.x, xi, ci[j]));
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) p.taps[PART + 4 * j] = mt[j];
+#pragma unroll
+    for (int j = 0; j < NK; ++j) p.corr[PART + 4 * j] = make_float2(cr[j], ci[j]);
+    if (PART == 0) p.have = 1;
+  }
+}
+
 template <bool kTails>
 __global__ void __launch_bounds__(kPlanParThreads)
 bank_plan_par_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* plan) {
@@ -1008,8 +1098,22 @@ bank_plan_par_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* 
 #if PB_PLAN_STOP == 3
   return;
 #endif
-  // 4. one thread per span: merged taps and the 9 corrections in registers
-  //    (fully unrolled; a flat (span, slot) split diverges inside warps)
+  // 4. the span plans.  PB_PLAN_QUAD: four threads per span, warp w taking
+  //    part w % 4 -- merged taps t and corrections k with t, k = part (mod 4)
+  //    (the same sums in the same order as one thread per span, so the same
+  //    plan); otherwise one thread per span, everything fully unrolled.
+#if PB_PLAN_QUAD
+  {
+    const int part = warp & 3;
+    const int i0 = (warp >> 2) * 32 + lane;
+    switch (part) {
+      case 0: plan_part<0, kTails>(bank, res, B, plan, s, E, lo, np, i0, nb, taps, hist, mask, prev, have, tails, stails, t0, in_base); break;
+      case 1: plan_part<1, kTails>(bank, res, B, plan, s, E, lo, np, i0, nb, taps, hist, mask, prev, have, tails, stails, t0, in_base); break;
+      case 2: plan_part<2, kTails>(bank, res, B, plan, s, E, lo, np, i0, nb, taps, hist, mask, prev, have, tails, stails, t0, in_base); break;
+      default: plan_part<3, kTails>(bank, res, B, plan, s, E, lo, np, i0, nb, taps, hist, mask, prev, have, tails, stails, t0, in_base); break;
+    }
+  }
+#else
   for (int i = tid; i < np; i += kPlanParThreads) {
     const int n = lo + i;
     BankPlan& p = plan[(int64_t)s * E + n];
@@ -1080,6 +1184,7 @@ bank_plan_par_kernel(pb_filter_bank bank, pb_resolved res, int64_t B, BankPlan* 
     for (int k = 0; k < kHist; ++k) p.corr[k] = make_float2(cr[k], ci[k]);
     p.have = 1;
   }
+#endif
 }
 
 #ifndef PB_MERGED_PT
