@@ -285,9 +285,15 @@ image_fast_kernel(pb_image_actor a, pb_resolved res) {
 // (kMRF per CTA): the word-parallel arithmetic of image_fast_kernel, with the
 // blurred frame and the mask kept in shared memory.
 #ifndef PB_MRF
-#define PB_MRF 8
+#define PB_MRF 16
 #endif
 constexpr int kMRF = PB_MRF;   // frames per CTA (one extra blur per run)
+#ifndef PB_MR_REG
+#define PB_MR_REG 1   // sides 32 / 64: the register form below
+#endif
+#ifndef PB_MR_T64
+#define PB_MR_T64 128   // threads per CTA of the register form at side 64 (8 rows each; 256: 0.377 vs 0.335 ms)
+#endif
 
 template <int LW>
 __device__ __forceinline__ void mr_blur(const uint32_t* fr, uint32_t* hs, uint32_t* out, int tid) {
@@ -401,6 +407,130 @@ motion_region_kernel(pb_motion_region r, pb_resolved res) {
   }
 }
 
+// Register form for sides 32 and 64: thread (band, xw) owns word column xw
+// of R consecutive rows for the whole run, so the blurred frame, the previous
+// one and the mask never leave registers; horizontal neighbours come from
+// warp shuffles, and only the two rows above and below each band cross
+// threads (a double-buffered shared-memory halo, two barriers per frame).
+template <int LW, int T>
+__global__ void __launch_bounds__(T)
+motion_region_reg_kernel(pb_motion_region r, pb_resolved res) {
+  constexpr int W = 1 << LW, side = 4 * W, bands = T / W, R = side / bands;
+  static_assert(R >= 2 && R * bands == side, "register motion region: sides 32, 64");
+  const int s = blockIdx.y, tid = threadIdx.x;
+  const int n0 = blockIdx.x * kMRF, n1 = min(res.n_iter, n0 + kMRF);
+  if (n0 >= res.n_iter) return;
+  const int xw = tid & (W - 1), band = tid >> LW, y0 = band * R;
+  __shared__ uint2 hh[2][bands][4][W];      // blur: rows y0, y0+1, y0+R-2, y0+R-1 of each band
+  __shared__ uint32_t mh[2][bands][2][W];   // mask: rows y0, y0+R-1
+  const int thr = r.threshold;
+  const uint32_t t4 = (uint32_t)min(max(thr, 0), 255) * 0x01010101u;
+  auto fetch = [&](const uint8_t* src, uint32_t (&x)[R]) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) x[j] = reinterpret_cast<const uint32_t*>(src)[(y0 + j) * W + xw];
+  };
+  int hb = 0;   // halo buffer parity
+  // the blur of one frame held in x (every thread takes part: two barriers)
+  auto blur = [&](const uint32_t (&x)[R], uint32_t (&out)[R]) {
+    constexpr uint32_t K4 = 0x04060401u;
+    uint2 h[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      uint32_t wa = __shfl_up_sync(0xffffffffu, x[j], 1, W);
+      uint32_t wc = __shfl_down_sync(0xffffffffu, x[j], 1, W);
+      if (xw == 0) wa = 0u;
+      if (xw == W - 1) wc = 0u;
+      const uint32_t wb = x[j];
+      const uint32_t h0 = __dp4a(__byte_perm(wa, wb, 0x5432), K4, (wb >> 16) & 0xFFu);
+      const uint32_t h1 = __dp4a(__byte_perm(wa, wb, 0x6543), K4, wb >> 24);
+      const uint32_t h2 = __dp4a(wb, K4, wc & 0xFFu);
+      const uint32_t h3 = __dp4a(__byte_perm(wb, wc, 0x4321), K4, (wc >> 8) & 0xFFu);
+      h[j] = make_uint2(h0 | (h1 << 16), h2 | (h3 << 16));
+    }
+    hh[hb][band][0][xw] = h[0];
+    hh[hb][band][1][xw] = h[1];
+    hh[hb][band][2][xw] = h[R - 2];
+    hh[hb][band][3][xw] = h[R - 1];
+    __syncthreads();
+    const uint2 zero = make_uint2(0u, 0u);
+    const uint2 a2 = band > 0 ? hh[hb][band - 1][2][xw] : zero;   // row y0 - 2
+    const uint2 a1 = band > 0 ? hh[hb][band - 1][3][xw] : zero;   // row y0 - 1
+    const uint2 b1 = band < bands - 1 ? hh[hb][band + 1][0][xw] : zero;   // row y0 + R
+    const uint2 b2 = band < bands - 1 ? hh[hb][band + 1][1][xw] : zero;   // row y0 + R + 1
+    hb ^= 1;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int y = y0 + j;
+      uint32_t word = x[j];
+      if (y >= 2 && y < side - 2) {
+        const uint2 r0 = j >= 2 ? h[j - 2] : (j == 1 ? a1 : a2);
+        const uint2 r1 = j >= 1 ? h[j - 1] : a1;
+        const uint2 r3 = j + 1 < R ? h[j + 1] : b1;
+        const uint2 r4 = j + 2 < R ? h[j + 2] : (j + 1 < R ? b1 : b2);
+        const uint2 r2 = h[j];
+        uint32_t lo = r0.x + 4u * r1.x + 6u * r2.x + 4u * r3.x + r4.x;
+        uint32_t hi = r0.y + 4u * r1.y + 6u * r2.y + 4u * r3.y + r4.y;
+        lo = (lo >> 8) & 0x00FF00FFu;
+        hi = (hi >> 8) & 0x00FF00FFu;
+        word = __byte_perm(lo, hi, 0x6420);
+        if (xw == 0) word = __byte_perm(word, x[j], 0x3254);
+        if (xw == W - 1) word = __byte_perm(word, x[j], 0x7610);
+      }
+      out[j] = word;
+    }
+  };
+  uint32_t x[R], xn[R], cur[R], prev[R];
+  if (n0 == 0) {
+    fetch(pb::span_ptr(r.prev_in, res, s, 0), prev);
+  } else {
+    fetch(pb::span_ptr(r.in, res, s, n0 - 1), x);
+    blur(x, prev);
+  }
+  fetch(pb::span_ptr(r.in, res, s, n0), xn);
+  for (int n = n0; n < n1; ++n) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) x[j] = xn[j];
+    if (n + 1 < n1) fetch(pb::span_ptr(r.in, res, s, n + 1), xn);
+    blur(x, cur);
+    uint32_t mk[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      mk[j] = thr < 0 ? 0xFFFFFFFFu : thr >= 255 ? 0u : __vcmpgtu4(__vabsdiffu4(cur[j], prev[j]), t4);
+    if (n == res.n_iter - 1) {   // the next epoch's first "prev"
+      uint32_t* po = reinterpret_cast<uint32_t*>(pb::span_ptr(r.prev_out, res, s, n));
+#pragma unroll
+      for (int j = 0; j < R; ++j) po[(y0 + j) * W + xw] = cur[j];
+    }
+    mh[hb][band][0][xw] = mk[0];
+    mh[hb][band][1][xw] = mk[R - 1];
+    __syncthreads();
+    const uint32_t above = band > 0 ? mh[hb][band - 1][1][xw] : 0u;
+    const uint32_t below = band < bands - 1 ? mh[hb][band + 1][0][xw] : 0u;
+    hb ^= 1;
+    uint32_t* o = reinterpret_cast<uint32_t*>(pb::span_ptr(r.out, res, s, n));
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int y = y0 + j;
+      const uint32_t cw = mk[j];
+      uint32_t pl = __shfl_up_sync(0xffffffffu, cw, 1, W);
+      uint32_t nx = __shfl_down_sync(0xffffffffu, cw, 1, W);
+      uint32_t word = cw;
+      if (y >= 1 && y < side - 1) {
+        const uint32_t up = j > 0 ? mk[j - 1] : above, dn = j + 1 < R ? mk[j + 1] : below;
+        if (xw == 0) pl = 0u;
+        if (xw == W - 1) nx = 0u;
+        const uint32_t lf = __byte_perm(pl, cw, 0x6543), rt = __byte_perm(cw, nx, 0x4321);
+        word = med5(cw, up, dn, lf, rt);
+        if (xw == 0) word = __byte_perm(word, cw, 0x3214);
+        if (xw == W - 1) word = __byte_perm(word, cw, 0x7210);
+      }
+      o[y * W + xw] = word;
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) prev[j] = cur[j];
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -425,8 +555,14 @@ int pb_fire_motion_region(pb_motion_region r, pb_resolved res, void* stream) {
   switch (side) {
     case 8: motion_region_kernel<1><<<grid, kFastThreads, smem, st>>>(r, res); break;
     case 16: motion_region_kernel<2><<<grid, kFastThreads, smem, st>>>(r, res); break;
-    case 32: motion_region_kernel<3><<<grid, kFastThreads, smem, st>>>(r, res); break;
-    case 64: motion_region_kernel<4><<<grid, kFastThreads, smem, st>>>(r, res); break;
+    case 32:
+      if (PB_MR_REG) motion_region_reg_kernel<3, 128><<<grid, 128, 0, st>>>(r, res);
+      else motion_region_kernel<3><<<grid, kFastThreads, smem, st>>>(r, res);
+      break;
+    case 64:
+      if (PB_MR_REG) motion_region_reg_kernel<4, PB_MR_T64><<<grid, PB_MR_T64, 0, st>>>(r, res);
+      else motion_region_kernel<4><<<grid, kFastThreads, smem, st>>>(r, res);
+      break;
     default: motion_region_kernel<5><<<grid, kFastThreads, smem, st>>>(r, res); break;
   }
   PB_LAUNCHED("motion_region_kernel");

@@ -27,8 +27,8 @@ FB = SIDE * SIDE
 # and writes the mask; median reads the mask and writes the output
 BYTES_PER_FRAME = (FB + 2 * FB) + (2 * FB + FB) + (FB + FB)
 # the fused region (motion_region_kernel) reads each frame and writes its output;
-# the frame before each CTA's run is read a second time (kMRF = 8 frames per CTA)
-BYTES_PER_FRAME_FUSED = FB + FB + FB / 8
+# the frame before each CTA run is read a second time (kMRF = 16 frames per CTA)
+BYTES_PER_FRAME_FUSED = FB + FB + FB / 16
 
 
 def _ref_stream(args):
