@@ -87,6 +87,38 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 // ----------------------------------------------------------------- device side
 namespace pb {
 
+// mbarrier phase wait that cannot hang the device: after 5 s of failed
+// try_waits (no pipeline wait in these kernels legitimately lasts longer than a
+// launch) it traps, so a protocol fault becomes a launch error instead of a
+// hung GPU.  One inline loop; %globaltimer is read every 1024 failed tries.
+// SCOPE_CLUSTER: acquire at cluster scope (CTA-pair pipelines).
+#define PB_MBAR_WAIT_TRAP(addr, parity, TRYWAIT)                                   \
+  asm volatile(                                                                   \
+      "{\n\t.reg .pred p, q;\n\t.reg .u64 t0, t1;\n\t.reg .u32 i;\n\t"              \
+      "mov.u32 i, 0;\n\t"                                                          \
+      "mov.u64 t0, %%globaltimer;\n"                                               \
+      "W_%=:\n\t" TRYWAIT " p, [%0], %1;\n\t"                                         \
+      "@p bra D_%=;\n\t"                                                            \
+      "add.u32 i, i, 1;\n\t"                                                        \
+      "and.b32 i, i, 1023;\n\t"                                                     \
+      "setp.ne.u32 q, i, 0;\n\t"                                                    \
+      "@q bra W_%=;\n\t"                                                            \
+      "mov.u64 t1, %%globaltimer;\n\t"                                              \
+      "sub.u64 t1, t1, t0;\n\t"                                                     \
+      "setp.gt.u64 q, t1, 5000000000;\n\t"                                          \
+      "@q trap;\n\t"                                                                \
+      "bra W_%=;\n"                                                                  \
+      "D_%=:\n\t}" ::"r"(addr),                                                     \
+      "r"(parity)                                                                   \
+      : "memory")
+
+__device__ __forceinline__ void mbar_wait_trap(uint32_t addr, uint32_t parity) {
+  PB_MBAR_WAIT_TRAP(addr, parity, "mbarrier.try_wait.parity.shared::cta.b64");
+}
+__device__ __forceinline__ void mbar_wait_trap_cluster(uint32_t addr, uint32_t parity) {
+  PB_MBAR_WAIT_TRAP(addr, parity, "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64");
+}
+
 // wait for the previous kernel of the stream (PDL), then let the next one be
 // scheduled
 __device__ __forceinline__ void pdl_enter() {

@@ -103,40 +103,20 @@ __device__ __forceinline__ void bar_init(uint64_t* bar, int count) {
 __device__ __forceinline__ void bar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(bar)) : "memory");
 }
-// A pipeline wait that cannot hang the device: a phase that has not completed
-// after 5 s of try_waits (no legitimate wait in these kernels is longer than a
-// launch) traps, so a protocol fault surfaces as a launch error, not a hang.
-// One inline loop; the timer is read every 1024 failed tries.
+// pipeline waits trap after 5 s instead of hanging the device (pb_common.cuh);
+// PB_WAIT_TRAP=0 builds the plain spin
 #ifndef PB_WAIT_TRAP
 #define PB_WAIT_TRAP 1
 #endif
 __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
-  if (!PB_WAIT_TRAP) {
-    asm volatile(
-        "{\n\t.reg .pred p;\nW_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(
-            s_u32(bar)),
-        "r"(parity)
-        : "memory");
+  if (PB_WAIT_TRAP) {
+    pb::mbar_wait_trap(s_u32(bar), parity);
     return;
   }
   asm volatile(
-      "{\n\t.reg .pred p, q;\n\t.reg .u64 t0, t1;\n\t.reg .u32 i;\n\t"
-      "mov.u32 i, 0;\n\t"
-      "mov.u64 t0, %%globaltimer;\n"
-      "W_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@p bra D_%=;\n\t"
-      "add.u32 i, i, 1;\n\t"
-      "and.b32 i, i, 1023;\n\t"
-      "setp.ne.u32 q, i, 0;\n\t"
-      "@q bra W_%=;\n\t"
-      "mov.u64 t1, %%globaltimer;\n\t"
-      "sub.u64 t1, t1, t0;\n\t"
-      "setp.gt.u64 q, t1, 5000000000;\n\t"
-      "@q trap;\n\t"
-      "bra W_%=;\n"
-      "D_%=:\n\t}" ::"r"(s_u32(bar)),
+      "{\n\t.reg .pred p;\nW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(
+          s_u32(bar)),
       "r"(parity)
       : "memory");
 }

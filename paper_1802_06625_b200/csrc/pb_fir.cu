@@ -116,13 +116,7 @@ __device__ __forceinline__ void mbar_wait(u64* bar, uint32_t parity) {
         "r"(parity), "r"((uint32_t)PB_FIR_SUSPEND_NS)
         : "memory");
   } else {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
+    pb::mbar_wait_trap(smem_u32(bar), parity);
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, u64* bar) {
