@@ -278,3 +278,22 @@ def test_vision_graph_full_c3_every_frame(i8):
         assert (got.argmax(1)[clear] == want.argmax(1)[clear]).all(), s
     mode = "int8 limbs" if i8 else "bf16x3"
     print(f"worst logit error over {S * firings // 2 * R} frames ({mode}): {worst:.2e}")
+
+
+def test_tile_kernels_still_match(monkeypatch):
+    """PB_CONV_IMPL=tiles: both conv layers on the round-1 tile kernels
+    (bf16x3, TMA tiles, layer 2 on CTA pairs); layer 1's output scales then
+    come from the separate frame_absmax pass (pb_conv_actor.absmax_out) -- the
+    logits stay within the tolerance of the oracle, the bypass marker exact."""
+    monkeypatch.setenv("PB_CONV_IMPL", "tiles")
+    R, firings = 4, 4
+    x = vision.make_frames(2, R * firings)
+    desc = vision.build_description(R)
+    (rep,) = run_streams(desc, 1, RuntimeConfig(source_firings=firings, capture_sinks=True),
+                         seeds=[5], sources={"src": [x.tobytes()]})
+    p = oc.graph_params(desc)
+    logits = np.frombuffer(rep.sink_data["sink"], np.float32).reshape(firings, R, 4)
+    for j in range(0, firings, 2):
+        want = oc.forward(x[j * R:(j + 1) * R], p)["logits"]
+        assert np.abs(logits[j] - want).max() <= LOGIT_TOL
+    assert (logits[1::2] == np.float32(p["marker"])).all()
