@@ -332,6 +332,26 @@ typedef struct {
 } pb_matmul_chain_actor;
 int pb_fire_matmul_chain(pb_matmul_chain_actor actor, pb_resolved res, void* stream);
 
+/* The whole adaptive-bypass region (bypass.py:69-132: route -> matmul chain ->
+ * path_merge, the route's other output straight into the merge's bypass port)
+ * as ONE launch: per merge firing the live path is read once -- the chain's
+ * input through its layers (pb_fire_matmul_chain's arithmetic) or the bypass
+ * token plus the marker (PathMerge.fire) -- and written to the merge's output;
+ * the chain's link channels and its output channel are not materialised.  A
+ * firing with != 1 live path sets *error_flag.  N = 8. */
+typedef struct {
+  pb_span_ref chain_in;   /* the chain's first input channel (consumer side) */
+  pb_span_ref bypass_in;  /* the merge's bypass input channel (consumer side) */
+  pb_span_ref out;        /* the merge's output channel (producer side) */
+  const float* weights;   /* device [layers][8][8] */
+  int32_t layers;
+  int32_t chain_live;     /* condition of the chain's output channel (its path is live) */
+  int32_t cond;           /* the merge's activity condition */
+  float marker;
+  int32_t* error_flag;
+} pb_bypass_region;
+int pb_fire_bypass_region(pb_bypass_region region, pb_resolved res, void* stream);
+
 /* path_merge (bypass.py:52-66): exactly one live input is forwarded; the
  * marker is added when it is the bypass port.  A firing with != 1 live input
  * sets *error_flag (device int32) -> ActorPanic. */

@@ -116,6 +116,12 @@ class ImageActor(C.Structure):
 PB_IMG_BLUR, PB_IMG_DIFF, PB_IMG_MEDIAN = 0, 1, 2
 
 
+class BypassRegion(C.Structure):
+    _fields_ = [("chain_in", SpanRef), ("bypass_in", SpanRef), ("out", SpanRef), ("weights", vp),
+                ("layers", i32), ("chain_live", i32), ("cond", i32), ("marker", C.c_float),
+                ("error_flag", vp)]
+
+
 class MotionRegion(C.Structure):
     _fields_ = [("in_", SpanRef), ("prev_in", SpanRef), ("prev_out", SpanRef), ("out", SpanRef),
                 ("side", i32), ("threshold", i32)]
@@ -200,6 +206,7 @@ SIGNATURES = {
     "pb_fire_matmul": (C.c_int, [MatmulActor, Resolved, vp]),
     "pb_fire_matmul_chain": (C.c_int, [MatmulChainActor, Resolved, vp]),
     "pb_fire_motion_region": (C.c_int, [MotionRegion, Resolved, vp]),
+    "pb_fire_bypass_region": (C.c_int, [BypassRegion, Resolved, vp]),
     "pb_fire_path_merge": (C.c_int, [PathMergeActor, Resolved, vp]),
     "pb_fire_image": (C.c_int, [ImageActor, Resolved, vp]),
     "pb_fire_conv_pool": (C.c_int, [ConvActor, Resolved, vp]),

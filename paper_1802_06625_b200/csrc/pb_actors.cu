@@ -257,6 +257,96 @@ matmul_chain_kernel(pb_matmul_chain_actor a, pb_resolved res) {
   }
 }
 
+// The fused bypass region (pb_bypass_region): the chain kernel's layout, one
+// lane group per merge firing; the leader resolves the live path once.
+__global__ void __launch_bounds__(256)
+bypass_region_kernel(pb_bypass_region a, pb_resolved res) {
+  constexpr int N = 8, L = 16;
+  const int s = blockIdx.y, lane = threadIdx.x & 31;
+  __shared__ float w[kChainMax * N * N];
+  for (int e = threadIdx.x; e < a.layers * N * N; e += blockDim.x) w[e] = a.weights[e];
+  __syncthreads();
+  const int g = lane / L, sub = lane - g * L;
+  const int j0 = (((int)blockIdx.x * 8 + (threadIdx.x >> 5)) * 2 + g) * kCMF;
+  const int leader = g * L;
+  const unsigned grp = 0xFFFFu << leader;
+  const int cnt = pb::cond_count(res, a.cond, s);
+  if (j0 >= cnt) return;   // whole lane groups leave together
+  const float* x[kCMF];
+  float* out[kCMF];
+  int path[kCMF];   // 0 none, 1 chain, 2 bypass
+#pragma unroll
+  for (int f = 0; f < kCMF; ++f) {
+    x[f] = nullptr;
+    out[f] = nullptr;
+    path[f] = 0;
+    if (sub == 0 && j0 + f < cnt) {
+      const int n = pb::firing_iter(res, a.cond, s, j0 + f);
+      const bool ch = pb::active(res, a.chain_live, s, n);
+      const bool by = pb::active(res, a.bypass_in.act_cond, s, n);
+      if (ch == by) {
+        atomicExch(a.error_flag, 1);
+      } else {
+        path[f] = ch ? 1 : 2;
+        x[f] = reinterpret_cast<const float*>(pb::span_ptr(ch ? a.chain_in : a.bypass_in, res, s, n));
+        out[f] = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
+      }
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < kCMF; ++f) {
+    path[f] = __shfl_sync(grp, path[f], leader);
+    x[f] = reinterpret_cast<const float*>(
+        __shfl_sync(grp, reinterpret_cast<unsigned long long>(x[f]), leader));
+    out[f] = reinterpret_cast<float*>(
+        __shfl_sync(grp, reinterpret_cast<unsigned long long>(out[f]), leader));
+  }
+  const int i = sub >> 1, cb = sub & 1;   // row i, columns 4 cb .. 4 cb + 3
+  float4 col[kCMF][N];
+#pragma unroll
+  for (int f = 0; f < kCMF; ++f)
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+      col[f][k] = path[f] == 1 ? __ldg(reinterpret_cast<const float4*>(x[f] + k * N) + cb)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int f = 0; f < kCMF; ++f) {
+    if (path[f] != 2) continue;   // bypass: the token plus the marker (PathMerge.fire)
+    float4 v = __ldg(reinterpret_cast<const float4*>(x[f]) + sub);
+    v.x = __fadd_rn(v.x, a.marker); v.y = __fadd_rn(v.y, a.marker);
+    v.z = __fadd_rn(v.z, a.marker); v.w = __fadd_rn(v.w, a.marker);
+    reinterpret_cast<float4*>(out[f])[sub] = v;
+  }
+  for (int l = 0; l < a.layers; ++l) {
+    const float* wl = w + l * N * N + i * N;
+#pragma unroll
+    for (int f = 0; f < kCMF; ++f) {
+      if (path[f] != 1) continue;   // uniform within the lane group
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const float wk = wl[k];
+        acc[0] = __fadd_rn(acc[0], __fmul_rn(wk, col[f][k].x));
+        acc[1] = __fadd_rn(acc[1], __fmul_rn(wk, col[f][k].y));
+        acc[2] = __fadd_rn(acc[2], __fmul_rn(wk, col[f][k].z));
+        acc[3] = __fadd_rn(acc[3], __fmul_rn(wk, col[f][k].w));
+      }
+      if (l + 1 == a.layers) {
+        reinterpret_cast<float4*>(out[f])[sub] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const int src = leader + 2 * k + cb;
+          col[f][k].x = __shfl_sync(grp, acc[0], src);
+          col[f][k].y = __shfl_sync(grp, acc[1], src);
+          col[f][k].z = __shfl_sync(grp, acc[2], src);
+          col[f][k].w = __shfl_sync(grp, acc[3], src);
+        }
+      }
+    }
+  }
+}
+
 // Packed form for tokens of 16..512 bytes in 16-byte units (the reference's
 // 256-B matrices: 16 lanes per firing, two firings per warp): the first lane
 // of each firing's lane group resolves the firing (activity, live input,
@@ -377,6 +467,17 @@ int pb_fire_matmul_chain(pb_matmul_chain_actor actor, pb_resolved res, void* str
   dim3 grid((unsigned)((res.n_iter + per_cta - 1) / per_cta), res.n_streams);
   matmul_chain_kernel<<<grid, 256, 0, pb::as_stream(stream)>>>(actor, res);
   PB_LAUNCHED("matmul_chain_kernel");
+  return PB_OK;
+}
+
+int pb_fire_bypass_region(pb_bypass_region r, pb_resolved res, void* stream) {
+  if (res.n_iter == 0) return PB_OK;
+  if (r.layers < 1 || r.layers > kChainMax)
+    return pb::fail(PB_E_UNSUPPORTED, "bypass region: 1..8 matmul layers");
+  const int per_cta = 8 * 2 * kCMF;
+  dim3 grid((unsigned)((res.n_iter + per_cta - 1) / per_cta), res.n_streams);
+  bypass_region_kernel<<<grid, 256, 0, pb::as_stream(stream)>>>(r, res);
+  PB_LAUNCHED("bypass_region_kernel");
   return PB_OK;
 }
 

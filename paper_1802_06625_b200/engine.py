@@ -44,8 +44,8 @@ from .behaviors import (ActorBehavior, DeviceBehavior, FileSource, FireContext, 
                         decode_control, native_policy_kind, resolve)
 from .errors import ActorPanic, DeviceUnavailable, Timeout, UnsupportedGraph
 from .graph import CONTROL_IN, CONTROL_OUT, DRP, Graph, PortRef, as_graph
-from .plan import (ALWAYS, ExecPlan, admit, find_filter_banks, find_matmul_chains,
-                   find_motion_regions, is_device)
+from .plan import (ALWAYS, ExecPlan, admit, find_bypass_regions, find_filter_banks,
+                   find_matmul_chains, find_motion_regions, is_device)
 
 
 @dataclass
@@ -293,11 +293,17 @@ class DeviceRuntime:
         self.motions = [m for m in find_motion_regions(plan, self.behaviors[0])
                         if not ({m.blur, m.detect, m.clean} & set(self.host_fired))] \
             if config.fuse else []
+        # a chain between a route and a path_merge whose other input is the
+        # route's other output: the whole bypass region as one launch
+        self.bypasses = [b for b in find_bypass_regions(plan, self.behaviors[0], self.chains)
+                         if not ({b.route, b.merge} & set(self.host_fired))]
         self.fused_actors = {a for grp in self.banks for a in [grp.router, *grp.branches]}
         self.fused_actors |= {a for c in self.chains for a in c.actors[1:]}
+        self.fused_actors |= {b.merge for b in self.bypasses}
         self.fused_actors |= {a for m in self.motions for a in (m.detect, m.clean)}
         self.virtual = {fid for grp in self.banks for fid in grp.internal_fifos}
         self.virtual |= {fid for c in self.chains for fid in c.internal_fifos}
+        self.virtual |= {b.chain_out for b in self.bypasses}
         self.virtual |= {fid for m in self.motions for fid in (m.cur_fifo, m.mask_fifo)}
         self._allocate()
         self.launches, self.fir_groups = self._build_launches()
@@ -506,6 +512,7 @@ class DeviceRuntime:
         done: set[str] = set()
         bank_at = {grp.combiner: grp for grp in self.banks}
         chain_at = {c.actors[0]: c for c in self.chains}
+        bypass_at = {b.chain.actors[0]: b for b in self.bypasses}
         motion_at = {m.blur: m for m in self.motions}
         # topological depth so independent FIR actors share a launch (the
         # delayed channels inside cycles do not order an epoch's firings)
@@ -579,6 +586,24 @@ class DeviceRuntime:
                                         int(g.actor(m.detect).params.get("threshold", 16)))
                 launches.append(("motion_region", act))
                 done.update({m.blur, m.detect, m.clean})
+                continue
+            if aid in bypass_at:
+                bp = bypass_at[aid]
+                c = bp.chain
+                x = g.actor(c.actors[0])
+                fin = g.fifo_into(PortRef(x.id, x.data_inputs[0].id))
+                w = np.concatenate([np.array(g.actor(m).params["w"], dtype=np.float32)
+                                    for m in c.actors])
+                mg = g.actor(bp.merge)
+                act = _lib.BypassRegion(self._ref(fin.id), self._ref(bp.bypass_fifo),
+                                        self._ref(bp.out_fifo, producer=True), self.mem.upload(w),
+                                        len(c.actors), plan.fifo_cond[bp.chain_out],
+                                        cond_of(bp.merge),
+                                        float(np.float32(mg.params.get("marker", 0.5))),
+                                        self.err_flag)
+                launches.append(("bypass_region", act))
+                done.update(c.actors)
+                done.add(bp.merge)
                 continue
             if aid in chain_at:
                 c = chain_at[aid]
@@ -1139,6 +1164,8 @@ class DeviceRuntime:
                 _lib.check(lib.pb_fire_matmul(item[1], res, st), "matmul")
             elif kind == "matmul_chain":
                 _lib.check(lib.pb_fire_matmul_chain(item[1], res, st), "matmul chain")
+            elif kind == "bypass_region":
+                _lib.check(lib.pb_fire_bypass_region(item[1], res, st), "bypass region")
             elif kind == "motion_region":
                 _lib.check(lib.pb_fire_motion_region(item[1], res, st), "motion region")
             elif kind == "path_merge":

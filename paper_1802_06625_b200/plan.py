@@ -464,6 +464,56 @@ def find_matmul_chains(plan: ExecPlan, behaviors: dict[str, ActorBehavior]) -> l
 
 
 @dataclass
+class BypassRegion:
+    """route -> matmul chain -> path_merge, the route's other output straight
+    into the merge's bypass port (bypass.py:69-132), fired as one kernel."""
+
+    chain: MatmulChain
+    route: str
+    merge: str
+    chain_out: str       # the chain's output channel into the merge (not materialised)
+    bypass_fifo: str     # route -> merge bypass channel
+    out_fifo: str        # the merge's output channel
+
+
+def find_bypass_regions(plan: ExecPlan, behaviors: dict[str, ActorBehavior],
+                        chains: list[MatmulChain]) -> list[BypassRegion]:
+    g = plan.graph
+    kern = lambda aid: getattr(behaviors.get(aid), "kernel", None)
+    out = []
+    for c in chains:
+        head, tail = g.actor(c.actors[0]), g.actor(c.actors[-1])
+        f_in = g.fifo_into(PortRef(head.id, head.data_inputs[0].id))
+        r = g.actor(f_in.src.actor)
+        if kern(r.id) != "route" or len(r.data_inputs) != 1 or len(r.output_ports) != 2 or \
+                any(p.kind != DRP for p in r.output_ports) or f_in.delay:
+            continue
+        fo = g.fifos_from(PortRef(tail.id, tail.output_ports[0].id))
+        if len(fo) != 1 or fo[0].delay:
+            continue
+        m = g.actor(fo[0].dst.actor)
+        bport = m.params.get("bypass_port", "")
+        if kern(m.id) != "path_merge" or len(m.data_inputs) != 2 or fo[0].dst.port == bport \
+                or len(m.output_ports) != 1:
+            continue
+        other = [p for p in r.output_ports if p.id != f_in.src.port]
+        fb = g.fifos_from(PortRef(r.id, other[0].id))
+        if len(fb) != 1 or fb[0].dst != PortRef(m.id, bport) or fb[0].delay:
+            continue
+        fm = g.fifos_from(PortRef(m.id, m.output_ports[0].id))
+        if len(fm) != 1 or fm[0].delay:
+            continue
+        src = g.fifo_into(PortRef(r.id, r.data_inputs[0].id))
+        span = src.rate * src.token_bytes
+        if any(f.rate * f.token_bytes != span for f in (f_in, fo[0], fb[0], fm[0])) or span != 256:
+            continue
+        if plan.extra.get(m.id, 0) != 0 or plan.extra.get(r.id, 0) != 0:
+            continue
+        out.append(BypassRegion(c, r.id, m.id, fo[0].id, fb[0].id, fm[0].id))
+    return out
+
+
+@dataclass
 class MotionRegion:
     """blur -> frame_diff_threshold (cur, prev delayed one frame) -> plus_median
     fired as one kernel (pb_fire_motion_region)."""

@@ -48,8 +48,45 @@ def test_bypass_chain_fused_and_unfused(golden, tmp_path, fuse):
     assert rep.firing_counts == g["firing_counts"]
     rt = DeviceRuntime(desc, config=cfg, n_streams=1, seeds=[5])
     kinds = [item[0] for item in rt.launches]
-    assert ("matmul_chain" in kinds) == fuse and ("matmul" in kinds) != fuse
+    # fused: the whole route -> chain -> path_merge region is one launch
+    assert kinds == (["bypass_region"] if fuse else ["matmul"] * 3 + ["path_merge"])
     rt.close()
+
+
+def test_static_matmul_chain_kernel():
+    """A matmul chain outside a bypass region (src -> m1 -> m2 -> m3 -> sink)
+    fires as matmul_chain_kernel, bit-identical to the layer-by-layer launches."""
+    import numpy as np
+    from paper_1802_06625_b200 import run_streams
+    from paper_1802_06625_b200.apps.bypass import layer_weights
+    from paper_1802_06625_b200.engine import DeviceRuntime
+
+    def port(pid, d):
+        return {"id": pid, "dir": d, "kind": "srp", "rate": 1}
+    acts = [{"id": "src", "kind": "static", "behavior": "file_source", "params": {"path": "x"},
+             "ports": [port("out", "out")]},
+            {"id": "sink", "kind": "static", "behavior": "null_sink", "ports": [port("in", "in")]}]
+    acts += [{"id": f"m{k}", "kind": "static", "behavior": "matmul",
+              "params": {"w": layer_weights(k)}, "ports": [port("in", "in"), port("out", "out")]}
+             for k in (1, 2, 3)]
+
+    def ff(fid, src, dst):
+        return {"id": fid, "src": src, "dst": dst, "rate": 1, "delay": 0, "token_bytes": 256}
+    desc = {"name": "lin", "actors": acts, "control": {},
+            "fifos": [ff("a", "src.out", "m1.in"), ff("b", "m1.out", "m2.in"),
+                      ff("c", "m2.out", "m3.in"), ff("d", "m3.out", "sink.in")]}
+    F = 50
+    x = np.random.default_rng(4).uniform(-1, 1, (F, 8, 8)).astype(np.float32)
+    outs = {}
+    for fuse in (True, False):
+        cfg = RuntimeConfig(source_firings=F, capture_sinks=True, fuse=fuse)
+        (rep,) = run_streams(desc, 1, cfg, sources={"src": [x.tobytes()]})
+        outs[fuse] = rep.sink_data["sink"]
+        rt = DeviceRuntime(desc, config=cfg, n_streams=1, sources={"src": [x.tobytes()]})
+        kinds = [item[0] for item in rt.launches]
+        assert kinds == (["matmul_chain"] if fuse else ["matmul"] * 3)
+        rt.close()
+    assert outs[True] == outs[False]
 
 
 def test_matmul_chain_layers_exact(tmp_path):

@@ -228,3 +228,23 @@ def test_motion_region_found():
                            for f in desc["fifos"]])
     assert regions(d2) == []
     assert regions(motion.build_description(12)) == []    # not a power-of-two side
+
+
+def test_bypass_region_found():
+    """plan.find_bypass_regions: the bypass app's fork -> l1..l3 -> join with
+    the f_bypass edge; the chain's output channel f_chain is internal."""
+    from paper_1802_06625_b200.apps import bypass
+    from paper_1802_06625_b200.behaviors import resolve
+    from paper_1802_06625_b200.plan import find_bypass_regions, find_matmul_chains
+    desc = bypass.build_description("x.bin")
+    p = admit(as_graph(desc))
+    behaviors = {}
+    for a in desc["actors"]:
+        b = resolve(a["behavior"])
+        if a["behavior"] != "file_source":
+            b.init(a["id"], a.get("params", {}), None)
+        behaviors[a["id"]] = b
+    regions = find_bypass_regions(p, behaviors, find_matmul_chains(p, behaviors))
+    assert [(r.route, r.merge, r.chain.actors, r.chain_out, r.bypass_fifo, r.out_fifo)
+            for r in regions] == [("fork", "join", ["l1", "l2", "l3"], "f_chain", "f_bypass",
+                                   "f_out")]

@@ -85,11 +85,12 @@ def measure(S=1024, mats=1024, steps=50, fuse=1):
            "kernel_ms_per_step": per_kind,
            "note": "half the firings run l1 -> l2 -> l3 (3 x 512 rounded mul/add per matrix), "
                    "half the bypass; tokens are 256-B matrices in rings"}
-    # algorithmic HBM bytes per matrix: fused, a chain firing reads its matrix
-    # and writes l3's (the link channels stay in registers) and the merge
-    # moves 512 B; unfused, each of the 3 matmuls moves 512 B; a bypass firing
-    # moves 512 B in the merge (route aliases its input)
-    per = (512 + 512 + 512) / 2 if fuse else (3 * 512 + 512 + 512) / 2
+    # algorithmic HBM bytes per matrix: unfused, each of the 3 matmuls moves
+    # 512 B and the merge 512 B; a bypass firing moves 512 B in the merge
+    # (route aliases its input)
+    # the fused region (bypass_region_kernel) reads each firing's live token
+    # once and writes the merge output: 512 B whichever path is live
+    per = 512 if fuse else (3 * 512 + 512 + 512) / 2
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs") \
         if (ROOT / "MEASURED_PEAKS.json").exists() else 6555.5
     out["fused_chain"] = bool(fuse)
