@@ -414,13 +414,18 @@ def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
 
     S, F, R = args.cnn_streams, args.cnn_firings, CNN_FRAMES_PER_FIRING
     desc = vision.build_description(R, policy="fixed_policy")
+    # the caller's frames: one ordinary (pageable) numpy array [S][F*R][96][96][3]
+    # whose rows are the streams' sources (page-locked in place on first use,
+    # DMA'd straight into the rings), and the same frames in the runtime's own
+    # pinned staging buffer for the device-resident steps
+    X = np.stack([vision.make_frames(rank * S + s, F * R) for s in range(S)])
     rt = DeviceRuntime(desc, config=RuntimeConfig(source_firings=F, epoch=F, device=local,
                                                   capture_sinks=True),
                        n_streams=S, seeds=[rank * S + s for s in range(S)],
-                       sources={"src": [None] * S})
+                       sources={"src": list(X)})
     stage = rt.source_staging("src")
     for s in range(S):
-        stage[s] = vision.make_frames(rank * S + s, F * R).reshape(F, -1).view(np.uint8)
+        stage[s] = X[s].reshape(F, -1).view(np.uint8)
     lib = rt.lib
 
     def ev():
@@ -479,16 +484,21 @@ def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
     frames = S * F * R
     value = frames * world / (step_ms / 1e3)
 
-    # end to end: pinned host frames -> logits on the host (+ digests)
-    e2e_t = []
-    for k in range(args.cnn_e2e_steps + 1 if args.cnn_e2e_steps > 0 else 0):
-        barrier()
-        t0 = time.perf_counter()
-        reps = rt.run_all(prestaged=True)
-        t1 = time.perf_counter()
-        if k:
-            e2e_t.append(max_over_ranks(t1 - t0))
-    e2e_s = statistics.median(e2e_t) if e2e_t else float("nan")
+    # end to end: the caller's frames -> logits on the host (+ digests); the
+    # first (untimed) run page-locks X in place; prestaged: from the runtime's
+    # pinned staging buffer
+    def e2e_runs(prestaged):
+        ts, out = [], None
+        for k in range(args.cnn_e2e_steps + 1 if args.cnn_e2e_steps > 0 else 0):
+            barrier()
+            t0 = time.perf_counter()
+            out = rt.run_all(prestaged=prestaged)
+            t1 = time.perf_counter()
+            if k:
+                ts.append(max_over_ranks(t1 - t0))
+        return (statistics.median(ts) if ts else float("nan")), out, ts
+    e2e_pre_s, _, _ = e2e_runs(True)
+    e2e_s, reps, e2e_t = e2e_runs(False)
     parity = None
     if rank == 0 and e2e_t:
         from oracle import cnn as oc
@@ -610,8 +620,12 @@ def cnn_leg(args, rank, world, local, barrier, max_over_ranks, peaks):
                 "h2d_bytes_per_step": frames * vision.FRAME_BYTES,
                 "d2h_bytes_per_step": frames * vision.N_CLASSES * 4,
                 "seconds_per_step": e2e_s,
-                "includes": "H2D pinned frames, native control actor, device firings, "
-                            "logits D2H, SHA-256 per stream"},
+                "includes": "DeviceRuntime.run_all() with sources = rows of the caller's numpy "
+                            "array (page-locked in place on first use, DMA straight into the "
+                            "rings), native control actor, device firings, logits D2H, "
+                            "SHA-256 per stream",
+                "prestaged": {"value": frames * world / e2e_pre_s, "seconds_per_step": e2e_pre_s,
+                              "includes": "the same from the runtime's pinned staging buffer"}},
         "gpu_launches": launches,
         "adaptive": {"value": frames * world / (adaptive_ms / 1e3), "unit": "frames/s",
                      "ms_per_step": adaptive_ms,
