@@ -173,29 +173,23 @@ matmul_packed_kernel(pb_matmul_actor a, pb_resolved res, int L) {
   }
 }
 
-// A fused chain of 8x8 matmul layers (pb_matmul_chain_actor): the layout of
-// matmul_packed_kernel (16 lanes per firing, lane = (row i, column block cb),
-// 4 outputs each, kMF firings per lane group) with the layer's result handed
-// to the next layer through registers: the next layer's lane (i, cb) needs
-// column block cb of every row k, i.e. the float4 lane (k, cb) holds -- eight
-// shuffles of a float4 per layer.  Same products and sums in the same order
-// as one matmul_packed_kernel launch per layer.
+// A fused chain of 8x8 matmul layers (pb_matmul_chain_actor), in the column
+// form of bypass_region_kernel below: lane j of an 8-lane group carries column
+// j of its firing through every layer in registers.  Same products and sums
+// in the same order as one matmul_packed_kernel launch per layer.
 constexpr int kChainMax = 8;
-#ifndef PB_CHAIN_MF
-#define PB_CHAIN_MF 2
-#endif
-constexpr int kCMF = PB_CHAIN_MF;   // firings per lane group (32 floats of x each)
+constexpr int kCMF = 2;   // firings per 8-lane group
 __global__ void __launch_bounds__(256)
 matmul_chain_kernel(pb_matmul_chain_actor a, pb_resolved res) {
-  constexpr int N = 8, L = 16;
+  constexpr int N = 8;
   const int s = blockIdx.y, lane = threadIdx.x & 31;
   __shared__ float w[kChainMax * N * N];
   for (int e = threadIdx.x; e < a.layers * N * N; e += blockDim.x) w[e] = a.weights[e];
   __syncthreads();
-  const int g = lane / L, sub = lane - g * L;
-  const int j0 = (((int)blockIdx.x * 8 + (threadIdx.x >> 5)) * 2 + g) * kCMF;
-  const int leader = g * L;
-  const unsigned grp = 0xFFFFu << leader;
+  const int g = lane >> 3, j = lane & 7;
+  const int j0 = (((int)blockIdx.x * 8 + (threadIdx.x >> 5)) * 4 + g) * kCMF;
+  const int leader = g * 8;
+  const unsigned grp = 0xFFu << leader;
   const int cnt = pb::cond_count(res, a.cond, s);
   if (j0 >= cnt) return;   // whole lane groups leave together
   const float* x[kCMF];
@@ -204,7 +198,7 @@ matmul_chain_kernel(pb_matmul_chain_actor a, pb_resolved res) {
   for (int f = 0; f < kCMF; ++f) {
     x[f] = nullptr;
     out[f] = nullptr;
-    if (sub == 0 && j0 + f < cnt) {
+    if (j == 0 && j0 + f < cnt) {
       const int n = pb::firing_iter(res, a.cond, s, j0 + f);
       x[f] = reinterpret_cast<const float*>(pb::span_ptr(a.in, res, s, n));
       out[f] = reinterpret_cast<float*>(pb::span_ptr(a.out, res, s, n));
@@ -217,70 +211,65 @@ matmul_chain_kernel(pb_matmul_chain_actor a, pb_resolved res) {
     out[f] = reinterpret_cast<float*>(
         __shfl_sync(grp, reinterpret_cast<unsigned long long>(out[f]), leader));
   }
-  const int i = sub >> 1, cb = sub & 1;   // row i, columns 4 cb .. 4 cb + 3
-  // every lane of the group loads the column block cb of all 8 rows
-  float4 col[kCMF][N];
+  float c[kCMF][N];
 #pragma unroll
   for (int f = 0; f < kCMF; ++f)
 #pragma unroll
-    for (int k = 0; k < N; ++k)
-      col[f][k] = x[f] != nullptr ? __ldg(reinterpret_cast<const float4*>(x[f] + k * N) + cb)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int l = 0; l < a.layers; ++l) {
-    const float* wl = w + l * N * N + i * N;
+    for (int k = 0; k < N; ++k) c[f][k] = x[f] != nullptr ? __ldg(x[f] + k * N + j) : 0.f;
 #pragma unroll
-    for (int f = 0; f < kCMF; ++f) {
-      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  for (int f = 0; f < kCMF; ++f) {
+    if (x[f] == nullptr) continue;
+    for (int l = 0; l < a.layers; ++l) {
+      const float* wl = w + l * N * N;
+      float y[N];
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        const float wk = wl[k];
-        acc[0] = __fadd_rn(acc[0], __fmul_rn(wk, col[f][k].x));
-        acc[1] = __fadd_rn(acc[1], __fmul_rn(wk, col[f][k].y));
-        acc[2] = __fadd_rn(acc[2], __fmul_rn(wk, col[f][k].z));
-        acc[3] = __fadd_rn(acc[3], __fmul_rn(wk, col[f][k].w));
+      for (int i = 0; i < N; ++i) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k < N; ++k) acc = __fadd_rn(acc, __fmul_rn(wl[i * N + k], c[f][k]));
+        y[i] = acc;
       }
-      if (l + 1 == a.layers) {
-        if (x[f] != nullptr)
-          reinterpret_cast<float4*>(out[f])[sub] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      } else {
-        // row k of the next input, column block cb, lives in lane 2 k + cb
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-          const int src = leader + 2 * k + cb;
-          col[f][k].x = __shfl_sync(grp, acc[0], src);
-          col[f][k].y = __shfl_sync(grp, acc[1], src);
-          col[f][k].z = __shfl_sync(grp, acc[2], src);
-          col[f][k].w = __shfl_sync(grp, acc[3], src);
-        }
-      }
+      for (int i = 0; i < N; ++i) c[f][i] = y[i];
     }
+#pragma unroll
+    for (int k = 0; k < N; ++k) out[f][k * N + j] = c[f][k];
   }
 }
 
-// The fused bypass region (pb_bypass_region): the chain kernel's layout, one
-// lane group per merge firing; the leader resolves the live path once.
+// The fused bypass region (pb_bypass_region).  Column form: output column j
+// of W x depends only on input column j, so lane j of an 8-lane group carries
+// column j of its firing through every layer in registers (no exchange between
+// lanes, ~30 registers: many firings in flight per SM, which is what a
+// latency-bound per-firing kernel needs); each row load / store of the group
+// is 32 contiguous bytes.  kBMF firings per group, resolved together by the
+// group's first lane.  Same products and sums in the same order as MatMul.fire.
+#ifndef PB_BYPASS_MF
+#define PB_BYPASS_MF 2   // firings per 8-lane group (2: 5.6, 4: 5.2, 8: 4.5 G matrices/s)
+#endif
+constexpr int kBMF = PB_BYPASS_MF;
 __global__ void __launch_bounds__(256)
 bypass_region_kernel(pb_bypass_region a, pb_resolved res) {
-  constexpr int N = 8, L = 16;
+  constexpr int N = 8;
   const int s = blockIdx.y, lane = threadIdx.x & 31;
   __shared__ float w[kChainMax * N * N];
   for (int e = threadIdx.x; e < a.layers * N * N; e += blockDim.x) w[e] = a.weights[e];
   __syncthreads();
-  const int g = lane / L, sub = lane - g * L;
-  const int j0 = (((int)blockIdx.x * 8 + (threadIdx.x >> 5)) * 2 + g) * kCMF;
-  const int leader = g * L;
-  const unsigned grp = 0xFFFFu << leader;
+  const int g = lane >> 3, j = lane & 7;   // group of the warp, column
+  const int j0 = (((int)blockIdx.x * 8 + (threadIdx.x >> 5)) * 4 + g) * kBMF;
+  const int leader = g * 8;
+  const unsigned grp = 0xFFu << leader;
   const int cnt = pb::cond_count(res, a.cond, s);
   if (j0 >= cnt) return;   // whole lane groups leave together
-  const float* x[kCMF];
-  float* out[kCMF];
-  int path[kCMF];   // 0 none, 1 chain, 2 bypass
+  const float* x[kBMF];
+  float* out[kBMF];
+  int path[kBMF];   // 0 none, 1 chain, 2 bypass
 #pragma unroll
-  for (int f = 0; f < kCMF; ++f) {
+  for (int f = 0; f < kBMF; ++f) {
     x[f] = nullptr;
     out[f] = nullptr;
     path[f] = 0;
-    if (sub == 0 && j0 + f < cnt) {
+    if (j == 0 && j0 + f < cnt) {
       const int n = pb::firing_iter(res, a.cond, s, j0 + f);
       const bool ch = pb::active(res, a.chain_live, s, n);
       const bool by = pb::active(res, a.bypass_in.act_cond, s, n);
@@ -294,55 +283,39 @@ bypass_region_kernel(pb_bypass_region a, pb_resolved res) {
     }
   }
 #pragma unroll
-  for (int f = 0; f < kCMF; ++f) {
+  for (int f = 0; f < kBMF; ++f) {
     path[f] = __shfl_sync(grp, path[f], leader);
     x[f] = reinterpret_cast<const float*>(
         __shfl_sync(grp, reinterpret_cast<unsigned long long>(x[f]), leader));
     out[f] = reinterpret_cast<float*>(
         __shfl_sync(grp, reinterpret_cast<unsigned long long>(out[f]), leader));
   }
-  const int i = sub >> 1, cb = sub & 1;   // row i, columns 4 cb .. 4 cb + 3
-  float4 col[kCMF][N];
+  float c[kBMF][N];   // column j of each firing's token
 #pragma unroll
-  for (int f = 0; f < kCMF; ++f)
+  for (int f = 0; f < kBMF; ++f)
 #pragma unroll
-    for (int k = 0; k < N; ++k)
-      col[f][k] = path[f] == 1 ? __ldg(reinterpret_cast<const float4*>(x[f] + k * N) + cb)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < N; ++k) c[f][k] = path[f] ? __ldg(x[f] + k * N + j) : 0.f;
 #pragma unroll
-  for (int f = 0; f < kCMF; ++f) {
-    if (path[f] != 2) continue;   // bypass: the token plus the marker (PathMerge.fire)
-    float4 v = __ldg(reinterpret_cast<const float4*>(x[f]) + sub);
-    v.x = __fadd_rn(v.x, a.marker); v.y = __fadd_rn(v.y, a.marker);
-    v.z = __fadd_rn(v.z, a.marker); v.w = __fadd_rn(v.w, a.marker);
-    reinterpret_cast<float4*>(out[f])[sub] = v;
-  }
-  for (int l = 0; l < a.layers; ++l) {
-    const float* wl = w + l * N * N + i * N;
+  for (int f = 0; f < kBMF; ++f) {
+    if (path[f] == 2) {   // bypass: the token plus the marker (PathMerge.fire)
 #pragma unroll
-    for (int f = 0; f < kCMF; ++f) {
-      if (path[f] != 1) continue;   // uniform within the lane group
-      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      for (int k = 0; k < N; ++k) out[f][k * N + j] = __fadd_rn(c[f][k], a.marker);
+    } else if (path[f] == 1) {
+      for (int l = 0; l < a.layers; ++l) {
+        const float* wl = w + l * N * N;
+        float y[N];
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        const float wk = wl[k];
-        acc[0] = __fadd_rn(acc[0], __fmul_rn(wk, col[f][k].x));
-        acc[1] = __fadd_rn(acc[1], __fmul_rn(wk, col[f][k].y));
-        acc[2] = __fadd_rn(acc[2], __fmul_rn(wk, col[f][k].z));
-        acc[3] = __fadd_rn(acc[3], __fmul_rn(wk, col[f][k].w));
-      }
-      if (l + 1 == a.layers) {
-        reinterpret_cast<float4*>(out[f])[sub] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      } else {
+        for (int i = 0; i < N; ++i) {
+          float acc = 0.0f;
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-          const int src = leader + 2 * k + cb;
-          col[f][k].x = __shfl_sync(grp, acc[0], src);
-          col[f][k].y = __shfl_sync(grp, acc[1], src);
-          col[f][k].z = __shfl_sync(grp, acc[2], src);
-          col[f][k].w = __shfl_sync(grp, acc[3], src);
+          for (int k = 0; k < N; ++k) acc = __fadd_rn(acc, __fmul_rn(wl[i * N + k], c[f][k]));
+          y[i] = acc;
         }
+#pragma unroll
+        for (int i = 0; i < N; ++i) c[f][i] = y[i];
       }
+#pragma unroll
+      for (int k = 0; k < N; ++k) out[f][k * N + j] = c[f][k];
     }
   }
 }
@@ -463,7 +436,7 @@ int pb_fire_matmul_chain(pb_matmul_chain_actor actor, pb_resolved res, void* str
   if (res.n_iter == 0) return PB_OK;
   if (actor.n != 8 || actor.layers < 1 || actor.layers > kChainMax)
     return pb::fail(PB_E_UNSUPPORTED, "matmul chain: N = 8 and 1..8 layers");
-  const int per_cta = 8 * 2 * kCMF;
+  const int per_cta = 8 * 4 * kCMF;
   dim3 grid((unsigned)((res.n_iter + per_cta - 1) / per_cta), res.n_streams);
   matmul_chain_kernel<<<grid, 256, 0, pb::as_stream(stream)>>>(actor, res);
   PB_LAUNCHED("matmul_chain_kernel");
@@ -474,7 +447,7 @@ int pb_fire_bypass_region(pb_bypass_region r, pb_resolved res, void* stream) {
   if (res.n_iter == 0) return PB_OK;
   if (r.layers < 1 || r.layers > kChainMax)
     return pb::fail(PB_E_UNSUPPORTED, "bypass region: 1..8 matmul layers");
-  const int per_cta = 8 * 2 * kCMF;
+  const int per_cta = 8 * 4 * kBMF;
   dim3 grid((unsigned)((res.n_iter + per_cta - 1) / per_cta), res.n_streams);
   bypass_region_kernel<<<grid, 256, 0, pb::as_stream(stream)>>>(r, res);
   PB_LAUNCHED("bypass_region_kernel");
