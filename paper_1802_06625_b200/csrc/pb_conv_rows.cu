@@ -63,6 +63,18 @@ constexpr int kCoutR = 32;
 constexpr int kUnitsThreads = 1024;
 constexpr int kDeclined = 1;   // fire_conv_rows: shape not handled here (nothing launched)
 
+// The epilogue's horizontal pool splits the 32 channels of a pooled pixel
+// between the lane pair (m, m ^ 1): lane `odd`'s i-th channel.  PB_EPI_SECTOR:
+// channels in runs of four alternating between the lanes, so the pair's q-th
+// 16-byte stores are adjacent and fill one 32-byte sector; else halves 0-15 /
+// 16-31 (two half sectors 64 bytes apart per store).
+#ifndef PB_EPI_SECTOR
+#define PB_EPI_SECTOR 1
+#endif
+__host__ __device__ constexpr int epi_channel(int i, bool odd) {
+  return PB_EPI_SECTOR ? (i / 4) * 8 + (odd ? 4 : 0) + (i % 4) : (odd ? 16 : 0) + i;
+}
+
 __device__ __forceinline__ uint32_t s_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -718,7 +730,7 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
     const bool odd = m & 1;
     float bias[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) bias[i] = B.bias[(odd ? 16 : 0) + i];
+    for (int i = 0; i < 16; ++i) bias[i] = B.bias[epi_channel(i, odd)];
     uint32_t pbase = 0, tnum = 0;
     for (int t = blockIdx.x; t < g.tiles; t += gridDim.x, pbase += n_pairs, ++tnum) {
       const LaneFrame f = lane_frame(g, list, t, m);
@@ -796,8 +808,13 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
         float res[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float lo_c = I8 ? r0[i] : fmaxf(r0[i], r1[i]);
-          const float hi_c = I8 ? r0[16 + i] : fmaxf(r0[16 + i], r1[16 + i]);
+          // channel sets: the even lane pools epi_channel(i, 0), the odd lane
+          // epi_channel(i, 1) (compile-time indices into r0 / r1)
+          constexpr int dummy = 0;
+          (void)dummy;
+          const int ca = epi_channel(i, false), cb = epi_channel(i, true);
+          const float lo_c = I8 ? r0[ca] : fmaxf(r0[ca], r1[ca]);
+          const float hi_c = I8 ? r0[cb] : fmaxf(r0[cb], r1[cb]);
           const float send = odd ? lo_c : hi_c;
           const float keep = odd ? hi_c : lo_c;
           const float other = __shfl_xor_sync(0xffffffffu, send, 1);
@@ -808,11 +825,14 @@ conv_rows_kernel(pb_conv_actor a, const LiveSpan* __restrict__ list,
           for (int i = 0; i < 16; ++i) fmax_out = fmaxf(fmax_out, fabsf(res[i]));
         }
         if (f.valid && !(a.debug & 2)) {
+          // PB_EPI_SECTOR: store q writes channels epi_channel(4q .. 4q+3): the
+          // lane pair fills one whole 32-byte sector of the pixel per store
           float4* dst = reinterpret_cast<float4*>(
-              f.out + ((int64_t)pr * (g.Wo >> 1) + (f.xo >> 1)) * kCoutR + (odd ? 16 : 0));
+              f.out + ((int64_t)pr * (g.Wo >> 1) + (f.xo >> 1)) * kCoutR);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            dst[i] = make_float4(res[4 * i], res[4 * i + 1], res[4 * i + 2], res[4 * i + 3]);
+            dst[epi_channel(4 * i, odd) / 4] =
+                make_float4(res[4 * i], res[4 * i + 1], res[4 * i + 2], res[4 * i + 3]);
         }
         w3.stop();
       }
