@@ -1116,7 +1116,10 @@ constexpr int kDAPiece = 128 * kDKC * 2;            // 16 KB (one precision piec
 constexpr int kDTmemCols = 256;
 constexpr int kDEpiWarps = 4, kDMmaWarp = 4;       // warps 0-3 epilogue, 4 MMA, 5-12 converters
 constexpr int kDEpiThreads = kDEpiWarps * 32;
-constexpr int kDCvtThreads = 256;
+#ifndef PB_DENSE_CVT
+#define PB_DENSE_CVT 512   // 256: 0.168 ms, 512: 0.163 ms per 6144 frames
+#endif
+constexpr int kDCvtThreads = PB_DENSE_CVT;   // converter threads (frame loads in flight)
 constexpr int kDItems = 512 / kDCvtThreads;        // (row, 16-K quarter) items per thread per chunk
 constexpr int kDThreads = (kDEpiWarps + 1) * 32 + kDCvtThreads;
 
