@@ -143,3 +143,49 @@ def test_host_actor_exception_is_actor_panic(golden):
         run(case["description"], behaviors={"s2": Boom()},
             config=RuntimeConfig(source_firings=4))
     assert e.value.actor == "s2"
+
+
+def test_overrides_keep_fused_regions_apart(golden, tmp_path):
+    """A Python override (here observers: device-behaviour subclasses whose fire
+    sees the device result) of a member of a fused region -- the bypass app's
+    l2, the motion app's clean -- keeps that region's channels materialised
+    (per-actor launches) and the reference's outputs unchanged; the observers
+    see every firing."""
+    from paper_1802_06625_b200.apps import bypass, motion
+    from paper_1802_06625_b200.behaviors import MatMul, PlusMedian
+    from paper_1802_06625_b200.engine import DeviceRuntime
+
+    class SeenMM(MatMul):
+        def __init__(self):
+            self.n = 0
+
+        def fire(self, ctx):
+            self.n += 1
+
+    class SeenMedian(PlusMedian):
+        def __init__(self):
+            self.n = 0
+
+        def fire(self, ctx):
+            self.n += 1
+
+    arr = golden["bypass_small"]
+    p = tmp_path / "input.bin"
+    p.write_bytes(arr["input"].tobytes())
+    obs = SeenMM()
+    desc = bypass.build_description(str(p))
+    cfg = RuntimeConfig(source_firings=32, seed=5, capture_sinks=True)
+    rep = run(desc, behaviors={"l2": obs}, config=cfg)
+    assert rep.sink_data["sink"] == arr["sink"].tobytes()
+    assert obs.n == rep.firing_counts["l2"] == golden["bypass"]["default"]["firing_counts"]["l2"]
+    rt = DeviceRuntime(desc, behaviors={"l2": SeenMM()}, config=cfg, n_streams=1, seeds=[5])
+    assert "bypass_region" not in [item[0] for item in rt.launches]
+    rt.close()
+
+    mp = tmp_path / "motion.bin"
+    mp.write_bytes(motion.make_input(7, 16))
+    mobs = SeenMedian()
+    rep = run(motion.build_description(input_path=str(mp)), behaviors={"clean": mobs},
+              config=RuntimeConfig(source_firings=16, seed=7, capture_sinks=True, epoch=5))
+    assert rep.sink_data["sink"] == golden["motion_small"]["sink_16_7"].tobytes()
+    assert mobs.n == 16
