@@ -130,6 +130,18 @@ __device__ __forceinline__ uint32_t med5(uint32_t a, uint32_t b, uint32_t c, uin
 #endif
 }
 
+// The median of five values that are each 0x00 or 0xFF is their majority, and
+// for such bytes the bitwise majority of the five words is the per-byte one:
+// the fused motion region's median runs on the threshold mask, which is only
+// ever 0 or 255 per pixel (frame_diff_threshold), so it takes the med5 network
+// with min = AND and max = OR (a handful of LOP3s per 4 pixels).
+__device__ __forceinline__ uint32_t maj5(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                         uint32_t e) {
+  const uint32_t f = (a & b) | (c & d);   // max(min(a, b), min(c, d))
+  const uint32_t g = (a | b) & (c | d);   // min(max(a, b), max(c, d))
+  return (e & f) | ((e | f) & g);         // med3(e, f, g) with f <= g
+}
+
 // frames per CTA: the span addressing of each frame (ring index arithmetic)
 // is done once per frame by one thread and shared, not by every thread
 constexpr int kFPC = 4;
@@ -288,6 +300,9 @@ image_fast_kernel(pb_image_actor a, pb_resolved res) {
 #define PB_MRF 16
 #endif
 constexpr int kMRF = PB_MRF;   // frames per CTA (one extra blur per run)
+#ifndef PB_MR_MAJ   // the region's median on the 0/255 mask as a bitwise majority
+#define PB_MR_MAJ 1
+#endif
 #ifndef PB_MR_REG
 #define PB_MR_REG 1   // sides 32 / 64: the register form below
 #endif
@@ -397,7 +412,7 @@ motion_region_kernel(pb_motion_region r, pb_resolved res) {
         const uint32_t pl = xw > 0 ? mk[y * W + xw - 1] : 0u;
         const uint32_t nx = xw < W - 1 ? mk[y * W + xw + 1] : 0u;
         const uint32_t lf = __byte_perm(pl, cw, 0x6543), rt = __byte_perm(cw, nx, 0x4321);
-        word = med5(cw, up, dn, lf, rt);
+        word = PB_MR_MAJ ? maj5(cw, up, dn, lf, rt) : med5(cw, up, dn, lf, rt);
         if (xw == 0) word = __byte_perm(word, cw, 0x3214);
         if (xw == W - 1) word = __byte_perm(word, cw, 0x7210);
       }
@@ -520,7 +535,7 @@ motion_region_reg_kernel(pb_motion_region r, pb_resolved res) {
         if (xw == 0) pl = 0u;
         if (xw == W - 1) nx = 0u;
         const uint32_t lf = __byte_perm(pl, cw, 0x6543), rt = __byte_perm(cw, nx, 0x4321);
-        word = med5(cw, up, dn, lf, rt);
+        word = PB_MR_MAJ ? maj5(cw, up, dn, lf, rt) : med5(cw, up, dn, lf, rt);
         if (xw == 0) word = __byte_perm(word, cw, 0x3214);
         if (xw == W - 1) word = __byte_perm(word, cw, 0x7210);
       }
