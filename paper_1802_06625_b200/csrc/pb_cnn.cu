@@ -1109,7 +1109,11 @@ int launch_conv(const pb_conv_actor& actor, const pb_resolved& res, cudaStream_t
 #endif
 constexpr int kDN = 112;                    // padded outputs per precision half
 constexpr int kDKC = 64;                    // K per pipeline chunk (4 K16 steps)
-constexpr int kDStages = 3;
+#ifndef PB_DENSE_CPASYNC   // 1: frame chunks into a 3-deep shared-memory ring by cp.async
+#define PB_DENSE_CPASYNC 0   // measured 0.201 vs 0.162 ms (the A / weight ring drops to 2 stages)
+#endif
+constexpr int kDStages = PB_DENSE_CPASYNC ? 2 : 3;   // A / weight ring
+constexpr int kDRaw = 3;                             // raw frame chunks in flight (cp.async)
 constexpr int kDStepBytes = 2 * kDN * 16 * 2;       // [wh; wl] 224 rows x 16 bf16
 constexpr int kDChunkBytes = 4 * kDStepBytes;       // 28 KB
 constexpr int kDAPiece = 128 * kDKC * 2;            // 16 KB (one precision piece)
@@ -1126,6 +1130,9 @@ constexpr int kDThreads = (kDEpiWarps + 1) * 32 + kDCvtThreads;
 struct DenseSmem {
   uint8_t a[kDStages][2][kDAPiece];        // K-major core layout [row/8][kb][row%8][16 B]
   uint8_t b[kDStages][kDChunkBytes];
+#if PB_DENSE_CPASYNC
+  uint8_t raw[kDRaw][kDCvtThreads * 64];   // each converter thread's 16 floats of a chunk
+#endif
   uint64_t full[kDStages], empty[kDStages], acc_full;
   uint32_t tmem_base;
   int last;
@@ -1219,18 +1226,48 @@ dense_kernel(pb_dense_actor a, pb_resolved res, float* partial, int* counters, i
           asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + (int64_t)c * kDKC + 16 * q));
       }
     };
+#if PB_DENSE_CPASYNC
+    static_assert(kDItems == 1, "cp.async ring: one item per converter thread");
+    // this thread's 64 bytes of chunk c into raw slot `slot` (zero rows of
+    // frames beyond the launch); one commit group per chunk, empty ones too
+    auto issue = [&](int c, int slot) {
+      if (c < c1) {
+        const int r = ct >> 2, q = ct & 3;
+        const float* rp = S.rowp[r];
+        const float* src = rp != nullptr ? rp + (int64_t)c * kDKC + 16 * q : a.bias;
+        const uint32_t dst = smem_u32(S.raw[slot] + ct * 64);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + 16 * u),
+                       "l"(src + 4 * u), "r"(rp != nullptr ? 16 : 0)
+                       : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue(c0, 0);
+    issue(c0 + 1, 1);
+#else
     if (c0 < c1) load_chunk(c0);
     if (c0 + 1 < c1) prefetch_chunk(c0 + 1);
+#endif
     for (int c = c0, it = 0; c < c1; ++c, ++it) {
       const int st = it % kDStages;
       const uint32_t use = (uint32_t)(it / kDStages);
       float4 cur[kDItems][4];
+#if PB_DENSE_CPASYNC
+      issue(c + 2, (it + 2) % kDRaw);
+      asm volatile("cp.async.wait_group 2;" ::: "memory");   // chunk c has landed
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        cur[0][u] = *reinterpret_cast<const float4*>(S.raw[it % kDRaw] + ct * 64 + 16 * u);
+#else
 #pragma unroll
       for (int k = 0; k < kDItems; ++k)
 #pragma unroll
         for (int u = 0; u < 4; ++u) cur[k][u] = nxt[k][u];
       if (c + 2 < c1) prefetch_chunk(c + 2);
       if (c + 1 < c1) load_chunk(c + 1);
+#endif
       mbar_wait(&S.empty[st], (use & 1) ^ 1);
       if (ct == 0) {
         mbar_arrive_tx(&S.full[st], kDChunkBytes);
